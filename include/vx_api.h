@@ -1,0 +1,116 @@
+/*
+ * vx_api.h — C ABI of the B200-native dense-view VGGT inference kernels.
+ *
+ * The reference (VGGT-X, arXiv 2509.25191) ships no operator/plugin/FFI
+ * interface for this path: the hot path is described
+ * only in PAPER.md:76-81 and the upstream `vggt` PyTorch modules.  Each entry
+ * point below replaces one upstream PyTorch op of that path (SURVEY.md §8a
+ * rows a1-a16, named in the comment); the Python host layer
+ * (paper_2509_25191_b200/ops.py) binds them with ctypes, and INTEGRATION.md
+ * shows the binding a `vggt` maintainer would add.
+ *
+ * Conventions
+ *   - all tensors are device pointers owned by the caller (PyTorch caching
+ *     allocator); the library never frees caller memory;
+ *   - bf16 = __nv_bfloat16 storage, fp32 = float;
+ *   - every call is asynchronous on `stream` (a cudaStream_t, may be NULL);
+ *   - return 0 on success, a negative VX_E* code otherwise; the message of the
+ *     last failure on the calling thread is available from vx_last_error().
+ *     No C++ exception crosses this boundary.
+ */
+#ifndef VX_API_H
+#define VX_API_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  VX_OK = 0,
+  VX_E_ARG = -1,         /* invalid argument / unsupported shape */
+  VX_E_CUDA = -2,        /* CUDA runtime / driver error */
+  VX_E_UNSUPPORTED = -3  /* device is not sm_100 */
+};
+
+/* GEMM epilogues (D = A[M,K] . B[N,K]^T accumulated in fp32 TMEM). */
+enum {
+  VX_EPI_BF16 = 0,   /* out bf16 [M, ldo]   = D + bias                       (Linear)            */
+  VX_EPI_GELU = 1,   /* out bf16 [M, ldo]   = gelu_erf(D + bias)             (Mlp.fc1 + GELU, a10) */
+  VX_EPI_RESID = 2,  /* resid fp32 [M, ldr] += gamma * (D + bias); optional
+                        kept bf16 [M, ldk] = new resid                       (proj/fc2 + LayerScale
+                                                                              + residual, a9/a10/a11) */
+  VX_EPI_QKV = 3,    /* qkv Linear + q/k LayerNorm(head_dim) + 2D RoPE, scattered
+                        to q/k/v bf16 [H, T, head_dim]                       (Attention.qkv/q_norm/
+                                                                              k_norm/rope, a4/a6)  */
+  VX_EPI_PATCH = 4,  /* patch-embed: resid fp32 row (f*tpf + ps + p) = D + bias (PatchEmbed, a2)    */
+  VX_EPI_F32 = 5     /* out fp32 [M, ldo]   = D + bias                                              */
+};
+
+typedef struct vx_epilogue {
+  const float* bias;          /* [N] or NULL */
+  void* out;                  /* VX_EPI_BF16/GELU/F32 output, row stride ldo elements */
+  int64_t ldo;
+  float* resid;               /* VX_EPI_RESID / VX_EPI_PATCH fp32 residual stream, stride ldr */
+  int64_t ldr;
+  const float* gamma;         /* VX_EPI_RESID LayerScale [N] */
+  void* kept;                 /* VX_EPI_RESID optional bf16 copy of the new residual, stride ldk */
+  int64_t ldk;
+  void* q;                    /* VX_EPI_QKV outputs, each bf16 [H, T, head_dim] */
+  void* k;
+  void* v;
+  const float* qn_w;          /* q_norm / k_norm affine [head_dim]; NULL disables qk-norm */
+  const float* qn_b;
+  const float* kn_w;
+  const float* kn_b;
+  const float* rope_cos;      /* [max_pos, head_dim/4] fp32; NULL disables RoPE */
+  const float* rope_sin;
+  int embed_dim;              /* C (=H*head_dim) */
+  int head_dim;               /* 32 or 64 */
+  int tokens_total;           /* T = rows of q/k/v per head */
+  int tokens_per_frame;       /* tokens per view (RoPE positions, patch row remap) */
+  int patch_start;            /* 1 + registers */
+  int grid_w;                 /* patches per image row */
+  float eps;                  /* q/k LayerNorm eps */
+} vx_epilogue;
+
+/* D[M,N] = A[M,K] (bf16, row stride lda) . B[N,K]^T (bf16, row stride ldb) with
+ * epilogue `epi`.  K % 64 == 0, N % 32 == 0. tcgen05/TMEM/TMA persistent kernel. */
+int vx_gemm(int epi, const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N, int K,
+            const vx_epilogue* ep, void* stream);
+
+/* Flash attention (non-causal, no dropout) — replaces F.scaled_dot_product_attention in
+ * Attention.forward for frame blocks (nseq = frames) and global blocks (nseq = 1) (a7/a8).
+ *   q: bf16 [H, Tq, D]; k, v: bf16 [H, Tk, D]; sequence s of head h uses rows
+ *   h*Tq + s*Lq .. +Lq (q) and h*Tk + s*Lk .. +Lk (k, v).
+ *   out: bf16, row (s*Lq + i), columns h*D .. h*D+D-1, row stride ldo.
+ *   lse: optional fp32 [H, Tq] natural-log log-sum-exp of the scaled scores.
+ * D in {32, 64}; scale = 1/sqrt(D). */
+int vx_attention(const void* q, const void* k, const void* v, void* out, int64_t ldo, float* lse,
+                 int D, int H, int nseq, int Lq, int Lk, int64_t Tq, int64_t Tk, void* stream);
+
+/* LayerNorm over the last dim (cols): y = (x - mean) * rstd * w + b.
+ * x_dtype / y_dtype: 0 = fp32, 1 = bf16.  w/b may be NULL (no affine). (norm1/norm2, a5) */
+int vx_layernorm(const void* x, int x_dtype, int64_t ldx, void* y, int y_dtype, int64_t ldy,
+                 const float* w, const float* b, int rows, int cols, float eps, void* stream);
+
+/* ResNet-normalise + im2col of (S,3,H,W) fp32 images into bf16 [S*P, Kpad] with
+ * K order (c, ky, kx) and zero padding K..Kpad-1.  (Aggregator normalize + PatchEmbed, a1/a2) */
+int vx_patchify(const float* images, void* out, int S, int H, int W, int patch, int Kpad,
+                void* stream);
+
+/* Write camera (1) and register (R) tokens into the fp32 residual stream:
+ * x[f*tpf + t] = (f == 0 ? tok[0] : tok[1])[t] for t < 1+R.  tokens: fp32 [2, 1+R, C]
+ * (slice_expand_and_flatten + cat, a3) */
+int vx_special_tokens(float* x, const float* tokens, int S, int tpf, int ntok, int C, void* stream);
+
+int vx_num_sms(void);
+const char* vx_last_error(void);
+const char* vx_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VX_API_H */

@@ -1,0 +1,168 @@
+"""Host orchestration of the VGGT Aggregator on the sm_100a kernels.
+
+Upstream call stack replaced:
+  Aggregator.forward -> normalize, patch_embed, special tokens, positions,
+  24 x (frame_blocks[i], global_blocks[i]), output_list.
+VGGT-X changes made native (`PAPER.md:79-81,146`):
+  * only the kept layers {4, 11, 17, 23} are materialised; the fc2 residual
+    epilogue of the frame / global block writes the bf16 copy straight into
+    the kept buffer's left / right half (no intermediate cache, no concat);
+  * bf16 GEMM / attention operands, fp32 inter-block residual stream
+    (SURVEY.md §7 "Parity under bf16" design rule);
+  * the frame-wise MLP is evaluated `frame_chunk` frames at a time so the
+    4C-wide hidden activation never exists for all views at once.
+
+HBM layout (T = S * tokens_per_frame rows, frame-major):
+  x      fp32 [T, C]        residual stream
+  xn     bf16 [T, C]        LayerNorm output (GEMM A operand)
+  q,k,v  bf16 [H, T, d]     head-major: frame attention reads rows f*N..f*N+N-1
+                            of each head, global attention all T rows
+  o      bf16 [T, C]        attention output (proj A operand)
+  h      bf16 [chunk*N, 4C] MLP hidden (per frame chunk)
+  kept   bf16 [S, N, 2C]    per kept layer: [frame_out | global_out]
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable, Dict, Optional
+
+import torch
+
+from . import ops
+from .config import VGGTConfig
+from .weights import is_bf16_param
+
+
+def rope_tables(head_dim: int, max_pos: int, freq: float):
+    """cos/sin of pos * freq^(-2i/(d/2)), i < d/4, fp32 — one quarter of the head
+    (the oracle's cat(angles, angles) duplicates it).  (max_pos, d/4) each."""
+    half = head_dim // 2
+    exponents = torch.arange(0, half, 2, dtype=torch.float32) / half
+    inv_freq = 1.0 / (freq ** exponents)
+    ang = torch.arange(max_pos, dtype=torch.float32)[:, None] * inv_freq[None, :]
+    return ang.cos().contiguous(), ang.sin().contiguous()
+
+
+class DeviceWeights:
+    """Device copies of the state dict: bf16 matrix weights, fp32 everything else."""
+
+    def __init__(self, sd: Dict[str, torch.Tensor], cfg: VGGTConfig, device="cuda"):
+        self.cfg = cfg
+        self.t: Dict[str, torch.Tensor] = {}
+        for name, v in sd.items():
+            dt = torch.bfloat16 if is_bf16_param(name, tuple(v.shape)) else torch.float32
+            self.t[name] = v.to(device=device, dtype=dt).contiguous()
+        a = "aggregator."
+        C = cfg.embed_dim
+        pw = sd[a + "patch_embed.proj.weight"].reshape(C, -1)
+        pad = torch.zeros(C, cfg.patch_k_padded)
+        pad[:, : cfg.patch_k] = pw
+        self.patch_w = pad.to(device=device, dtype=torch.bfloat16)
+        self.special = torch.cat([sd[a + "camera_token"][0], sd[a + "register_token"][0]], dim=1).to(
+            device=device, dtype=torch.float32).contiguous()  # (2, 1+R, C)
+        cos, sin = rope_tables(cfg.head_dim, cfg.grid + 1, cfg.rope_freq)
+        self.rope = (cos.to(device), sin.to(device))
+
+    def __getitem__(self, k):
+        return self.t[k]
+
+
+@dataclass
+class Workspace:
+    x: torch.Tensor
+    xn: torch.Tensor
+    q: torch.Tensor
+    k: torch.Tensor
+    v: torch.Tensor
+    o: torch.Tensor
+    h: torch.Tensor
+
+
+def alloc_workspace(cfg: VGGTConfig, S: int, device="cuda") -> Workspace:
+    T = S * cfg.tokens_per_frame
+    C, H, d = cfg.embed_dim, cfg.num_heads, cfg.head_dim
+    chunk_rows = min(S, cfg.frame_chunk) * cfg.tokens_per_frame
+    return Workspace(
+        x=torch.empty(T, C, device=device, dtype=torch.float32),
+        xn=torch.empty(T, C, device=device, dtype=torch.bfloat16),
+        q=torch.empty(H, T, d, device=device, dtype=torch.bfloat16),
+        k=torch.empty(H, T, d, device=device, dtype=torch.bfloat16),
+        v=torch.empty(H, T, d, device=device, dtype=torch.bfloat16),
+        o=torch.empty(T, C, device=device, dtype=torch.bfloat16),
+        h=torch.empty(chunk_rows, cfg.mlp_hidden, device=device, dtype=torch.bfloat16),
+    )
+
+
+# attention hook: (q, k, v, o, nseq, L) for a global block; the multi-GPU path
+# replaces it with the frame-sharded ring (ring.py)
+GlobalAttnFn = Callable[[torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor], None]
+
+
+def run_block(W: DeviceWeights, name: str, ws: Workspace, S: int, frame_attn: bool,
+              kept_half: Optional[torch.Tensor], global_attn: Optional[GlobalAttnFn] = None):
+    """One pre-norm VGGT Block on the whole residual stream."""
+    cfg = W.cfg
+    N = cfg.tokens_per_frame
+    T = S * N
+    C = cfg.embed_dim
+    ops.layernorm(ws.x, W[name + ".norm1.weight"], W[name + ".norm1.bias"], cfg.ln_eps, out=ws.xn)
+    ops.gemm(ws.xn, W[name + ".attn.qkv.weight"], ops.EPI_QKV, bias=W[name + ".attn.qkv.bias"],
+             qkv=(ws.q, ws.k, ws.v),
+             qk_norm=(W[name + ".attn.q_norm.weight"], W[name + ".attn.q_norm.bias"],
+                      W[name + ".attn.k_norm.weight"], W[name + ".attn.k_norm.bias"]),
+             rope=W.rope, head_dim=cfg.head_dim, tokens_total=T, tokens_per_frame=N,
+             patch_start=cfg.patch_start_idx, grid_w=cfg.grid, eps=cfg.ln_eps)
+    if frame_attn:
+        ops.attention(ws.q, ws.k, ws.v, ws.o, nseq=S, Lq=N, Lk=N)
+    elif global_attn is not None:
+        global_attn(ws.q, ws.k, ws.v, ws.o)
+    else:
+        ops.attention(ws.q, ws.k, ws.v, ws.o, nseq=1, Lq=T, Lk=T)
+    ops.gemm(ws.o, W[name + ".attn.proj.weight"], ops.EPI_RESID, bias=W[name + ".attn.proj.bias"],
+             resid=ws.x, gamma=W[name + ".ls1.gamma"])
+    ops.layernorm(ws.x, W[name + ".norm2.weight"], W[name + ".norm2.bias"], cfg.ln_eps, out=ws.xn)
+    rows = ws.h.shape[0]
+    for r0 in range(0, T, rows):
+        r1 = min(T, r0 + rows)
+        hb = ws.h[: r1 - r0]
+        ops.gemm(ws.xn[r0:r1], W[name + ".mlp.fc1.weight"], ops.EPI_GELU, bias=W[name + ".mlp.fc1.bias"],
+                 out=hb)
+        ops.gemm(hb, W[name + ".mlp.fc2.weight"], ops.EPI_RESID, bias=W[name + ".mlp.fc2.bias"],
+                 resid=ws.x[r0:r1], gamma=W[name + ".ls2.gamma"],
+                 kept=None if kept_half is None else kept_half[r0:r1])
+
+
+def embed(W: DeviceWeights, images: torch.Tensor, ws: Workspace, frame0_is_first: bool = True):
+    """a1-a3: special tokens + ResNet-normalised conv patch-embed into the fp32 stream."""
+    cfg = W.cfg
+    S = images.shape[0]
+    N = cfg.tokens_per_frame
+    special = W.special
+    if not frame0_is_first:  # a shard that does not own global frame 0 uses the "other" tokens
+        special = special[1:2].expand(2, -1, -1).contiguous()
+    ops.special_tokens(ws.x, special, S, N)
+    a = ops.patchify(images, cfg.patch_size, cfg.patch_k_padded)
+    ops.gemm(a, W.patch_w, ops.EPI_PATCH, bias=W["aggregator.patch_embed.proj.bias"], resid=ws.x,
+             tokens_per_frame=N, patch_start=cfg.patch_start_idx)
+
+
+def aggregator_forward(W: DeviceWeights, images: torch.Tensor, ws: Optional[Workspace] = None,
+                       global_attn: Optional[GlobalAttnFn] = None, frame0_is_first: bool = True
+                       ) -> Dict[int, torch.Tensor]:
+    """images (S,3,H,W) fp32 on device -> {layer: (S, N, 2C) bf16} for cfg.kept_layers."""
+    cfg = W.cfg
+    S = images.shape[0]
+    N = cfg.tokens_per_frame
+    C = cfg.embed_dim
+    if images.shape[-1] != cfg.img_size or images.shape[-2] != cfg.img_size:
+        raise ValueError(f"images must be {cfg.img_size}x{cfg.img_size}, got {tuple(images.shape)}")
+    if ws is None:
+        ws = alloc_workspace(cfg, S, images.device)
+    embed(W, images.float().contiguous(), ws, frame0_is_first)
+    kept = {i: torch.empty(S * N, 2 * C, device=images.device, dtype=torch.bfloat16) for i in cfg.kept_layers}
+    for i in range(cfg.depth):
+        kb = kept.get(i)
+        run_block(W, f"aggregator.frame_blocks.{i}", ws, S, True, None if kb is None else kb[:, :C])
+        run_block(W, f"aggregator.global_blocks.{i}", ws, S, False, None if kb is None else kb[:, C:],
+                  global_attn=global_attn)
+    return {i: t.view(S, N, 2 * C) for i, t in kept.items()}

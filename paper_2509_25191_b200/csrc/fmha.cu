@@ -1,0 +1,363 @@
+// tcgen05/TMEM flash attention for VGGT frame and global attention (sm_100a).
+//
+// Replaces F.scaled_dot_product_attention in the upstream Attention.forward
+// (frame blocks, batch S*16 sequences of 1374 tokens; a8:
+// global blocks, 16 sequences of S*1374 tokens).  Non-causal, d in {32, 64}.
+//
+// One CTA = one work unit = 256 query rows (two 128-row Q tiles) of one
+// (head, sequence); persistent grid over units, head-major so concurrently
+// running CTAs share K/V through L2.
+//
+// Warp roles (384 threads):
+//   w0      TMA producer: Q tiles once per unit, K/V tiles through a KST-stage ring
+//   w1      tcgen05.mma issuer (one lane): S_i = Q_i K^T (SS), O_i += P_i V (TS, P in TMEM)
+//   w2      TMEM allocator (512 columns: S0 | S1 | O0 | O1, P_i aliases S_i)
+//   w4..w7  softmax + epilogue for Q tile 0, w8..w11 for Q tile 1
+//           (thread = one query row = one TMEM lane: row max / sum are thread-local;
+//            lazy O rescaling only when the running max grows by > 2^8)
+// MMA issue order per KV tile j:  PV_0(j), S_0(j+1), PV_1(j), S_1(j+1), so each
+// softmax warpgroup's exp work overlaps the other tile's tensor-core work.
+#include <math.h>
+
+#include "../../include/vx_api.h"
+#include "common.cuh"
+#include "host_util.h"
+
+namespace vx {
+
+struct AttnArgs {
+  int H, nseq, Lq, Lk;
+  int64_t Tq, Tk;
+  int q_blocks, kv_tiles, units;
+  float scale_log2;
+  __nv_bfloat16* out;
+  int64_t ldo;
+  float* lse;
+};
+
+template <int D>
+struct AttnCfg {
+  static constexpr int KST = 3;
+  static constexpr uint32_t ROW_BYTES = D * 2;
+  static constexpr uint32_t TILE_BYTES = 128 * ROW_BYTES;
+  static constexpr int SWIZZLE = D == 64 ? 128 : 64;
+  static constexpr uint32_t LAYOUT = D == 64 ? 2 : 4;  // SWIZZLE_128B / SWIZZLE_64B
+  static constexpr uint32_t SBO = 8 * ROW_BYTES;       // 8-row core-matrix group
+  static constexpr uint32_t SMEM = (2 + 2 * KST) * TILE_BYTES + 1024 + 512;
+};
+
+constexpr int ATTN_THREADS = 384;
+constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
+
+template <int D>
+__global__ void __launch_bounds__(ATTN_THREADS, 1)
+    fmha_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                const __grid_constant__ CUtensorMap tmV, const AttnArgs a) {
+  using Cfg = AttnCfg<D>;
+  constexpr int KST = Cfg::KST;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;                                 // 2 tiles
+  uint8_t* sK = sQ + 2 * Cfg::TILE_BYTES;             // KST tiles
+  uint8_t* sV = sK + KST * Cfg::TILE_BYTES;           // KST tiles
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sV + KST * Cfg::TILE_BYTES);
+  uint64_t* q_full = bar;
+  uint64_t* q_empty = bar + 1;
+  uint64_t* k_full = bar + 2;
+  uint64_t* k_empty = k_full + KST;
+  uint64_t* v_full = k_empty + KST;
+  uint64_t* v_empty = v_full + KST;
+  uint64_t* s_full = v_empty + KST;  // [2]
+  uint64_t* p_full = s_full + 2;     // [2]
+  uint64_t* o_full = p_full + 2;     // [2]
+  uint64_t* o_empty = o_full + 2;    // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+
+  if (warp == 0 && elect_one()) {
+    tma_prefetch_desc(&tmQ);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
+    for (int s = 0; s < KST; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 4);
+      mbar_init(&o_full[i], 1);
+      mbar_init(&o_empty[i], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const int per_head = a.nseq * a.q_blocks;
+  const int nkv = a.kv_tiles;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (elect_one()) {
+      const uint64_t pol_kv = policy_evict_last();
+      const uint64_t pol_q = policy_evict_first();
+      uint32_t c = 0;  // global K/V tile counter
+      uint32_t n = 0;  // local unit counter
+      for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++n) {
+        const int h = u / per_head;
+        const int rem = u - h * per_head;
+        const int s = rem / a.q_blocks;
+        const int qb = rem - s * a.q_blocks;
+        const int q_row = int(h * a.Tq + (int64_t)s * a.Lq + qb * 256);
+        const int kv_row = int(h * a.Tk + (int64_t)s * a.Lk);
+        mbar_wait(q_empty, (n & 1) ^ 1);
+        mbar_expect_tx(q_full, 2 * Cfg::TILE_BYTES);
+        tma_load_2d_hint(sQ, &tmQ, q_full, 0, q_row, pol_q);
+        tma_load_2d_hint(sQ + Cfg::TILE_BYTES, &tmQ, q_full, 0, q_row + 128, pol_q);
+        for (int j = 0; j < nkv; ++j, ++c) {
+          const uint32_t st = c % KST, ph = (c / KST) & 1;
+          mbar_wait(&k_empty[st], ph ^ 1);
+          mbar_expect_tx(&k_full[st], Cfg::TILE_BYTES);
+          tma_load_2d_hint(sK + st * Cfg::TILE_BYTES, &tmK, &k_full[st], 0, kv_row + 128 * j, pol_kv);
+          mbar_wait(&v_empty[st], ph ^ 1);
+          mbar_expect_tx(&v_full[st], Cfg::TILE_BYTES);
+          tma_load_2d_hint(sV + st * Cfg::TILE_BYTES, &tmV, &v_full[st], 0, kv_row + 128 * j, pol_kv);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (elect_one()) {
+      constexpr uint32_t idesc_qk = make_idesc_bf16(128, 128, 0, 0);
+      constexpr uint32_t idesc_pv = make_idesc_bf16(128, D, 0, 1);
+      const uint32_t q0 = smem_u32(sQ), q1 = q0 + Cfg::TILE_BYTES;
+      auto issue_qk = [&](uint32_t d_tmem, uint32_t qs, uint32_t ks) {
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k)
+          mma_ss(d_tmem, make_sdesc(qs + k * 32, 16, Cfg::SBO, Cfg::LAYOUT),
+                 make_sdesc(ks + k * 32, 16, Cfg::SBO, Cfg::LAYOUT), idesc_qk, k > 0);
+      };
+      auto issue_pv = [&](uint32_t d_tmem, uint32_t p_tmem, uint32_t vs, uint32_t acc) {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          mma_ts(d_tmem, p_tmem + kk * 8, make_sdesc(vs + kk * 16 * Cfg::ROW_BYTES, 16, Cfg::SBO, Cfg::LAYOUT),
+                 idesc_pv, (acc | kk) != 0);
+      };
+      const uint32_t S0 = tmem, S1 = tmem + 128, O0 = tmem + 256, O1 = tmem + 384;
+      uint32_t c = 0;
+      uint32_t n = 0;
+      uint32_t pph0 = 0, pph1 = 0;
+      for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++n) {
+        mbar_wait(q_full, n & 1);
+        tc_fence_after();
+        {
+          const uint32_t st = c % KST, ph = (c / KST) & 1;
+          mbar_wait(&k_full[st], ph);
+          tc_fence_after();
+          const uint32_t ks = smem_u32(sK + st * Cfg::TILE_BYTES);
+          issue_qk(S0, q0, ks);
+          mma_commit(&s_full[0]);
+          issue_qk(S1, q1, ks);
+          mma_commit(&s_full[1]);
+          mma_commit(&k_empty[st]);
+          if (nkv == 1) mma_commit(q_empty);
+        }
+        for (int j = 0; j < nkv; ++j, ++c) {
+          const uint32_t st = c % KST, ph = (c / KST) & 1;
+          const uint32_t vs = smem_u32(sV + st * Cfg::TILE_BYTES);
+          const bool has_next = j + 1 < nkv;
+          const uint32_t nst = (c + 1) % KST, nph = ((c + 1) / KST) & 1;
+          const uint32_t nks = smem_u32(sK + nst * Cfg::TILE_BYTES);
+          mbar_wait(&v_full[st], ph);
+          // ---- tile 0
+          if (j == 0) mbar_wait(&o_empty[0], (n & 1) ^ 1);
+          mbar_wait(&p_full[0], pph0);
+          pph0 ^= 1;
+          tc_fence_after();
+          issue_pv(O0, S0, vs, j > 0);
+          if (!has_next) mma_commit(&o_full[0]);
+          if (has_next) {
+            mbar_wait(&k_full[nst], nph);
+            tc_fence_after();
+            issue_qk(S0, q0, nks);
+            mma_commit(&s_full[0]);
+          }
+          // ---- tile 1
+          if (j == 0) mbar_wait(&o_empty[1], (n & 1) ^ 1);
+          mbar_wait(&p_full[1], pph1);
+          pph1 ^= 1;
+          tc_fence_after();
+          issue_pv(O1, S1, vs, j > 0);
+          mma_commit(&v_empty[st]);
+          if (!has_next) mma_commit(&o_full[1]);
+          if (has_next) {
+            issue_qk(S1, q1, nks);
+            mma_commit(&s_full[1]);
+            mma_commit(&k_empty[nst]);
+            if (j + 2 == nkv) mma_commit(q_empty);
+          }
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ softmax / epilogue
+    const int tile = (warp - 4) / 4;  // Q tile handled by this warpgroup
+    const int wl = warp & 3;          // TMEM lane quarter
+    const int r = wl * 32 + lane;     // row within the Q tile
+    const uint32_t lane_off = uint32_t(wl * 32) << 16;
+    const uint32_t S_addr = tmem + lane_off + tile * 128;
+    const uint32_t O_addr = tmem + lane_off + 256 + tile * 128;
+    const float sl2 = a.scale_log2;
+    uint32_t sph = 0, oph = 0;
+    for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
+      const int h = u / per_head;
+      const int rem = u - h * per_head;
+      const int s = rem / a.q_blocks;
+      const int qb = rem - s * a.q_blocks;
+      const int q_local = qb * 256 + tile * 128 + r;
+      float m_run = -INFINITY, l_run = 0.f;
+      for (int j = 0; j < nkv; ++j) {
+        mbar_wait(&s_full[tile], sph);
+        sph ^= 1;
+        tc_fence_after();
+        uint32_t sr[128];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tmem_ld32(S_addr + 32 * c, sr + 32 * c);
+        tmem_wait_ld();
+        const int valid = a.Lk - 128 * j;
+        if (valid < 128) {
+#pragma unroll
+          for (int c = 0; c < 128; ++c)
+            if (c >= valid) sr[c] = 0xff800000u;  // -inf
+        }
+        float mx = __uint_as_float(sr[0]);
+#pragma unroll
+        for (int c = 1; c < 128; ++c) mx = fmaxf(mx, __uint_as_float(sr[c]));
+        const float m_new = mx * sl2;
+        const bool need = m_new > m_run + RESCALE_THRESHOLD;
+        const float alpha = need ? ex2(m_run - m_new) : 1.0f;
+        if (need) m_run = m_new;
+        float sum = 0.f;
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          uint32_t pk[32];
+#pragma unroll
+          for (int c = 0; c < 32; ++c) {
+            const float p0 = ex2(fmaf(__uint_as_float(sr[64 * half + 2 * c]), sl2, -m_run));
+            const float p1 = ex2(fmaf(__uint_as_float(sr[64 * half + 2 * c + 1]), sl2, -m_run));
+            sum += p0 + p1;
+            pk[c] = pack_bf16(p0, p1);
+          }
+          tmem_st32(S_addr + 32 * half, pk);
+        }
+        // lazy O correction (warp-uniform: tcgen05.ld/st are .sync.aligned); PV(j-1) has
+        // completed because s_full(j) was committed after it.
+        if (__any_sync(0xffffffff, need) && j > 0) {
+#pragma unroll
+          for (int c0 = 0; c0 < D; c0 += 32) {
+            uint32_t orr[32];
+            tmem_ld32(O_addr + c0, orr);
+            tmem_wait_ld();
+#pragma unroll
+            for (int c = 0; c < 32; ++c) orr[c] = __float_as_uint(__uint_as_float(orr[c]) * alpha);
+            tmem_st32(O_addr + c0, orr);
+          }
+        }
+        l_run = l_run * alpha + sum;
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[tile]);
+      }
+      // ---- epilogue: O / l -> bf16
+      mbar_wait(&o_full[tile], oph);
+      oph ^= 1;
+      tc_fence_after();
+      uint32_t orr[D];
+#pragma unroll
+      for (int c0 = 0; c0 < D; c0 += 32) tmem_ld32(O_addr + c0, orr + c0);
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&o_empty[tile]);
+      if (q_local < a.Lq) {
+        const float inv = 1.0f / l_run;
+        const int64_t orow = (int64_t)s * a.Lq + q_local;
+        uint4* dst = reinterpret_cast<uint4*>(a.out + orow * a.ldo + h * D);
+#pragma unroll
+        for (int c = 0; c < D / 8; ++c) {
+#define VX_O(i) (__uint_as_float(orr[8 * c + i]) * inv)
+          dst[c] = make_uint4(pack_bf16(VX_O(0), VX_O(1)), pack_bf16(VX_O(2), VX_O(3)),
+                              pack_bf16(VX_O(4), VX_O(5)), pack_bf16(VX_O(6), VX_O(7)));
+#undef VX_O
+        }
+        if (a.lse) a.lse[h * a.Tq + orow] = (m_run + __log2f(l_run)) * 0.69314718055994531f;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+template <int D>
+static int launch_fmha(const void* q, const void* k, const void* v, const AttnArgs& args, cudaStream_t st) {
+  using Cfg = AttnCfg<D>;
+  CUtensorMap tq, tk, tv;
+  if (!make_tmap_2d_bf16(&tq, q, (uint64_t)args.H * args.Tq, D, D, 128, D, Cfg::SWIZZLE)) return VX_E_ARG;
+  if (!make_tmap_2d_bf16(&tk, k, (uint64_t)args.H * args.Tk, D, D, 128, D, Cfg::SWIZZLE)) return VX_E_ARG;
+  if (!make_tmap_2d_bf16(&tv, v, (uint64_t)args.H * args.Tk, D, D, 128, D, Cfg::SWIZZLE)) return VX_E_ARG;
+  auto kern = fmha_kernel<D>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    if (e != cudaSuccess) return fail_cuda(e, "fmha: cudaFuncSetAttribute");
+    attr_set = true;
+  }
+  const int grid = args.units < num_sms() ? args.units : num_sms();
+  kern<<<grid, ATTN_THREADS, Cfg::SMEM, st>>>(tq, tk, tv, args);
+  VX_CHECK_LAUNCH("fmha launch");
+  return VX_OK;
+}
+
+}  // namespace vx
+
+extern "C" int vx_attention(const void* q, const void* k, const void* v, void* out, int64_t ldo, float* lse, int D,
+                            int H, int nseq, int Lq, int Lk, int64_t Tq, int64_t Tk, void* stream) {
+  using namespace vx;
+  VX_CHECK_ARG(q && k && v && out, "vx_attention: null pointer");
+  VX_CHECK_ARG(D == 32 || D == 64, "vx_attention: head_dim %d unsupported (32, 64)", D);
+  VX_CHECK_ARG(H > 0 && nseq > 0 && Lq > 0 && Lk > 0, "vx_attention: empty problem");
+  VX_CHECK_ARG((int64_t)nseq * Lq <= Tq && (int64_t)nseq * Lk <= Tk, "vx_attention: sequences exceed buffers");
+  VX_CHECK_ARG((int64_t)H * Tq + 512 < (1ll << 31) && (int64_t)H * Tk + 512 < (1ll << 31),
+               "vx_attention: too many rows for 32-bit TMA coordinates");
+  VX_CHECK_ARG(ldo >= (int64_t)H * D && ldo % 8 == 0, "vx_attention: bad ldo");
+  AttnArgs a;
+  a.H = H;
+  a.nseq = nseq;
+  a.Lq = Lq;
+  a.Lk = Lk;
+  a.Tq = Tq;
+  a.Tk = Tk;
+  a.q_blocks = (Lq + 255) / 256;
+  a.kv_tiles = (Lk + 127) / 128;
+  a.units = H * nseq * a.q_blocks;
+  a.scale_log2 = (1.0f / sqrtf(float(D))) * 1.4426950408889634f;
+  a.out = reinterpret_cast<__nv_bfloat16*>(out);
+  a.ldo = ldo;
+  a.lse = lse;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  return D == 64 ? launch_fmha<64>(q, k, v, a, st) : launch_fmha<32>(q, k, v, a, st);
+}

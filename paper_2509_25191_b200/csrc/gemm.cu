@@ -1,0 +1,378 @@
+// Persistent warp-specialised tcgen05 GEMM with fused VGGT epilogues (sm_100a).
+//
+//   D[M, N] = A[M, K] . B[N, K]^T, bf16 operands (K-major, TMA SWIZZLE_128B),
+//   fp32 accumulators in TMEM (two BN-column buffers so the epilogue of tile t
+//   overlaps the main loop of tile t+1).
+//
+// Warp roles (256 threads): w0 TMA producer, w1 tcgen05.mma issuer (one elected
+// lane), w2 TMEM allocator, w4..w7 epilogue (thread i of warp 4+e owns TMEM lane /
+// tile row 32e+i, so per-row work such as the per-head q/k LayerNorm and RoPE of
+// the qkv epilogue is entirely thread-local).
+//
+// Replaces the upstream nn.Linear calls of the VGGT Block (SURVEY.md §8a a6, a9,
+// a10) and the conv patch-embed (a2), with the norm/RoPE/LayerScale/residual
+// element-wise ops fused into the epilogue.
+#include "../../include/vx_api.h"
+#include "common.cuh"
+#include "host_util.h"
+
+namespace vx {
+
+struct GemmArgs {
+  int M, N, K;
+  vx_epilogue ep;
+};
+
+constexpr int GEMM_BM = 128;
+constexpr int GEMM_BK = 64;
+constexpr int GEMM_THREADS = 256;
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int STAGES = BN == 256 ? 4 : 6;
+  static constexpr uint32_t A_BYTES = GEMM_BM * GEMM_BK * 2;
+  static constexpr uint32_t B_BYTES = BN * GEMM_BK * 2;
+  static constexpr uint32_t SMEM = STAGES * (A_BYTES + B_BYTES) + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr uint32_t TMEM_COLS = 2 * BN;
+};
+
+// ---------------------------------------------------------------------------
+// epilogues: one thread = one output row; columns processed 32 at a time
+// ---------------------------------------------------------------------------
+template <int EPI>
+VX_DEVICE void epi_chunk32(const GemmArgs& a, int row, int col, const uint32_t* r) {
+  const vx_epilogue& e = a.ep;
+  float v[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+  if (e.bias) {
+    const float4* b4 = reinterpret_cast<const float4*>(e.bias + col);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float4 b = __ldg(b4 + j);
+      v[4 * j] += b.x; v[4 * j + 1] += b.y; v[4 * j + 2] += b.z; v[4 * j + 3] += b.w;
+    }
+  }
+  if (row >= a.M) return;
+  if constexpr (EPI == VX_EPI_BF16 || EPI == VX_EPI_GELU) {
+    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(e.out) + (size_t)row * e.ldo + col);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float t[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) t[u] = (EPI == VX_EPI_GELU) ? gelu_erf(v[8 * j + u]) : v[8 * j + u];
+      dst[j] = make_uint4(pack_bf16(t[0], t[1]), pack_bf16(t[2], t[3]), pack_bf16(t[4], t[5]),
+                          pack_bf16(t[6], t[7]));
+    }
+  } else if constexpr (EPI == VX_EPI_F32) {
+    float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(e.out) + (size_t)row * e.ldo + col);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+  } else if constexpr (EPI == VX_EPI_PATCH) {
+    const int P = a.M / 1;  // unused
+    (void)P;
+    const int npatch = e.tokens_per_frame - e.patch_start;
+    const int f = row / npatch, p = row - f * npatch;
+    float4* dst = reinterpret_cast<float4*>(e.resid + ((size_t)f * e.tokens_per_frame + e.patch_start + p) * e.ldr + col);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+  } else if constexpr (EPI == VX_EPI_RESID) {
+    float4* x4 = reinterpret_cast<float4*>(e.resid + (size_t)row * e.ldr + col);
+    const float4* g4 = reinterpret_cast<const float4*>(e.gamma + col);
+    float4 xv[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) xv[j] = x4[j];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float4 g = __ldg(g4 + j);
+      xv[j].x += g.x * v[4 * j];
+      xv[j].y += g.y * v[4 * j + 1];
+      xv[j].z += g.z * v[4 * j + 2];
+      xv[j].w += g.w * v[4 * j + 3];
+      x4[j] = xv[j];
+    }
+    if (e.kept) {
+      uint4* kd = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(e.kept) + (size_t)row * e.ldk + col);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        kd[j] = make_uint4(pack_bf16(xv[2 * j].x, xv[2 * j].y), pack_bf16(xv[2 * j].z, xv[2 * j].w),
+                           pack_bf16(xv[2 * j + 1].x, xv[2 * j + 1].y),
+                           pack_bf16(xv[2 * j + 1].z, xv[2 * j + 1].w));
+    }
+  }
+}
+
+// q/k/v head epilogue: D columns (one head) per call.
+template <int D>
+VX_DEVICE void epi_qkv_head(const GemmArgs& a, int row, int col, float* v) {
+  const vx_epilogue& e = a.ep;
+  const int C = e.embed_dim;
+  const int which = col / C;
+  const int h = (col - which * C) / D;
+  if (e.bias) {
+    const float4* b4 = reinterpret_cast<const float4*>(e.bias + col);
+#pragma unroll
+    for (int j = 0; j < D / 4; ++j) {
+      float4 b = __ldg(b4 + j);
+      v[4 * j] += b.x; v[4 * j + 1] += b.y; v[4 * j + 2] += b.z; v[4 * j + 3] += b.w;
+    }
+  }
+  if (row >= a.M) return;
+  if (which < 2) {
+    const float* nw = which == 0 ? e.qn_w : e.kn_w;
+    const float* nb = which == 0 ? e.qn_b : e.kn_b;
+    if (nw) {
+      float mean = 0.f;
+#pragma unroll
+      for (int j = 0; j < D; ++j) mean += v[j];
+      mean *= (1.0f / D);
+      float var = 0.f;
+#pragma unroll
+      for (int j = 0; j < D; ++j) {
+        float d = v[j] - mean;
+        var += d * d;
+      }
+      const float rstd = rsqrtf(var * (1.0f / D) + e.eps);
+#pragma unroll
+      for (int j = 0; j < D; ++j) v[j] = (v[j] - mean) * rstd * __ldg(nw + j) + __ldg(nb + j);
+    }
+    if (e.rope_cos) {
+      const int t = row % e.tokens_per_frame;
+      int py = 0, px = 0;
+      if (t >= e.patch_start) {
+        const int p = t - e.patch_start;
+        py = p / e.grid_w + 1;
+        px = p - (py - 1) * e.grid_w + 1;
+      }
+      constexpr int Q4 = D / 4;
+      const float* cy = e.rope_cos + py * Q4;
+      const float* sy = e.rope_sin + py * Q4;
+      const float* cx = e.rope_cos + px * Q4;
+      const float* sx = e.rope_sin + px * Q4;
+#pragma unroll
+      for (int j = 0; j < Q4; ++j) {
+        float c = __ldg(cy + j), s = __ldg(sy + j);
+        float x0 = v[j], x1 = v[j + Q4];
+        v[j] = x0 * c - x1 * s;
+        v[j + Q4] = x1 * c + x0 * s;
+        c = __ldg(cx + j);
+        s = __ldg(sx + j);
+        x0 = v[2 * Q4 + j];
+        x1 = v[3 * Q4 + j];
+        v[2 * Q4 + j] = x0 * c - x1 * s;
+        v[3 * Q4 + j] = x1 * c + x0 * s;
+      }
+    }
+  }
+  __nv_bfloat16* base = reinterpret_cast<__nv_bfloat16*>(which == 0 ? e.q : (which == 1 ? e.k : e.v));
+  uint4* dst = reinterpret_cast<uint4*>(base + ((size_t)h * e.tokens_total + row) * D);
+#pragma unroll
+  for (int j = 0; j < D / 8; ++j)
+    dst[j] = make_uint4(pack_bf16(v[8 * j], v[8 * j + 1]), pack_bf16(v[8 * j + 2], v[8 * j + 3]),
+                        pack_bf16(v[8 * j + 4], v[8 * j + 5]), pack_bf16(v[8 * j + 6], v[8 * j + 7]));
+}
+
+// ---------------------------------------------------------------------------
+// kernel
+// ---------------------------------------------------------------------------
+template <int BN, int EPI, int HD>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const GemmArgs args) {
+  using Cfg = GemmCfg<BN>;
+  constexpr int STAGES = Cfg::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * Cfg::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * Cfg::B_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const int M = args.M, N = args.N, K = args.K;
+  const int num_n = (N + BN - 1) / BN;
+  const int num_m = (M + GEMM_BM - 1) / GEMM_BM;
+  const int tiles = num_m * num_n;
+  const int kblocks = K / GEMM_BK;
+
+  if (warp == 0 && elect_one()) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      const uint64_t pol_b = policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        const int m_blk = tile / num_n, n_blk = tile - m_blk * num_n;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], Cfg::A_BYTES + Cfg::B_BYTES);
+          tma_load_2d(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], kb * GEMM_BK, m_blk * GEMM_BM);
+          tma_load_2d_hint(sB + stage * Cfg::B_BYTES, &tmB, &full[stage], kb * GEMM_BK, n_blk * BN, pol_b);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (elect_one()) {
+      constexpr uint32_t idesc = make_idesc_bf16(GEMM_BM, BN, 0, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + stage * Cfg::A_BYTES);
+          const uint32_t b0 = smem_u32(sB + stage * Cfg::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < GEMM_BK / 16; ++k) {
+            mma_ss(d_tmem, make_sdesc(a0 + k * 32, 16, 1024, 2), make_sdesc(b0 + k * 32, 16, 1024, 2), idesc,
+                   (kb | k) != 0);
+          }
+          mma_commit(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        mma_commit(&tfull[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {
+    const int ew = warp - 4;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+      const int m_blk = tile / num_n, n_blk = tile - m_blk * num_n;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row = m_blk * GEMM_BM + ew * 32 + lane;
+      const uint32_t taddr = tmem_base + (uint32_t(ew * 32) << 16) + acc * BN;
+      if constexpr (EPI == VX_EPI_QKV) {
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += HD) {
+          const int col = n_blk * BN + c0;
+          if (col >= N) break;
+          uint32_t r[HD];
+#pragma unroll
+          for (int u = 0; u < HD; u += 32) tmem_ld32(taddr + c0 + u, r + u);
+          tmem_wait_ld();
+          float v[HD];
+#pragma unroll
+          for (int j = 0; j < HD; ++j) v[j] = __uint_as_float(r[j]);
+          epi_qkv_head<HD>(args, row, col, v);
+        }
+      } else {
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          const int col = n_blk * BN + c0;
+          if (col >= N) break;
+          uint32_t r[32];
+          tmem_ld32(taddr + c0, r);
+          tmem_wait_ld();
+          epi_chunk32<EPI>(args, row, col, r);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+  }
+}
+
+template <int BN, int EPI, int HD>
+static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& args, cudaStream_t st) {
+  using Cfg = GemmCfg<BN>;
+  auto kern = gemm_kernel<BN, EPI, HD>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    if (e != cudaSuccess) return fail_cuda(e, "gemm: cudaFuncSetAttribute");
+    attr_set = true;
+  }
+  const int tiles = ((args.M + GEMM_BM - 1) / GEMM_BM) * ((args.N + BN - 1) / BN);
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  kern<<<grid, GEMM_THREADS, Cfg::SMEM, st>>>(ta, tb, args);
+  VX_CHECK_LAUNCH("gemm launch");
+  return VX_OK;
+}
+
+template <int BN>
+static int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, cudaStream_t st) {
+  switch (epi) {
+    case VX_EPI_BF16: return launch_gemm<BN, VX_EPI_BF16, 0>(ta, tb, a, st);
+    case VX_EPI_GELU: return launch_gemm<BN, VX_EPI_GELU, 0>(ta, tb, a, st);
+    case VX_EPI_RESID: return launch_gemm<BN, VX_EPI_RESID, 0>(ta, tb, a, st);
+    case VX_EPI_PATCH: return launch_gemm<BN, VX_EPI_PATCH, 0>(ta, tb, a, st);
+    case VX_EPI_F32: return launch_gemm<BN, VX_EPI_F32, 0>(ta, tb, a, st);
+    case VX_EPI_QKV:
+      if (a.ep.head_dim == 64) return launch_gemm<BN, VX_EPI_QKV, 64>(ta, tb, a, st);
+      if (a.ep.head_dim == 32) return launch_gemm<BN, VX_EPI_QKV, 32>(ta, tb, a, st);
+      set_error("vx_gemm: qkv epilogue needs head_dim 32 or 64 (got %d)", a.ep.head_dim);
+      return VX_E_ARG;
+  }
+  set_error("vx_gemm: unknown epilogue %d", epi);
+  return VX_E_ARG;
+}
+
+}  // namespace vx
+
+extern "C" int vx_gemm(int epi, const void* A, int64_t lda, const void* B, int64_t ldb, int M, int N, int K,
+                       const vx_epilogue* ep, void* stream) {
+  using namespace vx;
+  VX_CHECK_ARG(A && B && ep, "vx_gemm: null pointer");
+  VX_CHECK_ARG(M > 0 && N > 0 && K > 0, "vx_gemm: empty problem M=%d N=%d K=%d", M, N, K);
+  VX_CHECK_ARG(K % GEMM_BK == 0, "vx_gemm: K=%d must be a multiple of %d", K, GEMM_BK);
+  VX_CHECK_ARG(N % 32 == 0, "vx_gemm: N=%d must be a multiple of 32", N);
+  VX_CHECK_ARG(lda >= K && ldb >= K && lda % 8 == 0 && ldb % 8 == 0, "vx_gemm: bad lda/ldb");
+  if (epi == VX_EPI_RESID) VX_CHECK_ARG(ep->resid && ep->gamma, "vx_gemm: resid epilogue needs resid+gamma");
+  if (epi == VX_EPI_QKV) {
+    VX_CHECK_ARG(ep->q && ep->k && ep->v, "vx_gemm: qkv epilogue needs q/k/v");
+    VX_CHECK_ARG(N == 3 * ep->embed_dim && ep->embed_dim % ep->head_dim == 0, "vx_gemm: qkv N != 3C");
+    VX_CHECK_ARG(ep->tokens_total >= M, "vx_gemm: tokens_total < M");
+  }
+  if (epi == VX_EPI_PATCH) VX_CHECK_ARG(ep->resid && ep->tokens_per_frame > ep->patch_start, "vx_gemm: patch args");
+  if (epi == VX_EPI_BF16 || epi == VX_EPI_GELU || epi == VX_EPI_F32) VX_CHECK_ARG(ep->out, "vx_gemm: null out");
+  GemmArgs args;
+  args.M = M;
+  args.N = N;
+  args.K = K;
+  args.ep = *ep;
+  const int BN = (N % 256 == 0 || N > 512) ? 256 : 128;
+  CUtensorMap ta, tb;
+  if (!make_tmap_2d_bf16(&ta, A, M, K, lda, GEMM_BM, GEMM_BK, 128)) return VX_E_ARG;
+  if (!make_tmap_2d_bf16(&tb, B, N, K, ldb, BN, GEMM_BK, 128)) return VX_E_ARG;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  return BN == 256 ? dispatch_epi<256>(epi, ta, tb, args, st) : dispatch_epi<128>(epi, ta, tb, args, st);
+}

@@ -1,0 +1,209 @@
+"""ctypes bindings of the C ABI (`include/vx_api.h`) over torch tensors.
+
+Every function checks shapes/dtypes/devices, passes raw device pointers plus
+the current CUDA stream, and raises RuntimeError with `vx_last_error()` on a
+non-zero status.  There is no fallback: if `libvx.so` is missing or the device
+is not a B200 the import / call fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+import torch
+
+_LIB_PATH = Path(__file__).resolve().parent / "libvx.so"
+
+EPI_BF16, EPI_GELU, EPI_RESID, EPI_QKV, EPI_PATCH, EPI_F32 = range(6)
+
+_vp = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_i32 = ctypes.c_int
+_f32 = ctypes.c_float
+
+
+class Epilogue(ctypes.Structure):
+    _fields_ = [
+        ("bias", _vp), ("out", _vp), ("ldo", _i64),
+        ("resid", _vp), ("ldr", _i64), ("gamma", _vp), ("kept", _vp), ("ldk", _i64),
+        ("q", _vp), ("k", _vp), ("v", _vp),
+        ("qn_w", _vp), ("qn_b", _vp), ("kn_w", _vp), ("kn_b", _vp),
+        ("rope_cos", _vp), ("rope_sin", _vp),
+        ("embed_dim", _i32), ("head_dim", _i32), ("tokens_total", _i32),
+        ("tokens_per_frame", _i32), ("patch_start", _i32), ("grid_w", _i32),
+        ("eps", _f32),
+    ]
+
+
+EXPORTED_SYMBOLS = ("vx_gemm", "vx_attention", "vx_layernorm", "vx_patchify",
+                    "vx_special_tokens", "vx_num_sms", "vx_last_error", "vx_version")
+
+_lib = None
+
+
+def load_library(path: os.PathLike | None = None) -> ctypes.CDLL:
+    """Load libvx.so (no GPU needed) and declare the prototypes."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = Path(path) if path else _LIB_PATH
+    if not p.exists():
+        raise ImportError(f"{p} is missing: run `python -m paper_2509_25191_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(str(p))
+    lib.vx_gemm.argtypes = [_i32, _vp, _i64, _vp, _i64, _i32, _i32, _i32, ctypes.POINTER(Epilogue), _vp]
+    lib.vx_attention.argtypes = [_vp, _vp, _vp, _vp, _i64, _vp, _i32, _i32, _i32, _i32, _i32, _i64, _i64, _vp]
+    lib.vx_layernorm.argtypes = [_vp, _i32, _i64, _vp, _i32, _i64, _vp, _vp, _i32, _i32, _f32, _vp]
+    lib.vx_patchify.argtypes = [_vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp]
+    lib.vx_special_tokens.argtypes = [_vp, _vp, _i32, _i32, _i32, _i32, _vp]
+    lib.vx_last_error.restype = ctypes.c_char_p
+    lib.vx_version.restype = ctypes.c_char_p
+    for name in ("vx_gemm", "vx_attention", "vx_layernorm", "vx_patchify", "vx_special_tokens", "vx_num_sms"):
+        getattr(lib, name).restype = _i32
+    if path is None:
+        _lib = lib
+    return lib
+
+
+def _check(status: int, what: str):
+    if status != 0:
+        msg = _lib.vx_last_error().decode(errors="replace")
+        raise RuntimeError(f"{what} failed ({status}): {msg}")
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _req(t, dtype, name):
+    if not t.is_cuda:
+        raise RuntimeError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if t.dtype != dtype:
+        raise TypeError(f"{name}: expected {dtype}, got {t.dtype}")
+
+
+def _rowmajor(t, name):
+    if t.dim() != 2 or t.stride(1) != 1:
+        raise ValueError(f"{name}: expected a 2-D row-major view, got shape {tuple(t.shape)} "
+                         f"strides {t.stride()}")
+    return t.stride(0)
+
+
+# ---------------------------------------------------------------------------
+def gemm(a: torch.Tensor, w: torch.Tensor, epi: int = EPI_BF16, bias=None, out=None, resid=None,
+         gamma=None, kept=None, qkv=None, qk_norm=None, rope=None, head_dim=0, tokens_total=0,
+         tokens_per_frame=1, patch_start=0, grid_w=1, eps=1e-5):
+    """D = a @ w.T with the given fused epilogue (see include/vx_api.h)."""
+    load_library()
+    _req(a, torch.bfloat16, "a")
+    _req(w, torch.bfloat16, "w")
+    lda = _rowmajor(a, "a")
+    ldw = _rowmajor(w, "w")
+    M, K = a.shape
+    N = w.shape[0]
+    if w.shape[1] != K:
+        raise ValueError(f"gemm: K mismatch {a.shape} x {w.shape}")
+    ep = Epilogue()
+    if bias is not None:
+        _req(bias, torch.float32, "bias")
+        ep.bias = bias.data_ptr()
+    if epi in (EPI_BF16, EPI_GELU, EPI_F32):
+        want = torch.float32 if epi == EPI_F32 else torch.bfloat16
+        if out is None:
+            out = torch.empty(M, N, device=a.device, dtype=want)
+        _req(out, want, "out")
+        ep.out = out.data_ptr()
+        ep.ldo = _rowmajor(out, "out")
+    if epi in (EPI_RESID, EPI_PATCH):
+        _req(resid, torch.float32, "resid")
+        ep.resid = resid.data_ptr()
+        ep.ldr = _rowmajor(resid, "resid")
+    if epi == EPI_RESID:
+        _req(gamma, torch.float32, "gamma")
+        ep.gamma = gamma.data_ptr()
+        if kept is not None:
+            _req(kept, torch.bfloat16, "kept")
+            ep.kept = kept.data_ptr()
+            ep.ldk = _rowmajor(kept, "kept")
+    if epi == EPI_QKV:
+        q, k, v = qkv
+        for t, nm in ((q, "q"), (k, "k"), (v, "v")):
+            _req(t, torch.bfloat16, nm)
+            if not t.is_contiguous():
+                raise ValueError(f"{nm} must be contiguous [H, T, d]")
+        ep.q, ep.k, ep.v = q.data_ptr(), k.data_ptr(), v.data_ptr()
+        if qk_norm is not None:
+            qw, qb, kw, kb = qk_norm
+            ep.qn_w, ep.qn_b, ep.kn_w, ep.kn_b = (t.data_ptr() for t in (qw, qb, kw, kb))
+        if rope is not None:
+            ep.rope_cos, ep.rope_sin = rope[0].data_ptr(), rope[1].data_ptr()
+        ep.embed_dim = N // 3
+        ep.head_dim = head_dim
+        ep.tokens_total = tokens_total
+    ep.tokens_per_frame = tokens_per_frame
+    ep.patch_start = patch_start
+    ep.grid_w = grid_w
+    ep.eps = eps
+    _check(_lib.vx_gemm(epi, _ptr(a), lda, _ptr(w), ldw, M, N, K, ctypes.byref(ep), _stream()), "vx_gemm")
+    return out
+
+
+def attention(q, k, v, out, nseq: int, Lq: int, Lk: int, lse=None):
+    """Flash attention over q [H, Tq, d], k/v [H, Tk, d] -> out [Tq', H*d] (bf16)."""
+    load_library()
+    for t, nm in ((q, "q"), (k, "k"), (v, "v"), (out, "out")):
+        _req(t, torch.bfloat16, nm)
+    H, Tq, D = q.shape
+    Tk = k.shape[1]
+    if k.shape != v.shape or k.shape[0] != H or k.shape[2] != D:
+        raise ValueError("attention: q/k/v shape mismatch")
+    if not (q.is_contiguous() and k.is_contiguous() and v.is_contiguous()):
+        raise ValueError("attention: q/k/v must be contiguous")
+    ldo = _rowmajor(out, "out")
+    if lse is not None:
+        _req(lse, torch.float32, "lse")
+    _check(_lib.vx_attention(_ptr(q), _ptr(k), _ptr(v), _ptr(out), ldo, _ptr(lse), D, H, nseq, Lq, Lk,
+                             Tq, Tk, _stream()), "vx_attention")
+    return out
+
+
+def layernorm(x, w, b, eps, out=None, out_dtype=torch.bfloat16):
+    load_library()
+    if not x.is_cuda:
+        raise RuntimeError("layernorm: CUDA tensor required")
+    ldx = _rowmajor(x, "x")
+    rows, cols = x.shape
+    if out is None:
+        out = torch.empty(rows, cols, device=x.device, dtype=out_dtype)
+    ldy = _rowmajor(out, "out")
+    code = {torch.float32: 0, torch.bfloat16: 1}
+    _check(_lib.vx_layernorm(_ptr(x), code[x.dtype], ldx, _ptr(out), code[out.dtype], ldy, _ptr(w), _ptr(b),
+                             rows, cols, eps, _stream()), "vx_layernorm")
+    return out
+
+
+def patchify(images, patch: int, kpad: int, out=None):
+    load_library()
+    _req(images, torch.float32, "images")
+    images = images.contiguous()
+    S, C, H, W = images.shape
+    P = (H // patch) * (W // patch)
+    if out is None:
+        out = torch.empty(S * P, kpad, device=images.device, dtype=torch.bfloat16)
+    _check(_lib.vx_patchify(_ptr(images), _ptr(out), S, H, W, patch, kpad, _stream()), "vx_patchify")
+    return out
+
+
+def special_tokens(x, tokens, S, tpf):
+    load_library()
+    _req(x, torch.float32, "x")
+    _req(tokens, torch.float32, "tokens")
+    ntok, C = tokens.shape[-2], tokens.shape[-1]
+    _check(_lib.vx_special_tokens(_ptr(x), _ptr(tokens.contiguous()), S, tpf, ntok, C, _stream()),
+           "vx_special_tokens")
+    return x

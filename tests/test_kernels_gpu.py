@@ -1,0 +1,227 @@
+"""Kernel-level parity of the sm_100a C-ABI ops against plain PyTorch fp32 references.
+
+Pattern follows the reference's native-vs-fallback parity tests
+(`pkg/tests/test_kernels.py:20-45`): same inputs, every implementation, stated
+tolerances.  bf16 operands, fp32 accumulation; tolerances are relative
+Frobenius errors with the bound written in each test.
+"""
+import math
+
+import pytest
+import torch
+import torch.nn.functional as F
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    a, b = a.float(), b.float()
+    return ((a - b).norm() / b.norm().clamp_min(1e-30)).item()
+
+
+@pytest.fixture(scope="module")
+def ops():
+    from paper_2509_25191_b200 import ops as _ops
+    _ops.load_library()
+    return _ops
+
+
+def _bf(*shape, scale=1.0, seed=0):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    return (torch.randn(*shape, device="cuda", generator=g) * scale).to(torch.bfloat16)
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (300, 256, 128), (1374, 1024, 1024), (777, 384, 128),
+                                   (2748, 4096, 1024), (1000, 1024, 4096), (64, 96, 192)])
+def test_gemm_bf16_bias(ops, M, N, K):
+    a = _bf(M, K, seed=1)
+    w = _bf(N, K, scale=0.05, seed=2)
+    bias = torch.randn(N, device="cuda")
+    out = ops.gemm(a, w, ops.EPI_BF16, bias=bias)
+    ref = a.float() @ w.float().T + bias
+    assert rel(out, ref) < 5e-3
+
+
+def test_gemm_gelu_and_f32(ops):
+    M, N, K = 1500, 512, 256
+    a = _bf(M, K, seed=3)
+    w = _bf(N, K, scale=0.1, seed=4)
+    bias = torch.randn(N, device="cuda")
+    ref = a.float() @ w.float().T + bias
+    g = ops.gemm(a, w, ops.EPI_GELU, bias=bias)
+    assert rel(g, F.gelu(ref)) < 5e-3
+    f = ops.gemm(a, w, ops.EPI_F32, bias=bias)
+    assert rel(f, ref) < 1e-5
+
+
+def test_gemm_strided_a(ops):
+    # A as a column slice of a wider row-major buffer (lda != K)
+    big = _bf(640, 256, seed=5)
+    a = big[:, 64:192]
+    w = _bf(256, 128, scale=0.1, seed=6)
+    out = ops.gemm(a, w, ops.EPI_BF16)
+    assert rel(out, a.float() @ w.float().T) < 5e-3
+
+
+@pytest.mark.parametrize("with_kept", [False, True])
+def test_gemm_residual_layerscale(ops, with_kept):
+    M, N, K = 2000, 1024, 4096
+    a = _bf(M, K, seed=7)
+    w = _bf(N, K, scale=0.02, seed=8)
+    bias = torch.randn(N, device="cuda") * 0.1
+    gamma = torch.rand(N, device="cuda") * 0.5
+    x = torch.randn(M, N, device="cuda")
+    x0 = x.clone()
+    kept = torch.zeros(M, 2 * N, device="cuda", dtype=torch.bfloat16) if with_kept else None
+    ops.gemm(a, w, ops.EPI_RESID, bias=bias, resid=x, gamma=gamma,
+             kept=kept[:, N:] if with_kept else None)
+    ref = x0 + gamma * (a.float() @ w.float().T + bias)
+    assert rel(x - x0, ref - x0) < 5e-3
+    assert rel(x, ref) < 1e-3
+    if with_kept:
+        assert rel(kept[:, N:], ref) < 5e-3
+        assert kept[:, :N].abs().max().item() == 0
+
+
+def test_gemm_patch_embed_remap(ops):
+    S, P, tpf, ps, C, K = 3, 1369, 1374, 5, 1024, 640
+    a = _bf(S * P, K, seed=9)
+    w = _bf(C, K, scale=0.02, seed=10)
+    bias = torch.randn(C, device="cuda")
+    x = torch.full((S * tpf, C), 7.0, device="cuda")
+    ops.gemm(a, w, ops.EPI_PATCH, bias=bias, resid=x, tokens_per_frame=tpf, patch_start=ps)
+    ref = (a.float() @ w.float().T + bias).view(S, P, C)
+    xv = x.view(S, tpf, C)
+    assert rel(xv[:, ps:], ref) < 1e-5
+    assert (xv[:, :ps] == 7.0).all()
+
+
+def _rope_ref(x, pos, freq=100.0):
+    from oracle.vggt_ref import rope_2d
+    return rope_2d(x, pos, freq)
+
+
+@pytest.mark.parametrize("C,H,S,grid", [(1024, 16, 2, 37), (128, 4, 8, 8), (256, 4, 3, 9)])
+def test_gemm_qkv_qknorm_rope(ops, C, H, S, grid):
+    from oracle.vggt_ref import positions, rope_tables
+    from paper_2509_25191_b200.config import VGGTConfig
+    cfg = VGGTConfig(img_size=grid * 14, embed_dim=C, num_heads=H)
+    d = C // H
+    tpf = cfg.tokens_per_frame
+    T = S * tpf
+    a = _bf(T, C, seed=11)
+    w = _bf(3 * C, C, scale=0.05, seed=12)
+    bias = torch.randn(3 * C, device="cuda") * 0.1
+    qw, qb, kw, kb = (torch.randn(d, device="cuda") * 0.1 + (1.0 if i % 2 == 0 else 0.0) for i in range(4))
+    cos, sin = rope_tables(d, grid + 1, 100.0)
+    cos_q = cos[:, : d // 4].contiguous().cuda()
+    sin_q = sin[:, : d // 4].contiguous().cuda()
+    q = torch.empty(H, T, d, device="cuda", dtype=torch.bfloat16)
+    k = torch.empty_like(q)
+    v = torch.empty_like(q)
+    ops.gemm(a, w, ops.EPI_QKV, bias=bias, qkv=(q, k, v), qk_norm=(qw, qb, kw, kb), rope=(cos_q, sin_q),
+             head_dim=d, tokens_total=T, tokens_per_frame=tpf, patch_start=cfg.patch_start_idx, grid_w=grid,
+             eps=1e-5)
+    y = (a.float() @ w.float().T + bias).cpu().view(T, 3, H, d).permute(1, 2, 0, 3)  # (3, H, T, d)
+    qr = F.layer_norm(y[0], (d,), qw.cpu(), qb.cpu(), 1e-5)
+    kr = F.layer_norm(y[1], (d,), kw.cpu(), kb.cpu(), 1e-5)
+    pos = positions(cfg).repeat(S, 1)
+    qr = _rope_ref(qr, pos)
+    kr = _rope_ref(kr, pos)
+    assert rel(q.cpu(), qr) < 5e-3
+    assert rel(k.cpu(), kr) < 5e-3
+    assert rel(v.cpu(), y[2]) < 5e-3
+
+
+def _sdpa_ref(q, k, v, nseq, Lq, Lk):
+    H, _, d = q.shape
+    qf = q.float()[:, : nseq * Lq].view(H, nseq, Lq, d)
+    kf = k.float()[:, : nseq * Lk].view(H, nseq, Lk, d)
+    vf = v.float()[:, : nseq * Lk].view(H, nseq, Lk, d)
+    s = torch.einsum("hsqd,hskd->hsqk", qf, kf) / math.sqrt(d)
+    lse = torch.logsumexp(s, dim=-1)
+    o = torch.einsum("hsqk,hskd->hsqd", s.softmax(-1), vf)
+    return o.permute(1, 2, 0, 3).reshape(nseq * Lq, H * d), lse.reshape(H, nseq * Lq)
+
+
+@pytest.mark.parametrize("D,H,nseq,L", [(64, 16, 3, 1374), (64, 2, 1, 5000), (64, 4, 5, 69), (32, 4, 8, 69),
+                                        (32, 4, 1, 552), (64, 1, 2, 128), (64, 3, 1, 300), (64, 2, 1, 17)])
+def test_attention_matches_sdpa(ops, D, H, nseq, L):
+    T = nseq * L
+    q = _bf(H, T, D, seed=20)
+    k = _bf(H, T, D, seed=21)
+    v = _bf(H, T, D, seed=22)
+    out = torch.empty(T, H * D, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(H, T, device="cuda")
+    ops.attention(q, k, v, out, nseq, L, L, lse=lse)
+    ref, lse_ref = _sdpa_ref(q, k, v, nseq, L, L)
+    assert rel(out, ref) < 1e-2
+    assert (lse - lse_ref).abs().max().item() < 1e-2
+
+
+def test_attention_large_logits_rescale(ops):
+    # peaked scores force the lazy O-rescaling path
+    H, L, D = 2, 2000, 64
+    q = _bf(H, L, D, scale=4.0, seed=30)
+    k = _bf(H, L, D, scale=4.0, seed=31)
+    v = _bf(H, L, D, seed=32)
+    out = torch.empty(L, H * D, device="cuda", dtype=torch.bfloat16)
+    ops.attention(q, k, v, out, 1, L, L)
+    ref, _ = _sdpa_ref(q, k, v, 1, L, L)
+    assert rel(out, ref) < 1e-2
+
+
+def test_attention_cross_lengths(ops):
+    # ring-step shape: local queries against a remote K/V shard of another length
+    H, Lq, Lk, D = 4, 700, 1900, 64
+    q = _bf(H, Lq, D, seed=40)
+    k = _bf(H, Lk, D, seed=41)
+    v = _bf(H, Lk, D, seed=42)
+    out = torch.empty(Lq, H * D, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(H, Lq, device="cuda")
+    ops.attention(q, k, v, out, 1, Lq, Lk, lse=lse)
+    ref, lse_ref = _sdpa_ref(q, k, v, 1, Lq, Lk)
+    assert rel(out, ref) < 1e-2
+    assert (lse - lse_ref).abs().max().item() < 1e-2
+
+
+@pytest.mark.parametrize("cols,dt_in", [(1024, torch.float32), (128, torch.float32), (2048, torch.bfloat16),
+                                        (256, torch.float32)])
+def test_layernorm(ops, cols, dt_in):
+    rows = 3001
+    x = (torch.randn(rows, cols, device="cuda") * 3 + 1).to(dt_in)
+    w = torch.randn(cols, device="cuda")
+    b = torch.randn(cols, device="cuda")
+    y = ops.layernorm(x, w, b, 1e-5)
+    ref = F.layer_norm(x.float(), (cols,), w, b, 1e-5)
+    assert rel(y, ref) < 5e-3
+    y32 = ops.layernorm(x, w, b, 1e-5, out_dtype=torch.float32)
+    assert rel(y32, ref) < 1e-5
+
+
+def test_patchify_matches_conv(ops):
+    from oracle.vggt_ref import RESNET_MEAN, RESNET_STD
+    S, Hh = 2, 518
+    img = torch.rand(S, 3, Hh, Hh, device="cuda")
+    a = ops.patchify(img, 14, 640)
+    w = _bf(64, 640, scale=0.05, seed=50)
+    w[:, 588:] = 0
+    out = a.float() @ w.float().T
+    mean = torch.tensor(RESNET_MEAN, device="cuda").view(1, 3, 1, 1)
+    std = torch.tensor(RESNET_STD, device="cuda").view(1, 3, 1, 1)
+    ref = F.conv2d((img - mean) / std, w.float()[:, :588].reshape(64, 3, 14, 14), stride=14)
+    ref = ref.flatten(2).transpose(1, 2).reshape(-1, 64)
+    assert rel(out, ref) < 5e-3
+    assert (a[:, 588:] == 0).all()
+
+
+def test_special_tokens(ops):
+    S, tpf, C = 4, 69, 128
+    tok = torch.randn(2, 5, C, device="cuda")
+    x = torch.zeros(S * tpf, C, device="cuda")
+    ops.special_tokens(x, tok, S, tpf)
+    xv = x.view(S, tpf, C)
+    assert torch.equal(xv[0, :5], tok[0])
+    for f in range(1, S):
+        assert torch.equal(xv[f, :5], tok[1])
+    assert (xv[:, 5:] == 0).all()
