@@ -30,6 +30,7 @@ import torch
 
 from . import ops
 from .config import VGGTConfig
+from .profiling import phase
 from .weights import is_bf16_param
 
 
@@ -105,31 +106,40 @@ def run_block(W: DeviceWeights, name: str, ws: Workspace, S: int, frame_attn: bo
     N = cfg.tokens_per_frame
     T = S * N
     C = cfg.embed_dim
-    ops.layernorm(ws.x, W[name + ".norm1.weight"], W[name + ".norm1.bias"], cfg.ln_eps, out=ws.xn)
-    ops.gemm(ws.xn, W[name + ".attn.qkv.weight"], ops.EPI_QKV, bias=W[name + ".attn.qkv.bias"],
-             qkv=(ws.q, ws.k, ws.v),
-             qk_norm=(W[name + ".attn.q_norm.weight"], W[name + ".attn.q_norm.bias"],
-                      W[name + ".attn.k_norm.weight"], W[name + ".attn.k_norm.bias"]),
-             rope=W.rope, head_dim=cfg.head_dim, tokens_total=T, tokens_per_frame=N,
-             patch_start=cfg.patch_start_idx, grid_w=cfg.grid, eps=cfg.ln_eps)
+    with phase("layernorm"):
+        ops.layernorm(ws.x, W[name + ".norm1.weight"], W[name + ".norm1.bias"], cfg.ln_eps, out=ws.xn)
+    with phase("gemm_qkv"):
+        ops.gemm(ws.xn, W[name + ".attn.qkv.weight"], ops.EPI_QKV, bias=W[name + ".attn.qkv.bias"],
+                 qkv=(ws.q, ws.k, ws.v),
+                 qk_norm=(W[name + ".attn.q_norm.weight"], W[name + ".attn.q_norm.bias"],
+                          W[name + ".attn.k_norm.weight"], W[name + ".attn.k_norm.bias"]),
+                 rope=W.rope, head_dim=cfg.head_dim, tokens_total=T, tokens_per_frame=N,
+                 patch_start=cfg.patch_start_idx, grid_w=cfg.grid, eps=cfg.ln_eps)
     if frame_attn:
-        ops.attention(ws.q, ws.k, ws.v, ws.o, nseq=S, Lq=N, Lk=N)
+        with phase("attn_frame"):
+            ops.attention(ws.q, ws.k, ws.v, ws.o, nseq=S, Lq=N, Lk=N)
     elif global_attn is not None:
-        global_attn(ws.q, ws.k, ws.v, ws.o)
+        with phase("attn_global"):
+            global_attn(ws.q, ws.k, ws.v, ws.o)
     else:
-        ops.attention(ws.q, ws.k, ws.v, ws.o, nseq=1, Lq=T, Lk=T)
-    ops.gemm(ws.o, W[name + ".attn.proj.weight"], ops.EPI_RESID, bias=W[name + ".attn.proj.bias"],
-             resid=ws.x, gamma=W[name + ".ls1.gamma"])
-    ops.layernorm(ws.x, W[name + ".norm2.weight"], W[name + ".norm2.bias"], cfg.ln_eps, out=ws.xn)
+        with phase("attn_global"):
+            ops.attention(ws.q, ws.k, ws.v, ws.o, nseq=1, Lq=T, Lk=T)
+    with phase("gemm_proj"):
+        ops.gemm(ws.o, W[name + ".attn.proj.weight"], ops.EPI_RESID, bias=W[name + ".attn.proj.bias"],
+                 resid=ws.x, gamma=W[name + ".ls1.gamma"])
+    with phase("layernorm"):
+        ops.layernorm(ws.x, W[name + ".norm2.weight"], W[name + ".norm2.bias"], cfg.ln_eps, out=ws.xn)
     rows = ws.h.shape[0]
     for r0 in range(0, T, rows):
         r1 = min(T, r0 + rows)
         hb = ws.h[: r1 - r0]
-        ops.gemm(ws.xn[r0:r1], W[name + ".mlp.fc1.weight"], ops.EPI_GELU, bias=W[name + ".mlp.fc1.bias"],
-                 out=hb)
-        ops.gemm(hb, W[name + ".mlp.fc2.weight"], ops.EPI_RESID, bias=W[name + ".mlp.fc2.bias"],
-                 resid=ws.x[r0:r1], gamma=W[name + ".ls2.gamma"],
-                 kept=None if kept_half is None else kept_half[r0:r1])
+        with phase("gemm_fc1"):
+            ops.gemm(ws.xn[r0:r1], W[name + ".mlp.fc1.weight"], ops.EPI_GELU, bias=W[name + ".mlp.fc1.bias"],
+                     out=hb)
+        with phase("gemm_fc2"):
+            ops.gemm(hb, W[name + ".mlp.fc2.weight"], ops.EPI_RESID, bias=W[name + ".mlp.fc2.bias"],
+                     resid=ws.x[r0:r1], gamma=W[name + ".ls2.gamma"],
+                     kept=None if kept_half is None else kept_half[r0:r1])
 
 
 def embed(W: DeviceWeights, images: torch.Tensor, ws: Workspace, frame0_is_first: bool = True):
@@ -140,10 +150,11 @@ def embed(W: DeviceWeights, images: torch.Tensor, ws: Workspace, frame0_is_first
     special = W.special
     if not frame0_is_first:  # a shard that does not own global frame 0 uses the "other" tokens
         special = special[1:2].expand(2, -1, -1).contiguous()
-    ops.special_tokens(ws.x, special, S, N)
-    a = ops.patchify(images, cfg.patch_size, cfg.patch_k_padded)
-    ops.gemm(a, W.patch_w, ops.EPI_PATCH, bias=W["aggregator.patch_embed.proj.bias"], resid=ws.x,
-             tokens_per_frame=N, patch_start=cfg.patch_start_idx)
+    with phase("embed"):
+        ops.special_tokens(ws.x, special, S, N)
+        a = ops.patchify(images, cfg.patch_size, cfg.patch_k_padded)
+        ops.gemm(a, W.patch_w, ops.EPI_PATCH, bias=W["aggregator.patch_embed.proj.bias"], resid=ws.x,
+                 tokens_per_frame=N, patch_start=cfg.patch_start_idx)
 
 
 def aggregator_forward(W: DeviceWeights, images: torch.Tensor, ws: Optional[Workspace] = None,

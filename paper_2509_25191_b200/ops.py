@@ -66,7 +66,13 @@ def load_library(path: os.PathLike | None = None) -> ctypes.CDLL:
     return lib
 
 
+# number of vx kernel launches issued by this process (bench.py's gpu_launches)
+launch_count = 0
+
+
 def _check(status: int, what: str):
+    global launch_count
+    launch_count += 1
     if status != 0:
         msg = _lib.vx_last_error().decode(errors="replace")
         raise RuntimeError(f"{what} failed ({status}): {msg}")

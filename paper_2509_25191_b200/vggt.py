@@ -1,0 +1,121 @@
+"""Drop-in `VGGT` inference module (SURVEY.md §8b "Python API to keep").
+
+    model = VGGT(cfg)                 # seeded random-init weights (no checkpoints on disk)
+    preds = model(images)             # images (S,3,H,W) or (1,S,3,H,W) in [0, 1]
+    preds["pose_enc"]                 # (1, S, 9) fp32  [T(3), quat XYZW(4), fov_h, fov_w]
+    preds["depth"], ["depth_conf"]    # (1, S, H, W, 1), (1, S, H, W) fp32
+    preds["world_points"], [..._conf] # (1, S, H, W, 3), (1, S, H, W) fp32
+    kept, psi = model.aggregator(images)  # {layer: (1, S, N, 2C) bf16}, patch_start_idx
+
+Under torchrun with world_size > 1 (`dist=True`) the views are frame-sharded:
+every rank passes the FULL image batch (or its own slice with `sharded_input`),
+the global attention layers run the K/V ring (ring.py), the camera head sees
+all camera tokens (all-gather), and the dense outputs returned are this rank's
+frame slice while `pose_enc` is global.
+"""
+from __future__ import annotations
+
+from typing import Dict, Optional, Tuple
+
+import torch
+
+from . import ops
+from .aggregator import DeviceWeights, aggregator_forward, alloc_workspace
+from .config import VGGTConfig, vggt_1b
+from .heads import DPTHeadDevice, camera_head
+from .profiling import phase
+from .pose import pose_encoding_to_extri_intri  # noqa: F401  (re-export, upstream location)
+from .weights import make_state_dict
+
+
+def _require_b200(device):
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2509_25191_b200 needs a CUDA device (sm_100a); there is no CPU fallback")
+    cap = torch.cuda.get_device_capability(device)
+    if cap[0] != 10:
+        raise RuntimeError(f"sm_100a kernels need a Blackwell B200 (got compute capability {cap})")
+
+
+class VGGT:
+    def __init__(self, cfg: Optional[VGGTConfig] = None, state_dict=None, seed: int = 0, device="cuda",
+                 dist: bool = False):
+        self.cfg = cfg or vggt_1b()
+        self.device = torch.device(device)
+        _require_b200(self.device)
+        ops.load_library()
+        sd = state_dict if state_dict is not None else make_state_dict(self.cfg, seed)
+        self.W = DeviceWeights(sd, self.cfg, self.device)
+        self.depth_head = DPTHeadDevice(self.W, "depth_head.", "exp")
+        self.point_head = DPTHeadDevice(self.W, "point_head.", "inv_log")
+        self.dist = dist
+        self.ring = None
+        if dist:
+            from .ring import FrameShardedRing
+            self.ring = FrameShardedRing(self.cfg, self.device)
+
+    # -- helpers ------------------------------------------------------------
+    def _prep(self, images: torch.Tensor) -> torch.Tensor:
+        if images.dim() == 5:
+            if images.shape[0] != 1:
+                raise ValueError("batch size B must be 1 (frames are the batch dimension)")
+            images = images[0]
+        if images.dim() != 4 or images.shape[1] != 3:
+            raise ValueError(f"images must be (S,3,H,W) or (1,S,3,H,W); got {tuple(images.shape)}")
+        return images.to(self.device, torch.float32, non_blocking=True).contiguous()
+
+    def _local(self, images, sharded_input: bool):
+        """(local images, global frame offset, global S) for this rank."""
+        if self.ring is None:
+            return images, 0, images.shape[0]
+        return self.ring.local_frames(images, sharded_input)
+
+    # -- API ------------------------------------------------------------------
+    @torch.no_grad()
+    def aggregator(self, images: torch.Tensor, sharded_input: bool = False) -> Tuple[Dict[int, torch.Tensor], int]:
+        images = self._prep(images)
+        local, f0, S = self._local(images, sharded_input)
+        kept = self._aggregate(local, f0)
+        return {i: t[None] for i, t in kept.items()}, self.cfg.patch_start_idx
+
+    def _aggregate(self, local: torch.Tensor, f0: int) -> Dict[int, torch.Tensor]:
+        ws = alloc_workspace(self.cfg, local.shape[0], self.device)
+        gattn = None if self.ring is None else self.ring.global_attention
+        kept = aggregator_forward(self.W, local, ws, global_attn=gattn, frame0_is_first=(f0 == 0))
+        del ws
+        return kept
+
+    @torch.no_grad()
+    def forward(self, images: torch.Tensor, sharded_input: bool = False) -> Dict[str, torch.Tensor]:
+        cfg = self.cfg
+        images = self._prep(images)
+        local, f0, S = self._local(images, sharded_input)
+        kept = self._aggregate(local, f0)
+        Sl = local.shape[0]
+        N = cfg.tokens_per_frame
+        # camera head over ALL views (attention across camera tokens)
+        cam = kept[cfg.kept_layers[-1]][:, 0]                      # (Sl, 2C) strided view
+        if self.ring is not None:
+            cam = self.ring.all_gather_frames(cam.contiguous())
+        with phase("camera_head"):
+            pose_list = camera_head(self.W, cam)
+        H = W = cfg.img_size
+        dev = self.device
+        depth = torch.empty(Sl, H, W, 1, device=dev)
+        depth_conf = torch.empty(Sl, H, W, device=dev)
+        pts = torch.empty(Sl, H, W, 3, device=dev)
+        pts_conf = torch.empty(Sl, H, W, device=dev)
+        with phase("dpt_heads"):
+            self.depth_head(kept, depth, depth_conf, cfg.head_chunk)
+            self.point_head(kept, pts, pts_conf, cfg.head_chunk)
+        return {
+            "pose_enc": pose_list[-1][None],
+            "pose_enc_list": [p[None] for p in pose_list],
+            "depth": depth[None],
+            "depth_conf": depth_conf[None],
+            "world_points": pts[None],
+            "world_points_conf": pts_conf[None],
+            "images": local[None],
+            "frame_offset": f0,
+        }
+
+    __call__ = forward
