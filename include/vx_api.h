@@ -106,6 +106,12 @@ int vx_patchify(const float* images, void* out, int S, int H, int W, int patch, 
  * (slice_expand_and_flatten + cat, a3) */
 int vx_special_tokens(float* x, const float* tokens, int S, int tpf, int ntok, int C, void* stream);
 
+/* Bilinear resize with align_corners=True of NHWC bf16 maps in [F, h, w, C] -> out [F, H, W, C],
+ * plus an optional bf16 [H, W, C] map added after interpolation (DPT pos-embed / skip).
+ * (F.interpolate(mode="bilinear", align_corners=True) in DPTHead / FeatureFusionBlock, a14) */
+int vx_upsample_bilinear(const void* in, int F, int h, int w, int C, void* out, int H, int W,
+                         const void* add_hwc, void* stream);
+
 int vx_num_sms(void);
 const char* vx_last_error(void);
 const char* vx_version(void);

@@ -22,6 +22,9 @@ VX_DEVICE uint32_t smem_u32(const void* p) {
 }
 VX_DEVICE uint32_t warp_id() { return __shfl_sync(0xffffffff, threadIdx.x / 32, 0); }
 VX_DEVICE uint32_t lane_id() { return threadIdx.x & 31; }
+VX_DEVICE void named_bar_sync(uint32_t id, uint32_t nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 VX_DEVICE bool elect_one() {
   uint32_t pred = 0;
   asm volatile(
@@ -177,7 +180,7 @@ VX_DEVICE void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::
 #define VX_W8(a, o) "r"(a[o + 0]), "r"(a[o + 1]), "r"(a[o + 2]), "r"(a[o + 3]), \
                     "r"(a[o + 4]), "r"(a[o + 5]), "r"(a[o + 6]), "r"(a[o + 7])
 
-VX_DEVICE void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+VX_DEVICE void tmem_ld16(uint32_t taddr, uint32_t* r) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
       : VX_R8(r, 0), VX_R8(r, 8)
@@ -213,6 +216,66 @@ VX_DEVICE float ex2(float x) {
   asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// three-input max (FMNMX3 on sm_100a)
+VX_DEVICE float max3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+// 2^x on the FMA pipe (degree-3 polynomial, rel. err 2.2e-4 < bf16 ulp), x <= ~64.
+// Splits x = n + f with the 1.5*2^23 rounding trick; (bits(t) << 23) == n << 23 (mod 2^32).
+// The clamp at -126 keeps the exponent add from wrapping into the sign bit.
+VX_DEVICE float ex2_poly(float x) {
+  x = fmaxf(x, -126.0f);
+  const float t = x + 12582912.0f;
+  const float f = x - (t - 12582912.0f);
+  const float p = fmaf(fmaf(fmaf(0.05286732f, f, 0.24215214f), f, 0.6935868f), f, 0.99996275f);
+  return __uint_as_float(__float_as_uint(p) + (__float_as_uint(t) << 23));
+}
+
+// ---- packed fp32x2 arithmetic (FFMA2 / FADD2 on sm_100a) ----
+VX_DEVICE uint64_t f2_pack(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+VX_DEVICE void f2_unpack(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+VX_DEVICE uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+VX_DEVICE uint64_t f2_add(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+VX_DEVICE uint64_t f2_mul(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+// two 2^x at once on the FMA pipe (packed polynomial); returns (2^lo, 2^hi)
+VX_DEVICE void ex2_poly2(float x0, float x1, float& y0, float& y1) {
+  const uint64_t MAGIC = f2_pack(12582912.0f, 12582912.0f);
+  const uint64_t NMAGIC = f2_pack(-12582912.0f, -12582912.0f);
+  const uint64_t NEG1 = f2_pack(-1.0f, -1.0f);
+  const uint64_t x = f2_pack(fmaxf(x0, -126.0f), fmaxf(x1, -126.0f));
+  const uint64_t t = f2_add(x, MAGIC);
+  const uint64_t f = f2_fma(f2_add(t, NMAGIC), NEG1, x);
+  uint64_t p = f2_fma(f2_pack(0.05286732f, 0.05286732f), f, f2_pack(0.24215214f, 0.24215214f));
+  p = f2_fma(p, f, f2_pack(0.6935868f, 0.6935868f));
+  p = f2_fma(p, f, f2_pack(0.99996275f, 0.99996275f));
+  float p0, p1, t0, t1;
+  f2_unpack(p, p0, p1);
+  f2_unpack(t, t0, t1);
+  y0 = __uint_as_float(__float_as_uint(p0) + (__float_as_uint(t0) << 23));
+  y1 = __uint_as_float(__float_as_uint(p1) + (__float_as_uint(t1) << 23));
+}
+
+VX_DEVICE void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 VX_DEVICE uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);

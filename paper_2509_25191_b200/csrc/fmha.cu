@@ -15,9 +15,12 @@
 //   w4..w7  softmax + epilogue for Q tile 0, w8..w11 for Q tile 1
 //           (thread = one query row = one TMEM lane: row max / sum are thread-local;
 //            lazy O rescaling only when the running max grows by > 2^8)
+//   (v4: each Q tile's 128 score columns are split over two warpgroups, 16 softmax warps in
+//    total, partial row maxima exchanged through shared memory + a named barrier)
 // MMA issue order per KV tile j:  PV_0(j), S_0(j+1), PV_1(j), S_1(j+1), so each
 // softmax warpgroup's exp work overlaps the other tile's tensor-core work.
 #include <math.h>
+#include <stdlib.h>
 
 #include "../../include/vx_api.h"
 #include "common.cuh"
@@ -43,13 +46,15 @@ struct AttnCfg {
   static constexpr int SWIZZLE = D == 64 ? 128 : 64;
   static constexpr uint32_t LAYOUT = D == 64 ? 2 : 4;  // SWIZZLE_128B / SWIZZLE_64B
   static constexpr uint32_t SBO = 8 * ROW_BYTES;       // 8-row core-matrix group
-  static constexpr uint32_t SMEM = (2 + 2 * KST) * TILE_BYTES + 1024 + 512;
+  static constexpr uint32_t ONES_BYTES = 2048;  // 16 x 64 bf16 ones (row-sum B operand)
+  static constexpr uint32_t SMEM = (2 + 2 * KST) * TILE_BYTES + ONES_BYTES + 1024 + 512 + 2048;
 };
 
-constexpr int ATTN_THREADS = 384;
+constexpr int ATTN_THREADS = 640;  // 4 control warps + 4 softmax warpgroups
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
 
-template <int D>
+// EMU_PAIRS_OF_8: of every 8 exp pairs, this many use the FMA-pipe polynomial
+template <int D, int EMU_PAIRS_OF_8>
 __global__ void __launch_bounds__(ATTN_THREADS, 1)
     fmha_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                 const __grid_constant__ CUtensorMap tmV, const AttnArgs a) {
@@ -60,7 +65,8 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
   uint8_t* sQ = smem;                                 // 2 tiles
   uint8_t* sK = sQ + 2 * Cfg::TILE_BYTES;             // KST tiles
   uint8_t* sV = sK + KST * Cfg::TILE_BYTES;           // KST tiles
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sV + KST * Cfg::TILE_BYTES);
+  uint8_t* sOnes = sV + KST * Cfg::TILE_BYTES;        // 2 KB of bf16 1.0
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sOnes + Cfg::ONES_BYTES);
   uint64_t* q_full = bar;
   uint64_t* q_empty = bar + 1;
   uint64_t* k_full = bar + 2;
@@ -72,6 +78,7 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
   uint64_t* o_full = p_full + 2;     // [2]
   uint64_t* o_empty = o_full + 2;    // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
+  float* xmax = reinterpret_cast<float*>(bar + 64);  // [2 tiles][2 halves][128 rows] partial maxima
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -90,13 +97,18 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], 4);
+      mbar_init(&p_full[i], 8);
       mbar_init(&o_full[i], 1);
-      mbar_init(&o_empty[i], 4);
+      mbar_init(&o_empty[i], 8);
     }
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, 512);
+  if (warp == 3) {
+    uint4* o4 = reinterpret_cast<uint4*>(sOnes);
+    for (int i = lane; i < int(Cfg::ONES_BYTES / 16); i += 32) o4[i] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
+    fence_proxy_async_smem();
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -146,11 +158,16 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
           mma_ss(d_tmem, make_sdesc(qs + k * 32, 16, Cfg::SBO, Cfg::LAYOUT),
                  make_sdesc(ks + k * 32, 16, Cfg::SBO, Cfg::LAYOUT), idesc_qk, k > 0);
       };
+      constexpr uint32_t idesc_sum = make_idesc_bf16(128, 16, 0, 0);
+      const uint64_t ones_desc = make_sdesc(smem_u32(sOnes), 16, 1024, 2);
+      // O[:, 0:D] += P V ; O[:, D:D+16] += P 1 (row sums of the bf16 P, on the tensor core)
       auto issue_pv = [&](uint32_t d_tmem, uint32_t p_tmem, uint32_t vs, uint32_t acc) {
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
+        for (int kk = 0; kk < 8; ++kk) {
           mma_ts(d_tmem, p_tmem + kk * 8, make_sdesc(vs + kk * 16 * Cfg::ROW_BYTES, 16, Cfg::SBO, Cfg::LAYOUT),
                  idesc_pv, (acc | kk) != 0);
+          mma_ts(d_tmem + D, p_tmem + kk * 8, ones_desc, idesc_sum, (acc | kk) != 0);
+        }
       };
       const uint32_t S0 = tmem, S1 = tmem + 128, O0 = tmem + 256, O1 = tmem + 384;
       uint32_t c = 0;
@@ -210,12 +227,18 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ softmax / epilogue
-    const int tile = (warp - 4) / 4;  // Q tile handled by this warpgroup
+    // 4 warpgroups: (tile, half) = Q tile 0/1 x score columns 0-63 / 64-127 of the same rows;
+    // the two halves of a tile exchange their partial row maxima through shared memory.
+    const int sw = warp - 4;
+    const int tile = sw >> 3;
+    const int half = (sw >> 2) & 1;
     const int wl = warp & 3;          // TMEM lane quarter
     const int r = wl * 32 + lane;     // row within the Q tile
     const uint32_t lane_off = uint32_t(wl * 32) << 16;
     const uint32_t S_addr = tmem + lane_off + tile * 128;
     const uint32_t O_addr = tmem + lane_off + 256 + tile * 128;
+    float* my_max = xmax + (tile * 2 + half) * 128;
+    const float* other_max = xmax + (tile * 2 + (half ^ 1)) * 128;
     const float sl2 = a.scale_log2;
     uint32_t sph = 0, oph = 0;
     for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
@@ -224,83 +247,112 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
       const int s = rem / a.q_blocks;
       const int qb = rem - s * a.q_blocks;
       const int q_local = qb * 256 + tile * 128 + r;
-      float m_run = -INFINITY, l_run = 0.f;
+      float m_run = -INFINITY;
       for (int j = 0; j < nkv; ++j) {
         mbar_wait(&s_full[tile], sph);
         sph ^= 1;
         tc_fence_after();
-        uint32_t sr[128];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) tmem_ld32(S_addr + 32 * c, sr + 32 * c);
+        uint32_t sr[64];
+        tmem_ld32(S_addr + 64 * half, sr);
+        tmem_ld32(S_addr + 64 * half + 32, sr + 32);
         tmem_wait_ld();
-        const int valid = a.Lk - 128 * j;
-        if (valid < 128) {
+        const int valid = a.Lk - 128 * j - 64 * half;
+        if (valid < 64) {
 #pragma unroll
-          for (int c = 0; c < 128; ++c)
+          for (int c = 0; c < 64; ++c)
             if (c >= valid) sr[c] = 0xff800000u;  // -inf
         }
-        float mx = __uint_as_float(sr[0]);
+        // partial row max over 64 columns: 4 independent FMNMX3 chains + tree
+        float mq[4];
 #pragma unroll
-        for (int c = 1; c < 128; ++c) mx = fmaxf(mx, __uint_as_float(sr[c]));
+        for (int u = 0; u < 4; ++u) mq[u] = fmaxf(__uint_as_float(sr[u]), __uint_as_float(sr[u + 4]));
+#pragma unroll
+        for (int c = 8; c < 64; c += 8)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) mq[u] = max3(mq[u], __uint_as_float(sr[c + u]), __uint_as_float(sr[c + 4 + u]));
+        const float pmax = fmaxf(max3(mq[0], mq[1], mq[2]), mq[3]);
+        my_max[r] = pmax;
+        named_bar_sync(1 + tile, 256);   // both halves loaded S and published their maxima
+        const float mx = fmaxf(pmax, other_max[r]);
         const float m_new = mx * sl2;
         const bool need = m_new > m_run + RESCALE_THRESHOLD;
         const float alpha = need ? ex2(m_run - m_new) : 1.0f;
         if (need) m_run = m_new;
-        float sum = 0.f;
+        const uint64_t SL2 = f2_pack(sl2, sl2);
+        const uint64_t NEGM = f2_pack(-m_run, -m_run);
+        uint32_t pk[32];
 #pragma unroll
-        for (int half = 0; half < 2; ++half) {
-          uint32_t pk[32];
-#pragma unroll
-          for (int c = 0; c < 32; ++c) {
-            const float p0 = ex2(fmaf(__uint_as_float(sr[64 * half + 2 * c]), sl2, -m_run));
-            const float p1 = ex2(fmaf(__uint_as_float(sr[64 * half + 2 * c + 1]), sl2, -m_run));
-            sum += p0 + p1;
-            pk[c] = pack_bf16(p0, p1);
+        for (int c = 0; c < 32; ++c) {
+          // x = s * scale*log2(e) - m for two columns with one FFMA2
+          const uint64_t x = f2_fma(f2_pack(__uint_as_float(sr[2 * c]), __uint_as_float(sr[2 * c + 1])), SL2, NEGM);
+          float x0, x1, p0, p1;
+          f2_unpack(x, x0, x1);
+          if ((c & 7) >= 8 - EMU_PAIRS_OF_8) {  // part of the exps on the FMA pipe
+            ex2_poly2(x0, x1, p0, p1);
+          } else {
+            p0 = ex2(x0);
+            p1 = ex2(x1);
           }
-          tmem_st32(S_addr + 32 * half, pk);
+          pk[c] = pack_bf16(p0, p1);
         }
-        // lazy O correction (warp-uniform: tcgen05.ld/st are .sync.aligned); PV(j-1) has
-        // completed because s_full(j) was committed after it.
+        // P (bf16 pairs) overwrites S columns [32*half, 32*half + 32): the other half has already
+        // loaded its S columns (named barrier above)
+        tmem_st32(S_addr + 32 * half, pk);
+        // lazy O / row-sum correction (warp-uniform); PV(j-1) completed before s_full(j)
         if (__any_sync(0xffffffff, need) && j > 0) {
+          if (half == 0) {
+            uint32_t orr[D];
 #pragma unroll
-          for (int c0 = 0; c0 < D; c0 += 32) {
-            uint32_t orr[32];
-            tmem_ld32(O_addr + c0, orr);
+            for (int c0 = 0; c0 < D; c0 += 32) tmem_ld32(O_addr + c0, orr + c0);
             tmem_wait_ld();
 #pragma unroll
-            for (int c = 0; c < 32; ++c) orr[c] = __float_as_uint(__uint_as_float(orr[c]) * alpha);
-            tmem_st32(O_addr + c0, orr);
+            for (int c = 0; c < D; ++c) orr[c] = __float_as_uint(__uint_as_float(orr[c]) * alpha);
+#pragma unroll
+            for (int c0 = 0; c0 < D; c0 += 32) tmem_st32(O_addr + c0, orr + c0);
+          } else {
+            uint32_t orr[16];
+            tmem_ld16(O_addr + D, orr);
+            tmem_wait_ld();
+#pragma unroll
+            for (int c = 0; c < 16; ++c) orr[c] = __float_as_uint(__uint_as_float(orr[c]) * alpha);
+            tmem_st16(O_addr + D, orr);
           }
         }
-        l_run = l_run * alpha + sum;
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[tile]);
       }
-      // ---- epilogue: O / l -> bf16
+      // ---- epilogue: O[:, half*D/2 : +D/2] / l -> bf16
       mbar_wait(&o_full[tile], oph);
       oph ^= 1;
       tc_fence_after();
-      uint32_t orr[D];
-#pragma unroll
-      for (int c0 = 0; c0 < D; c0 += 32) tmem_ld32(O_addr + c0, orr + c0);
+      constexpr int DH = D / 2;
+      uint32_t orr[DH];
+      uint32_t lr[16];
+      if constexpr (DH == 32) {
+        tmem_ld32(O_addr + half * DH, orr);
+      } else {
+        tmem_ld16(O_addr + half * DH, orr);
+      }
+      tmem_ld16(O_addr + D, lr);
       tmem_wait_ld();
+      const float l_run = __uint_as_float(lr[0]);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&o_empty[tile]);
       if (q_local < a.Lq) {
         const float inv = 1.0f / l_run;
         const int64_t orow = (int64_t)s * a.Lq + q_local;
-        uint4* dst = reinterpret_cast<uint4*>(a.out + orow * a.ldo + h * D);
+        uint4* dst = reinterpret_cast<uint4*>(a.out + orow * a.ldo + h * D + half * DH);
 #pragma unroll
-        for (int c = 0; c < D / 8; ++c) {
+        for (int c = 0; c < DH / 8; ++c) {
 #define VX_O(i) (__uint_as_float(orr[8 * c + i]) * inv)
           dst[c] = make_uint4(pack_bf16(VX_O(0), VX_O(1)), pack_bf16(VX_O(2), VX_O(3)),
                               pack_bf16(VX_O(4), VX_O(5)), pack_bf16(VX_O(6), VX_O(7)));
 #undef VX_O
         }
-        if (a.lse) a.lse[h * a.Tq + orow] = (m_run + __log2f(l_run)) * 0.69314718055994531f;
+        if (a.lse && half == 0) a.lse[h * a.Tq + orow] = (m_run + __log2f(l_run)) * 0.69314718055994531f;
       }
     }
   }
@@ -312,14 +364,14 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
   }
 }
 
-template <int D>
+template <int D, int EMU>
 static int launch_fmha(const void* q, const void* k, const void* v, const AttnArgs& args, cudaStream_t st) {
   using Cfg = AttnCfg<D>;
   CUtensorMap tq, tk, tv;
   if (!make_tmap_2d_bf16(&tq, q, (uint64_t)args.H * args.Tq, D, D, 128, D, Cfg::SWIZZLE)) return VX_E_ARG;
   if (!make_tmap_2d_bf16(&tk, k, (uint64_t)args.H * args.Tk, D, D, 128, D, Cfg::SWIZZLE)) return VX_E_ARG;
   if (!make_tmap_2d_bf16(&tv, v, (uint64_t)args.H * args.Tk, D, D, 128, D, Cfg::SWIZZLE)) return VX_E_ARG;
-  auto kern = fmha_kernel<D>;
+  auto kern = fmha_kernel<D, EMU>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
@@ -359,5 +411,19 @@ extern "C" int vx_attention(const void* q, const void* k, const void* v, void* o
   a.ldo = ldo;
   a.lse = lse;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  return D == 64 ? launch_fmha<64>(q, k, v, a, st) : launch_fmha<32>(q, k, v, a, st);
+  static int emu = [] {
+    const char* e = getenv("VX_FMHA_EMU");  // diagnostic: exp pairs (of 8) on the FMA pipe
+    return e ? atoi(e) : 3;
+  }();
+  if (D == 64) {
+    switch (emu) {
+      case 0: return launch_fmha<64, 0>(q, k, v, a, st);
+      case 2: return launch_fmha<64, 2>(q, k, v, a, st);
+      case 3: return launch_fmha<64, 3>(q, k, v, a, st);
+      case 5: return launch_fmha<64, 5>(q, k, v, a, st);
+      case 4: return launch_fmha<64, 4>(q, k, v, a, st);
+      default: return launch_fmha<64, 3>(q, k, v, a, st);
+    }
+  }
+  return launch_fmha<32, 3>(q, k, v, a, st);
 }

@@ -7,8 +7,9 @@ Precision policy ("bf16 except MLP in heads", `PAPER.md:81`):
   * DPT heads: LayerNorm + the four 1x1 projections run on the vx kernels
     (LN + tcgen05 GEMM, NHWC output); the conv / conv-transpose / bilinear
     stack runs in bf16 channels-last (cuDNN library kernels — a native
-    implicit-GEMM conv is the next §8 row); the final
-    output_conv2 and the activations run in fp32.
+    implicit-GEMM conv is the next §8 row); bilinear resizes
+    (+ fused pos-embed add) run on vx_upsample_bilinear; the final per-pixel
+    1x1 output conv and the activations run in fp32.
   * heads are evaluated `head_chunk` frames at a time (VGGT-X chunking).
 """
 from __future__ import annotations
@@ -115,12 +116,12 @@ class DPTHeadDevice:
         H = Wd = cfg.img_size
         self.proj_w = [W[f"{head}projects.{i}.weight"].reshape(-1, D).contiguous() for i in range(4)]
         self.pos_small = [dpt_pos_embed(oc, g, g, Wd, H).to(dev) for oc in cfg.dpt_out_channels]
-        self.pos_full = dpt_pos_embed(cfg.dpt_features // 2, H, Wd, Wd, H).to(dev).permute(2, 0, 1)[None].contiguous()
+        self.pos_full = dpt_pos_embed(cfg.dpt_features // 2, H, Wd, Wd, H).to(dev).to(torch.bfloat16).contiguous()
         # bf16 channels-last conv weights
         self.cw = {}
         for k, v in W.t.items():
             if k.startswith(head) and v.dim() == 4 and "projects" not in k:
-                if "output_conv2" in k:
+                if "output_conv2.2" in k:
                     self.cw[k] = v.float()
                 else:
                     self.cw[k] = v.to(torch.bfloat16).contiguous(memory_format=torch.channels_last)
@@ -142,11 +143,18 @@ class DPTHeadDevice:
         if x1 is not None:
             out = out + self._rcu(x1, name + ".resConfUnit1")
         out = self._rcu(out, name + ".resConfUnit2")
-        if size is None:
-            out = F.interpolate(out, scale_factor=2, mode="bilinear", align_corners=True)
-        else:
-            out = F.interpolate(out, size=size, mode="bilinear", align_corners=True)
+        h, w = out.shape[2:]
+        size = (2 * h, 2 * w) if size is None else tuple(size)
+        out = self._upsample(out, size)
         return self._conv(out, name + ".out_conv")
+
+    @staticmethod
+    def _upsample(x, size, add=None):
+        """bilinear align_corners=True on channels-last bf16 via vx_upsample_bilinear."""
+        nhwc = x.permute(0, 2, 3, 1)
+        if not nhwc.is_contiguous():
+            nhwc = nhwc.contiguous()
+        return ops.upsample_bilinear(nhwc, size, add=add).permute(0, 3, 1, 2)
 
     def forward_chunk(self, layers: List[torch.Tensor]):
         """layers: 4 x (F, N, 2C) bf16 kept tokens -> (F, H, W, odim) fp32 pre-activation."""
@@ -177,10 +185,9 @@ class DPTHeadDevice:
         out = self._fusion(sc + "refinenet2", out, l2, size=l1.shape[2:])
         out = self._fusion(sc + "refinenet1", out, l1, size=None)
         out = self._conv(out, sc + "output_conv1")
-        out = F.interpolate(out, size=(Hh, Ww), mode="bilinear", align_corners=True)
-        out = out.float() + self.pos_full
-        out = F.relu(self._conv(out, sc + "output_conv2.0", dtype=torch.float32))
-        out = self._conv(out, sc + "output_conv2.2", padding=0, dtype=torch.float32)
+        out = self._upsample(out, (Hh, Ww), add=self.pos_full)        # + UV pos-embed, fused
+        out = F.relu(self._conv(out, sc + "output_conv2.0"))
+        out = self._conv(out.float(), sc + "output_conv2.2", padding=0, dtype=torch.float32)
         return out.permute(0, 2, 3, 1)
 
     def __call__(self, kept: Dict[int, torch.Tensor], out_pred: torch.Tensor, out_conf: torch.Tensor,

@@ -36,8 +36,8 @@ class Epilogue(ctypes.Structure):
     ]
 
 
-EXPORTED_SYMBOLS = ("vx_gemm", "vx_attention", "vx_layernorm", "vx_patchify",
-                    "vx_special_tokens", "vx_num_sms", "vx_last_error", "vx_version")
+EXPORTED_SYMBOLS = ("vx_gemm", "vx_attention", "vx_layernorm", "vx_patchify", "vx_special_tokens",
+                    "vx_upsample_bilinear", "vx_num_sms", "vx_last_error", "vx_version")
 
 _lib = None
 
@@ -57,9 +57,11 @@ def load_library(path: os.PathLike | None = None) -> ctypes.CDLL:
     lib.vx_layernorm.argtypes = [_vp, _i32, _i64, _vp, _i32, _i64, _vp, _vp, _i32, _i32, _f32, _vp]
     lib.vx_patchify.argtypes = [_vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp]
     lib.vx_special_tokens.argtypes = [_vp, _vp, _i32, _i32, _i32, _i32, _vp]
+    lib.vx_upsample_bilinear.argtypes = [_vp, _i32, _i32, _i32, _i32, _vp, _i32, _i32, _vp, _vp]
     lib.vx_last_error.restype = ctypes.c_char_p
     lib.vx_version.restype = ctypes.c_char_p
-    for name in ("vx_gemm", "vx_attention", "vx_layernorm", "vx_patchify", "vx_special_tokens", "vx_num_sms"):
+    for name in ("vx_gemm", "vx_attention", "vx_layernorm", "vx_patchify", "vx_special_tokens",
+                 "vx_upsample_bilinear", "vx_num_sms"):
         getattr(lib, name).restype = _i32
     if path is None:
         _lib = lib
@@ -213,3 +215,22 @@ def special_tokens(x, tokens, S, tpf):
     _check(_lib.vx_special_tokens(_ptr(x), _ptr(tokens.contiguous()), S, tpf, ntok, C, _stream()),
            "vx_special_tokens")
     return x
+
+
+def upsample_bilinear(x: torch.Tensor, size, add=None, out=None):
+    """NHWC bf16 [F, h, w, C] -> [F, H, W, C], align_corners=True, + optional [H, W, C] add."""
+    load_library()
+    _req(x, torch.bfloat16, "x")
+    if not x.is_contiguous():
+        raise ValueError("upsample_bilinear: x must be contiguous NHWC")
+    F_, h, w, C = x.shape
+    H, W = size
+    if out is None:
+        out = torch.empty(F_, H, W, C, device=x.device, dtype=torch.bfloat16)
+    if add is not None:
+        _req(add, torch.bfloat16, "add")
+        if tuple(add.shape) != (H, W, C) or not add.is_contiguous():
+            raise ValueError("upsample_bilinear: add must be contiguous [H, W, C]")
+    _check(_lib.vx_upsample_bilinear(_ptr(x), F_, h, w, C, _ptr(out), H, W, _ptr(add), _stream()),
+           "vx_upsample_bilinear")
+    return out

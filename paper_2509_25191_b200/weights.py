@@ -31,8 +31,8 @@ from .config import VGGTConfig
 FP32_PREFIXES = (
     "camera_head.pose_branch.",
     "camera_head.embed_pose.",
-    "depth_head.scratch.output_conv2.",
-    "point_head.scratch.output_conv2.",
+    "depth_head.scratch.output_conv2.2.",
+    "point_head.scratch.output_conv2.2.",
 )
 
 
