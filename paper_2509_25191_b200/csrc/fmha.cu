@@ -8,17 +8,24 @@
 // (head, sequence); persistent grid over units, head-major so concurrently
 // running CTAs share K/V through L2.
 //
-// Warp roles (384 threads):
+// TMEM (512 columns), per Q tile i:  S_i [128 fp32] | P_i [64 = 128 bf16] | O_i [D fp32].
+// P has its own columns, so the MMA warp computes S_i(j+1) while the softmax
+// warps are still turning S_i(j) into P_i(j): the tensor core runs one KV tile
+// ahead of the softmax (aliasing P onto S, as in the first version, serialised them).
+//
+// Warp roles (640 threads):
 //   w0      TMA producer: Q tiles once per unit, K/V tiles through a KST-stage ring
-//   w1      tcgen05.mma issuer (one lane): S_i = Q_i K^T (SS), O_i += P_i V (TS, P in TMEM)
-//   w2      TMEM allocator (512 columns: S0 | S1 | O0 | O1, P_i aliases S_i)
-//   w4..w7  softmax + epilogue for Q tile 0, w8..w11 for Q tile 1
-//           (thread = one query row = one TMEM lane: row max / sum are thread-local;
-//            lazy O rescaling only when the running max grows by > 2^8)
-//   (v4: each Q tile's 128 score columns are split over two warpgroups, 16 softmax warps in
-//    total, partial row maxima exchanged through shared memory + a named barrier)
-// MMA issue order per KV tile j:  PV_0(j), S_0(j+1), PV_1(j), S_1(j+1), so each
-// softmax warpgroup's exp work overlaps the other tile's tensor-core work.
+//   w1      tcgen05.mma issuer (one lane): S_i = Q_i K^T (SS), O_i += P_i V (TS: P from TMEM)
+//   w2      TMEM allocator
+//   w4..w19 softmax + epilogue: 4 warpgroups = (Q tile) x (score columns 0-63 | 64-127);
+//           thread = one query row (TMEM lane); partial row maxima / sums of the two
+//           column halves are exchanged through shared memory.
+// Softmax arithmetic: x = s*scale*log2e - m with FFMA2, 1/4 of the exp2 on the FMA pipe
+// (packed degree-3 polynomial), the rest on MUFU; lazy O rescaling (only when the
+// running max grows by > 2^8); row sums with packed FADD2.
+//
+// MMA issue order per KV tile j:  S_0(j+1), S_1(j+1) (as soon as S_i(j) was loaded),
+// PV_0(j) (when P_0(j) is written), PV_1(j).
 #include <math.h>
 #include <stdlib.h>
 
@@ -46,12 +53,18 @@ struct AttnCfg {
   static constexpr int SWIZZLE = D == 64 ? 128 : 64;
   static constexpr uint32_t LAYOUT = D == 64 ? 2 : 4;  // SWIZZLE_128B / SWIZZLE_64B
   static constexpr uint32_t SBO = 8 * ROW_BYTES;       // 8-row core-matrix group
-  static constexpr uint32_t ONES_BYTES = 2048;  // 16 x 64 bf16 ones (row-sum B operand)
-  static constexpr uint32_t SMEM = (2 + 2 * KST) * TILE_BYTES + ONES_BYTES + 1024 + 512 + 2048;
+  static constexpr uint32_t BAR_BYTES = 512;
+  static constexpr uint32_t XCH_BYTES = 4096;          // [2 parity][2 tiles][2 halves][128] fp32
+  static constexpr uint32_t SMEM = (2 + 2 * KST) * TILE_BYTES + 1024 + BAR_BYTES + XCH_BYTES;
 };
 
-constexpr int ATTN_THREADS = 640;  // 4 control warps + 4 softmax warpgroups
+constexpr int ATTN_THREADS = 640;          // 4 control warps + 4 softmax warpgroups
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
+
+// TMEM column offsets of Q tile i
+__host__ __device__ constexpr uint32_t tm_S(int i) { return i * 256; }
+__host__ __device__ constexpr uint32_t tm_P(int i) { return i * 256 + 128; }
+__host__ __device__ constexpr uint32_t tm_O(int i) { return i * 256 + 192; }
 
 // EMU_PAIRS_OF_8: of every 8 exp pairs, this many use the FMA-pipe polynomial
 template <int D, int EMU_PAIRS_OF_8>
@@ -65,20 +78,20 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
   uint8_t* sQ = smem;                                 // 2 tiles
   uint8_t* sK = sQ + 2 * Cfg::TILE_BYTES;             // KST tiles
   uint8_t* sV = sK + KST * Cfg::TILE_BYTES;           // KST tiles
-  uint8_t* sOnes = sV + KST * Cfg::TILE_BYTES;        // 2 KB of bf16 1.0
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sOnes + Cfg::ONES_BYTES);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sV + KST * Cfg::TILE_BYTES);
   uint64_t* q_full = bar;
   uint64_t* q_empty = bar + 1;
   uint64_t* k_full = bar + 2;
   uint64_t* k_empty = k_full + KST;
   uint64_t* v_full = k_empty + KST;
   uint64_t* v_empty = v_full + KST;
-  uint64_t* s_full = v_empty + KST;  // [2]
-  uint64_t* p_full = s_full + 2;     // [2]
-  uint64_t* o_full = p_full + 2;     // [2]
-  uint64_t* o_empty = o_full + 2;    // [2]
+  uint64_t* s_full = v_empty + KST;  // [2] MMA -> softmax: S_i(j) computed
+  uint64_t* s_free = s_full + 2;     // [2] softmax -> MMA: S_i(j) loaded, buffer reusable
+  uint64_t* p_full = s_free + 2;     // [2] softmax -> MMA: P_i(j) written (O rescaled)
+  uint64_t* p_free = p_full + 2;     // [2] MMA -> softmax: PV_i(j) done (P reusable, O stable)
+  uint64_t* o_empty = p_free + 2;    // [2] softmax -> MMA: O_i read by the epilogue
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
-  float* xmax = reinterpret_cast<float*>(bar + 64);  // [2 tiles][2 halves][128 rows] partial maxima
+  float* xch = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bar) + Cfg::BAR_BYTES);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -97,18 +110,14 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
+      mbar_init(&s_free[i], 8);
       mbar_init(&p_full[i], 8);
-      mbar_init(&o_full[i], 1);
+      mbar_init(&p_free[i], 1);
       mbar_init(&o_empty[i], 8);
     }
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, 512);
-  if (warp == 3) {
-    uint4* o4 = reinterpret_cast<uint4*>(sOnes);
-    for (int i = lane; i < int(Cfg::ONES_BYTES / 16); i += 32) o4[i] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
-    fence_proxy_async_smem();
-  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -152,95 +161,100 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
       constexpr uint32_t idesc_qk = make_idesc_bf16(128, 128, 0, 0);
       constexpr uint32_t idesc_pv = make_idesc_bf16(128, D, 0, 1);
       const uint32_t q0 = smem_u32(sQ), q1 = q0 + Cfg::TILE_BYTES;
-      auto issue_qk = [&](uint32_t d_tmem, uint32_t qs, uint32_t ks) {
+      auto issue_qk = [&](int i, uint32_t ks) {
+        const uint32_t qs = i ? q1 : q0;
 #pragma unroll
         for (int k = 0; k < D / 16; ++k)
-          mma_ss(d_tmem, make_sdesc(qs + k * 32, 16, Cfg::SBO, Cfg::LAYOUT),
+          mma_ss(tmem + tm_S(i), make_sdesc(qs + k * 32, 16, Cfg::SBO, Cfg::LAYOUT),
                  make_sdesc(ks + k * 32, 16, Cfg::SBO, Cfg::LAYOUT), idesc_qk, k > 0);
       };
-      constexpr uint32_t idesc_sum = make_idesc_bf16(128, 16, 0, 0);
-      const uint64_t ones_desc = make_sdesc(smem_u32(sOnes), 16, 1024, 2);
-      // O[:, 0:D] += P V ; O[:, D:D+16] += P 1 (row sums of the bf16 P, on the tensor core)
-      auto issue_pv = [&](uint32_t d_tmem, uint32_t p_tmem, uint32_t vs, uint32_t acc) {
+      auto issue_pv = [&](int i, uint32_t vs, uint32_t acc) {
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          mma_ts(d_tmem, p_tmem + kk * 8, make_sdesc(vs + kk * 16 * Cfg::ROW_BYTES, 16, Cfg::SBO, Cfg::LAYOUT),
-                 idesc_pv, (acc | kk) != 0);
-          mma_ts(d_tmem + D, p_tmem + kk * 8, ones_desc, idesc_sum, (acc | kk) != 0);
-        }
+        for (int kk = 0; kk < 8; ++kk)
+          mma_ts(tmem + tm_O(i), tmem + tm_P(i) + kk * 8,
+                 make_sdesc(vs + kk * 16 * Cfg::ROW_BYTES, 16, Cfg::SBO, Cfg::LAYOUT), idesc_pv, (acc | kk) != 0);
       };
-      const uint32_t S0 = tmem, S1 = tmem + 128, O0 = tmem + 256, O1 = tmem + 384;
-      uint32_t c = 0;
-      uint32_t n = 0;
-      uint32_t pph0 = 0, pph1 = 0;
+      uint32_t c = 0;  // global K/V tile counter
+      uint32_t n = 0;  // local unit counter
+      uint32_t sfree_ph = 0, pfull_ph = 0;
       for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++n) {
         mbar_wait(q_full, n & 1);
         tc_fence_after();
-        {
+        {  // S(0) of both tiles; the S buffers were released by the previous unit's last s_free
           const uint32_t st = c % KST, ph = (c / KST) & 1;
           mbar_wait(&k_full[st], ph);
           tc_fence_after();
           const uint32_t ks = smem_u32(sK + st * Cfg::TILE_BYTES);
-          issue_qk(S0, q0, ks);
+          if (n > 0) mbar_wait(&s_free[0], sfree_ph);
+          tc_fence_after();
+          issue_qk(0, ks);
           mma_commit(&s_full[0]);
-          issue_qk(S1, q1, ks);
+          if (n > 0) {
+            mbar_wait(&s_free[1], sfree_ph);
+            sfree_ph ^= 1;
+          }
+          tc_fence_after();
+          issue_qk(1, ks);
           mma_commit(&s_full[1]);
           mma_commit(&k_empty[st]);
           if (nkv == 1) mma_commit(q_empty);
         }
         for (int j = 0; j < nkv; ++j, ++c) {
           const uint32_t st = c % KST, ph = (c / KST) & 1;
-          const uint32_t vs = smem_u32(sV + st * Cfg::TILE_BYTES);
-          const bool has_next = j + 1 < nkv;
-          const uint32_t nst = (c + 1) % KST, nph = ((c + 1) / KST) & 1;
-          const uint32_t nks = smem_u32(sK + nst * Cfg::TILE_BYTES);
-          mbar_wait(&v_full[st], ph);
-          // ---- tile 0
-          if (j == 0) mbar_wait(&o_empty[0], (n & 1) ^ 1);
-          mbar_wait(&p_full[0], pph0);
-          pph0 ^= 1;
-          tc_fence_after();
-          issue_pv(O0, S0, vs, j > 0);
-          if (!has_next) mma_commit(&o_full[0]);
-          if (has_next) {
+          if (j + 1 < nkv) {  // run one KV tile ahead: S(j+1) as soon as S(j) has been loaded
+            const uint32_t nst = (c + 1) % KST, nph = ((c + 1) / KST) & 1;
             mbar_wait(&k_full[nst], nph);
+            const uint32_t nks = smem_u32(sK + nst * Cfg::TILE_BYTES);
+            mbar_wait(&s_free[0], sfree_ph);
             tc_fence_after();
-            issue_qk(S0, q0, nks);
+            issue_qk(0, nks);
             mma_commit(&s_full[0]);
-          }
-          // ---- tile 1
-          if (j == 0) mbar_wait(&o_empty[1], (n & 1) ^ 1);
-          mbar_wait(&p_full[1], pph1);
-          pph1 ^= 1;
-          tc_fence_after();
-          issue_pv(O1, S1, vs, j > 0);
-          mma_commit(&v_empty[st]);
-          if (!has_next) mma_commit(&o_full[1]);
-          if (has_next) {
-            issue_qk(S1, q1, nks);
+            mbar_wait(&s_free[1], sfree_ph);
+            sfree_ph ^= 1;
+            tc_fence_after();
+            issue_qk(1, nks);
             mma_commit(&s_full[1]);
             mma_commit(&k_empty[nst]);
             if (j + 2 == nkv) mma_commit(q_empty);
           }
+          const uint32_t vs = smem_u32(sV + st * Cfg::TILE_BYTES);
+          mbar_wait(&v_full[st], ph);
+          if (j == 0) {  // the previous unit's epilogue must have read O
+            mbar_wait(&o_empty[0], (n & 1) ^ 1);
+            mbar_wait(&o_empty[1], (n & 1) ^ 1);
+          }
+          mbar_wait(&p_full[0], pfull_ph);
+          tc_fence_after();
+          issue_pv(0, vs, j > 0);
+          mma_commit(&p_free[0]);
+          mbar_wait(&p_full[1], pfull_ph);
+          pfull_ph ^= 1;
+          tc_fence_after();
+          issue_pv(1, vs, j > 0);
+          mma_commit(&p_free[1]);
+          mma_commit(&v_empty[st]);
         }
       }
     }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ softmax / epilogue
-    // 4 warpgroups: (tile, half) = Q tile 0/1 x score columns 0-63 / 64-127 of the same rows;
-    // the two halves of a tile exchange their partial row maxima through shared memory.
+    constexpr int DH = D / 2;
     const int sw = warp - 4;
     const int tile = sw >> 3;
     const int half = (sw >> 2) & 1;
     const int wl = warp & 3;          // TMEM lane quarter
     const int r = wl * 32 + lane;     // row within the Q tile
     const uint32_t lane_off = uint32_t(wl * 32) << 16;
-    const uint32_t S_addr = tmem + lane_off + tile * 128;
-    const uint32_t O_addr = tmem + lane_off + 256 + tile * 128;
-    float* my_max = xmax + (tile * 2 + half) * 128;
-    const float* other_max = xmax + (tile * 2 + (half ^ 1)) * 128;
+    const uint32_t S_addr = tmem + lane_off + tm_S(tile) + 64 * half;
+    const uint32_t P_addr = tmem + lane_off + tm_P(tile) + 32 * half;
+    const uint32_t Oh_addr = tmem + lane_off + tm_O(tile) + DH * half;
+    // exchange slots: [parity][tile][half][row]
+    float* const xbase = xch + tile * 256 + r;
     const float sl2 = a.scale_log2;
-    uint32_t sph = 0, oph = 0;
+    const uint64_t SL2 = f2_pack(sl2, sl2);
+    uint32_t sph = 0;     // s_full parity
+    uint32_t pv_cnt = 0;  // p_free waits (parity)
+    uint32_t xpar = 0;    // exchange buffer parity
     for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
       const int h = u / per_head;
       const int rem = u - h * per_head;
@@ -248,14 +262,18 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
       const int qb = rem - s * a.q_blocks;
       const int q_local = qb * 256 + tile * 128 + r;
       float m_run = -INFINITY;
+      float l_run = 0.f;  // partial row sum over this half's columns
       for (int j = 0; j < nkv; ++j) {
         mbar_wait(&s_full[tile], sph);
         sph ^= 1;
         tc_fence_after();
         uint32_t sr[64];
-        tmem_ld32(S_addr + 64 * half, sr);
-        tmem_ld32(S_addr + 64 * half + 32, sr + 32);
+        tmem_ld32(S_addr, sr);
+        tmem_ld32(S_addr + 32, sr + 32);
         tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_free[tile]);  // the S buffer may now receive S(j+1)
         const int valid = a.Lk - 128 * j - 64 * half;
         if (valid < 64) {
 #pragma unroll
@@ -265,25 +283,26 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
         // partial row max over 64 columns: 4 independent FMNMX3 chains + tree
         float mq[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) mq[u] = fmaxf(__uint_as_float(sr[u]), __uint_as_float(sr[u + 4]));
+        for (int q = 0; q < 4; ++q) mq[q] = fmaxf(__uint_as_float(sr[q]), __uint_as_float(sr[q + 4]));
 #pragma unroll
         for (int c = 8; c < 64; c += 8)
 #pragma unroll
-          for (int u = 0; u < 4; ++u) mq[u] = max3(mq[u], __uint_as_float(sr[c + u]), __uint_as_float(sr[c + 4 + u]));
+          for (int q = 0; q < 4; ++q) mq[q] = max3(mq[q], __uint_as_float(sr[c + q]), __uint_as_float(sr[c + 4 + q]));
         const float pmax = fmaxf(max3(mq[0], mq[1], mq[2]), mq[3]);
-        my_max[r] = pmax;
-        named_bar_sync(1 + tile, 256);   // both halves loaded S and published their maxima
-        const float mx = fmaxf(pmax, other_max[r]);
+        float* xs = xbase + xpar * 512;
+        xs[half * 128] = pmax;
+        named_bar_sync(1 + tile, 256);
+        const float mx = fmaxf(pmax, xs[(half ^ 1) * 128]);
+        xpar ^= 1;
         const float m_new = mx * sl2;
         const bool need = m_new > m_run + RESCALE_THRESHOLD;
         const float alpha = need ? ex2(m_run - m_new) : 1.0f;
         if (need) m_run = m_new;
-        const uint64_t SL2 = f2_pack(sl2, sl2);
         const uint64_t NEGM = f2_pack(-m_run, -m_run);
         uint32_t pk[32];
+        uint64_t acc[4] = {0, 0, 0, 0};
 #pragma unroll
         for (int c = 0; c < 32; ++c) {
-          // x = s * scale*log2(e) - m for two columns with one FFMA2
           const uint64_t x = f2_fma(f2_pack(__uint_as_float(sr[2 * c]), __uint_as_float(sr[2 * c + 1])), SL2, NEGM);
           float x0, x1, p0, p1;
           f2_unpack(x, x0, x1);
@@ -293,30 +312,31 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
             p0 = ex2(x0);
             p1 = ex2(x1);
           }
+          acc[c & 3] = f2_add(acc[c & 3], f2_pack(p0, p1));
           pk[c] = pack_bf16(p0, p1);
         }
-        // P (bf16 pairs) overwrites S columns [32*half, 32*half + 32): the other half has already
-        // loaded its S columns (named barrier above)
-        tmem_st32(S_addr + 32 * half, pk);
-        // lazy O / row-sum correction (warp-uniform); PV(j-1) completed before s_full(j)
-        if (__any_sync(0xffffffff, need) && j > 0) {
-          if (half == 0) {
-            uint32_t orr[D];
+        {
+          float a0, a1, b0, b1;
+          f2_unpack(f2_add(acc[0], acc[1]), a0, a1);
+          f2_unpack(f2_add(acc[2], acc[3]), b0, b1);
+          l_run = l_run * alpha + ((a0 + a1) + (b0 + b1));
+        }
+        // P_i(j) may overwrite P_i(j-1) only once PV_i(j-1) has completed (this also makes O stable)
+        if (j > 0) {
+          mbar_wait(&p_free[tile], pv_cnt & 1);
+          ++pv_cnt;
+          tc_fence_after();
+        }
+        tmem_st32(P_addr, pk);
+        if (__any_sync(0xffffffff, need) && j > 0) {  // lazy O correction, each half its D/2 columns
+          uint32_t orr[DH];
+          if constexpr (DH == 32) tmem_ld32(Oh_addr, orr);
+          else tmem_ld16(Oh_addr, orr);
+          tmem_wait_ld();
 #pragma unroll
-            for (int c0 = 0; c0 < D; c0 += 32) tmem_ld32(O_addr + c0, orr + c0);
-            tmem_wait_ld();
-#pragma unroll
-            for (int c = 0; c < D; ++c) orr[c] = __float_as_uint(__uint_as_float(orr[c]) * alpha);
-#pragma unroll
-            for (int c0 = 0; c0 < D; c0 += 32) tmem_st32(O_addr + c0, orr + c0);
-          } else {
-            uint32_t orr[16];
-            tmem_ld16(O_addr + D, orr);
-            tmem_wait_ld();
-#pragma unroll
-            for (int c = 0; c < 16; ++c) orr[c] = __float_as_uint(__uint_as_float(orr[c]) * alpha);
-            tmem_st16(O_addr + D, orr);
-          }
+          for (int c = 0; c < DH; ++c) orr[c] = __float_as_uint(__uint_as_float(orr[c]) * alpha);
+          if constexpr (DH == 32) tmem_st32(Oh_addr, orr);
+          else tmem_st16(Oh_addr, orr);
         }
         tmem_wait_st();
         tc_fence_before();
@@ -324,25 +344,22 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
         if (lane == 0) mbar_arrive(&p_full[tile]);
       }
       // ---- epilogue: O[:, half*D/2 : +D/2] / l -> bf16
-      mbar_wait(&o_full[tile], oph);
-      oph ^= 1;
+      mbar_wait(&p_free[tile], pv_cnt & 1);  // last PV of this unit
+      ++pv_cnt;
       tc_fence_after();
-      constexpr int DH = D / 2;
       uint32_t orr[DH];
-      uint32_t lr[16];
-      if constexpr (DH == 32) {
-        tmem_ld32(O_addr + half * DH, orr);
-      } else {
-        tmem_ld16(O_addr + half * DH, orr);
-      }
-      tmem_ld16(O_addr + D, lr);
+      if constexpr (DH == 32) tmem_ld32(Oh_addr, orr);
+      else tmem_ld16(Oh_addr, orr);
+      float* xs = xbase + xpar * 512;
+      xs[half * 128] = l_run;
       tmem_wait_ld();
-      const float l_run = __uint_as_float(lr[0]);
       tc_fence_before();
-      __syncwarp();
+      named_bar_sync(1 + tile, 256);
+      const float l_tot = l_run + xs[(half ^ 1) * 128];
+      xpar ^= 1;
       if (lane == 0) mbar_arrive(&o_empty[tile]);
       if (q_local < a.Lq) {
-        const float inv = 1.0f / l_run;
+        const float inv = 1.0f / l_tot;
         const int64_t orow = (int64_t)s * a.Lq + q_local;
         uint4* dst = reinterpret_cast<uint4*>(a.out + orow * a.ldo + h * D + half * DH);
 #pragma unroll
@@ -352,7 +369,7 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
                               pack_bf16(VX_O(4), VX_O(5)), pack_bf16(VX_O(6), VX_O(7)));
 #undef VX_O
         }
-        if (a.lse && half == 0) a.lse[h * a.Tq + orow] = (m_run + __log2f(l_run)) * 0.69314718055994531f;
+        if (a.lse && half == 0) a.lse[h * a.Tq + orow] = (m_run + __log2f(l_tot)) * 0.69314718055994531f;
       }
     }
   }
@@ -413,17 +430,17 @@ extern "C" int vx_attention(const void* q, const void* k, const void* v, void* o
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   static int emu = [] {
     const char* e = getenv("VX_FMHA_EMU");  // diagnostic: exp pairs (of 8) on the FMA pipe
-    return e ? atoi(e) : 3;
+    return e ? atoi(e) : 2;
   }();
   if (D == 64) {
     switch (emu) {
       case 0: return launch_fmha<64, 0>(q, k, v, a, st);
+      case 1: return launch_fmha<64, 1>(q, k, v, a, st);
       case 2: return launch_fmha<64, 2>(q, k, v, a, st);
-      case 3: return launch_fmha<64, 3>(q, k, v, a, st);
-      case 5: return launch_fmha<64, 5>(q, k, v, a, st);
       case 4: return launch_fmha<64, 4>(q, k, v, a, st);
-      default: return launch_fmha<64, 3>(q, k, v, a, st);
+      case 3: return launch_fmha<64, 3>(q, k, v, a, st);
+      default: return launch_fmha<64, 2>(q, k, v, a, st);
     }
   }
-  return launch_fmha<32, 3>(q, k, v, a, st);
+  return launch_fmha<32, 2>(q, k, v, a, st);
 }
