@@ -257,7 +257,17 @@ VX_DEVICE uint64_t f2_mul(uint64_t a, uint64_t b) {
   asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
   return r;
 }
-// two 2^x at once on the FMA pipe (packed polynomial); returns (2^lo, 2^hi)
+VX_DEVICE void st_shared_f32(uint32_t addr, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+VX_DEVICE float ld_shared_f32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+  return v;
+}
+// two 2^x at once on the FMA pipe (packed polynomial); returns (2^lo, 2^hi).
+// DEG 3: rel. err 2.2e-4; DEG 2: rel. err 1.8e-3 (below the bf16 rounding P receives anyway)
+template <int DEG = 3>
 VX_DEVICE void ex2_poly2(float x0, float x1, float& y0, float& y1) {
   const uint64_t MAGIC = f2_pack(12582912.0f, 12582912.0f);
   const uint64_t NMAGIC = f2_pack(-12582912.0f, -12582912.0f);
@@ -265,9 +275,15 @@ VX_DEVICE void ex2_poly2(float x0, float x1, float& y0, float& y1) {
   const uint64_t x = f2_pack(fmaxf(x0, -126.0f), fmaxf(x1, -126.0f));
   const uint64_t t = f2_add(x, MAGIC);
   const uint64_t f = f2_fma(f2_add(t, NMAGIC), NEG1, x);
-  uint64_t p = f2_fma(f2_pack(0.05286732f, 0.05286732f), f, f2_pack(0.24215214f, 0.24215214f));
-  p = f2_fma(p, f, f2_pack(0.6935868f, 0.6935868f));
-  p = f2_fma(p, f, f2_pack(0.99996275f, 0.99996275f));
+  uint64_t p;
+  if constexpr (DEG == 3) {
+    p = f2_fma(f2_pack(0.05286732f, 0.05286732f), f, f2_pack(0.24215214f, 0.24215214f));
+    p = f2_fma(p, f, f2_pack(0.6935868f, 0.6935868f));
+    p = f2_fma(p, f, f2_pack(0.99996275f, 0.99996275f));
+  } else {
+    p = f2_fma(f2_pack(0.23783102f, 0.23783102f), f, f2_pack(0.70340002f, 0.70340002f));
+    p = f2_fma(p, f, f2_pack(1.00051396f, 1.00051396f));
+  }
   float p0, p1, t0, t1;
   f2_unpack(p, p0, p1);
   f2_unpack(t, t0, t1);

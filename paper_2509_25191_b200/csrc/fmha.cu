@@ -66,15 +66,17 @@ __host__ __device__ constexpr uint32_t tm_S(int i) { return i * 256; }
 __host__ __device__ constexpr uint32_t tm_P(int i) { return i * 256 + 128; }
 __host__ __device__ constexpr uint32_t tm_O(int i) { return i * 256 + 192; }
 
-// EMU_PAIRS_OF_8: of every 8 exp pairs, this many use the FMA-pipe polynomial
-template <int D, int EMU_PAIRS_OF_8>
+// EMU_PAIRS_OF_8: of every 8 exp pairs, this many use the FMA-pipe polynomial (degree PDEG)
+template <int D, int EMU_PAIRS_OF_8, int PDEG>
 __global__ void __launch_bounds__(ATTN_THREADS, 1)
     fmha_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                 const __grid_constant__ CUtensorMap tmV, const AttnArgs a) {
   using Cfg = AttnCfg<D>;
   constexpr int KST = Cfg::KST;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B alignment by offsetting the __shared__ array itself (keeps the shared address space
+  // visible to the compiler: LDS/STS instead of generic loads)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sQ = smem;                                 // 2 tiles
   uint8_t* sK = sQ + 2 * Cfg::TILE_BYTES;             // KST tiles
   uint8_t* sV = sK + KST * Cfg::TILE_BYTES;           // KST tiles
@@ -307,7 +309,7 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
           float x0, x1, p0, p1;
           f2_unpack(x, x0, x1);
           if ((c & 7) >= 8 - EMU_PAIRS_OF_8) {  // part of the exps on the FMA pipe
-            ex2_poly2(x0, x1, p0, p1);
+            ex2_poly2<PDEG>(x0, x1, p0, p1);
           } else {
             p0 = ex2(x0);
             p1 = ex2(x1);
@@ -381,14 +383,14 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
   }
 }
 
-template <int D, int EMU>
+template <int D, int EMU, int PDEG = 3>
 static int launch_fmha(const void* q, const void* k, const void* v, const AttnArgs& args, cudaStream_t st) {
   using Cfg = AttnCfg<D>;
   CUtensorMap tq, tk, tv;
   if (!make_tmap_2d_bf16(&tq, q, (uint64_t)args.H * args.Tq, D, D, 128, D, Cfg::SWIZZLE)) return VX_E_ARG;
   if (!make_tmap_2d_bf16(&tk, k, (uint64_t)args.H * args.Tk, D, D, 128, D, Cfg::SWIZZLE)) return VX_E_ARG;
   if (!make_tmap_2d_bf16(&tv, v, (uint64_t)args.H * args.Tk, D, D, 128, D, Cfg::SWIZZLE)) return VX_E_ARG;
-  auto kern = fmha_kernel<D, EMU>;
+  auto kern = fmha_kernel<D, EMU, PDEG>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
@@ -432,12 +434,21 @@ extern "C" int vx_attention(const void* q, const void* k, const void* v, void* o
     const char* e = getenv("VX_FMHA_EMU");  // diagnostic: exp pairs (of 8) on the FMA pipe
     return e ? atoi(e) : 2;
   }();
+  static int pdeg = [] {
+    const char* e = getenv("VX_FMHA_PDEG");  // diagnostic: polynomial degree (2 or 3)
+    return e ? atoi(e) : 3;
+  }();
   if (D == 64) {
+    if (pdeg == 2) {
+      switch (emu) {
+        case 2: return launch_fmha<64, 2, 2>(q, k, v, a, st);
+        case 3: return launch_fmha<64, 3, 2>(q, k, v, a, st);
+        default: return launch_fmha<64, 4, 2>(q, k, v, a, st);
+      }
+    }
     switch (emu) {
       case 0: return launch_fmha<64, 0>(q, k, v, a, st);
       case 1: return launch_fmha<64, 1>(q, k, v, a, st);
-      case 2: return launch_fmha<64, 2>(q, k, v, a, st);
-      case 4: return launch_fmha<64, 4>(q, k, v, a, st);
       case 3: return launch_fmha<64, 3>(q, k, v, a, st);
       default: return launch_fmha<64, 2>(q, k, v, a, st);
     }
