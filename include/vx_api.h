@@ -106,11 +106,50 @@ int vx_patchify(const float* images, void* out, int S, int H, int W, int patch, 
  * (slice_expand_and_flatten + cat, a3) */
 int vx_special_tokens(float* x, const float* tokens, int S, int tpf, int ntok, int C, void* stream);
 
-/* Bilinear resize with align_corners=True of NHWC bf16 maps in [F, h, w, C] -> out [F, H, W, C],
- * plus an optional bf16 [H, W, C] map added after interpolation (DPT pos-embed / skip).
+/* Bilinear resize with align_corners=True of NHWC bf16 maps in [F, h, w, C] -> out [F, H, W, C]
+ * (out_pad = 1: written into the interior of a zero-bordered [F, H+2, W+2, C] buffer), plus an
+ * optional bf16 [H, W, C] map added after interpolation (DPT pos-embed).
  * (F.interpolate(mode="bilinear", align_corners=True) in DPTHead / FeatureFusionBlock, a14) */
 int vx_upsample_bilinear(const void* in, int F, int h, int w, int C, void* out, int H, int W,
-                         const void* add_hwc, void* stream);
+                         const void* add_hwc, int out_pad, void* stream);
+
+/* Spatial GEMM for the DPT heads: rows are pixels of F frames.
+ *   conv3x3 = 1: implicit-GEMM 3x3 / stride 1 / pad 1 convolution; A is a zero-padded NHWC
+ *                bf16 buffer [F, H+2, W+2, Cin] (K = 9*Cin, weight K order (ky, kx, cin)); GEMM
+ *                rows live on the padded grid and the border rows are discarded;
+ *   conv3x3 = 0: 1x1 convolution / linear over dense NHWC rows [F*H*W, K].
+ * Epilogue (per output element): v = acc + bias (+ pos[yo, xo, c]); relu?; + res1; + res2;
+ *   out1 = v, out2 = relu(v) — bf16 NHWC, each tensor padded (1-pixel zero border) or dense.
+ *   subsample2: stride-2 output (even y, x); shuffle = s: conv-transpose k = s, stride s with
+ *   N = s*s*Cout ordered (i, j, c).
+ * head_odim > 0 fuses the DPT output head (N == 32): relu(acc + bias) -> fp32 1x1 conv
+ *   (head_w [odim, 32], head_b) -> activation (head_act 0: exp, 1: sign*expm1|x|) for the first
+ *   odim-1 channels into head_pred [F, H, W, odim-1] and 1 + exp(x) into head_conf [F, H, W]. */
+typedef struct vx_spatial {
+  int conv3x3;
+  int F, H, W;
+  int subsample2;
+  int shuffle;
+  int relu;
+  const void* pos;
+  const void* res1;
+  int res1_pad;
+  const void* res2;
+  int res2_pad;
+  void* out1;
+  int out1_pad;
+  void* out2;
+  int out2_pad;
+  const float* head_w;
+  const float* head_b;
+  int head_odim;
+  int head_act;
+  float* head_pred;
+  float* head_conf;
+} vx_spatial;
+
+int vx_gemm_spatial(const void* A, const void* B, int N, int K, const float* bias, const vx_spatial* sp,
+                    void* stream);
 
 int vx_num_sms(void);
 const char* vx_last_error(void);

@@ -40,6 +40,14 @@ class VGGTConfig:
     frame_chunk: int = 128             # frames per chunk for frame-wise MLP work
     head_chunk: int = 8                # frames per DPT-head chunk
 
+    def __post_init__(self):
+        # native DPT convs use 64-channel K blocks and 32-channel output chunks
+        for c in (*self.dpt_out_channels, self.dpt_features, self.dpt_features // 2):
+            if c % 64:
+                raise ValueError(f"DPT channel counts must be multiples of 64 (got {c})")
+        if self.dpt_head_features_2 != 32:
+            raise ValueError("dpt_head_features_2 must be 32 (fused output head)")
+
     @property
     def grid(self) -> int:
         return self.img_size // self.patch_size
@@ -87,8 +95,8 @@ def vggt_tiny() -> VGGTConfig:
     return VGGTConfig(
         img_size=112, embed_dim=128, depth=4, num_heads=4,
         kept_layers=(0, 1, 2, 3),
-        cam_num_heads=4, dpt_features=64, dpt_out_channels=(32, 64, 128, 128),
-        dpt_head_features_2=16, frame_chunk=4, head_chunk=3,
+        cam_num_heads=4, dpt_features=128, dpt_out_channels=(64, 64, 128, 128),
+        dpt_head_features_2=32, frame_chunk=4, head_chunk=3,
     )
 
 
@@ -97,6 +105,6 @@ def vggt_small() -> VGGTConfig:
     return VGGTConfig(
         img_size=126, embed_dim=256, depth=4, num_heads=4,
         kept_layers=(0, 1, 2, 3),
-        cam_num_heads=4, dpt_features=64, dpt_out_channels=(32, 64, 128, 128),
-        dpt_head_features_2=16, frame_chunk=4, head_chunk=3,
+        cam_num_heads=4, dpt_features=128, dpt_out_channels=(64, 64, 128, 128),
+        dpt_head_features_2=32, frame_chunk=4, head_chunk=3,
     )

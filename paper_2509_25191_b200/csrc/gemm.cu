@@ -21,7 +21,13 @@ namespace vx {
 struct GemmArgs {
   int M, N, K;
   vx_epilogue ep;
+  vx_spatial sp;
+  int conv_cin_blocks;  // > 0: implicit 3x3 conv A addressing (K = 9 * cin_blocks * 64)
+  int conv_w2;          // padded row length W + 2
 };
+
+constexpr int VX_EPI_SPATIAL = 6;
+constexpr int VX_EPI_HEADOUT = 7;
 
 constexpr int GEMM_BM = 128;
 constexpr int GEMM_BK = 64;
@@ -173,6 +179,153 @@ VX_DEVICE void epi_qkv_head(const GemmArgs& a, int row, int col, float* v) {
 }
 
 // ---------------------------------------------------------------------------
+// spatial (DPT) epilogues
+// ---------------------------------------------------------------------------
+struct PixInfo {
+  bool valid;
+  int f, yo, xo;  // output pixel (before the shuffle offset)
+};
+
+VX_DEVICE PixInfo pix_of_row(const GemmArgs& a, int row) {
+  const vx_spatial& sp = a.sp;
+  PixInfo p;
+  const int rw = sp.conv3x3 ? sp.W + 2 : sp.W;
+  const int pf = sp.conv3x3 ? (sp.H + 2) * (sp.W + 2) : sp.H * sp.W;
+  p.f = row / pf;
+  const int rem = row - p.f * pf;
+  const int y = rem / rw;
+  const int x = rem - y * rw;
+  p.valid = row < a.M && y < sp.H && x < sp.W;
+  if (sp.subsample2) {
+    p.valid = p.valid && ((y | x) & 1) == 0;
+    p.yo = y >> 1;
+    p.xo = x >> 1;
+  } else {
+    p.yo = y * sp.shuffle;
+    p.xo = x * sp.shuffle;
+  }
+  return p;
+}
+
+VX_DEVICE int64_t pix_index(int f, int y, int x, int Ho, int Wo, int pad) {
+  return pad ? ((int64_t)(f * (Ho + 2) + y + 1) * (Wo + 2) + x + 1) : ((int64_t)(f * Ho + y) * Wo + x);
+}
+
+VX_DEVICE void load8_bf16(const void* base, int64_t elem, float* o) {
+  const uint4 u = *reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(base) + elem);
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float2 f = __bfloat1622float2(h[k]);
+    o[2 * k] = f.x;
+    o[2 * k + 1] = f.y;
+  }
+}
+
+VX_DEVICE void epi_spatial32(const GemmArgs& a, const PixInfo& pi, int col, const uint32_t* r) {
+  const vx_spatial& sp = a.sp;
+  const vx_epilogue& e = a.ep;
+  const int s = sp.shuffle;
+  const int Cout = a.N / (s * s);
+  int c = col, yo = pi.yo, xo = pi.xo;
+  if (s > 1) {
+    const int ij = col / Cout;
+    c = col - ij * Cout;
+    yo += ij / s;
+    xo += ij % s;
+  }
+  const int Ho = sp.subsample2 ? (sp.H + 1) / 2 : sp.H * s;
+  const int Wo = sp.subsample2 ? (sp.W + 1) / 2 : sp.W * s;
+  float v[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+  if (e.bias) {
+    const float4* b4 = reinterpret_cast<const float4*>(e.bias + c);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float4 b = __ldg(b4 + j);
+      v[4 * j] += b.x; v[4 * j + 1] += b.y; v[4 * j + 2] += b.z; v[4 * j + 3] += b.w;
+    }
+  }
+  if (!pi.valid) return;
+  float t[8];
+  if (sp.pos) {
+    const int64_t pe = ((int64_t)yo * Wo + xo) * Cout + c;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      load8_bf16(sp.pos, pe + 8 * q, t);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[8 * q + k] += t[k];
+    }
+  }
+  if (sp.relu) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.f);
+  }
+  if (sp.res1) {
+    const int64_t re = pix_index(pi.f, yo, xo, Ho, Wo, sp.res1_pad) * Cout + c;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      load8_bf16(sp.res1, re + 8 * q, t);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[8 * q + k] += t[k];
+    }
+  }
+  if (sp.res2) {
+    const int64_t re = pix_index(pi.f, yo, xo, Ho, Wo, sp.res2_pad) * Cout + c;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      load8_bf16(sp.res2, re + 8 * q, t);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[8 * q + k] += t[k];
+    }
+  }
+  {
+    uint4* d = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(sp.out1) +
+                                        pix_index(pi.f, yo, xo, Ho, Wo, sp.out1_pad) * Cout + c);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      d[q] = make_uint4(pack_bf16(v[8 * q], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
+                        pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+  }
+  if (sp.out2) {
+    uint4* d = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(sp.out2) +
+                                        pix_index(pi.f, yo, xo, Ho, Wo, sp.out2_pad) * Cout + c);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      d[q] = make_uint4(pack_bf16(fmaxf(v[8 * q], 0.f), fmaxf(v[8 * q + 1], 0.f)),
+                        pack_bf16(fmaxf(v[8 * q + 2], 0.f), fmaxf(v[8 * q + 3], 0.f)),
+                        pack_bf16(fmaxf(v[8 * q + 4], 0.f), fmaxf(v[8 * q + 5], 0.f)),
+                        pack_bf16(fmaxf(v[8 * q + 6], 0.f), fmaxf(v[8 * q + 7], 0.f)));
+  }
+}
+
+// DPT output head: relu(conv3x3 + b) (32 ch) -> fp32 1x1 (odim) -> activation
+VX_DEVICE void epi_headout(const GemmArgs& a, const PixInfo& pi, const uint32_t* r) {
+  const vx_spatial& sp = a.sp;
+  const vx_epilogue& e = a.ep;
+  float v[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = fmaxf(__uint_as_float(r[j]) + (e.bias ? __ldg(e.bias + j) : 0.f), 0.f);
+  if (!pi.valid) return;
+  const int od = sp.head_odim;
+  const int64_t pix = ((int64_t)pi.f * sp.H + pi.yo) * sp.W + pi.xo;
+  for (int k = 0; k < od; ++k) {
+    float o = __ldg(sp.head_b + k);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) o = fmaf(__ldg(sp.head_w + k * 32 + j), v[j], o);
+    if (k == od - 1) {
+      sp.head_conf[pix] = 1.0f + expf(o);
+    } else {
+      float pr;
+      if (sp.head_act == 0) pr = expf(o);
+      else pr = copysignf(expm1f(fabsf(o)), o);
+      sp.head_pred[pix * (od - 1) + k] = pr;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // kernel
 // ---------------------------------------------------------------------------
 template <int BN, int EPI, int HD>
@@ -228,7 +381,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], Cfg::A_BYTES + Cfg::B_BYTES);
-          tma_load_2d(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], kb * GEMM_BK, m_blk * GEMM_BM);
+          int a_col = kb * GEMM_BK, a_row = m_blk * GEMM_BM;
+          if (args.conv_cin_blocks > 0) {  // implicit 3x3 conv: tap t shifts the padded-grid row
+            const int t = kb / args.conv_cin_blocks;
+            a_col = (kb - t * args.conv_cin_blocks) * GEMM_BK;
+            a_row += (t / 3) * args.conv_w2 + (t % 3);
+          }
+          tma_load_2d(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], a_col, a_row);
           tma_load_2d_hint(sB + stage * Cfg::B_BYTES, &tmB, &full[stage], kb * GEMM_BK, n_blk * BN, pol_b);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -286,6 +445,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           for (int j = 0; j < HD; ++j) v[j] = __uint_as_float(r[j]);
           epi_qkv_head<HD>(args, row, col, v);
         }
+      } else if constexpr (EPI == VX_EPI_SPATIAL || EPI == VX_EPI_HEADOUT) {
+        const PixInfo pi = pix_of_row(args, row);
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          const int col = n_blk * BN + c0;
+          if (col >= N) break;
+          uint32_t r[32];
+          tmem_ld32(taddr + c0, r);
+          tmem_wait_ld();
+          if constexpr (EPI == VX_EPI_SPATIAL) epi_spatial32(args, pi, col, r);
+          else epi_headout(args, pi, r);
+        }
       } else {
 #pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += 32) {
@@ -336,6 +507,8 @@ static int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, c
     case VX_EPI_RESID: return launch_gemm<BN, VX_EPI_RESID, 0>(ta, tb, a, st);
     case VX_EPI_PATCH: return launch_gemm<BN, VX_EPI_PATCH, 0>(ta, tb, a, st);
     case VX_EPI_F32: return launch_gemm<BN, VX_EPI_F32, 0>(ta, tb, a, st);
+    case VX_EPI_SPATIAL: return launch_gemm<BN, VX_EPI_SPATIAL, 0>(ta, tb, a, st);
+    case VX_EPI_HEADOUT: return launch_gemm<BN, VX_EPI_HEADOUT, 0>(ta, tb, a, st);
     case VX_EPI_QKV:
       if (a.ep.head_dim == 64) return launch_gemm<BN, VX_EPI_QKV, 64>(ta, tb, a, st);
       if (a.ep.head_dim == 32) return launch_gemm<BN, VX_EPI_QKV, 32>(ta, tb, a, st);
@@ -364,7 +537,7 @@ extern "C" int vx_gemm(int epi, const void* A, int64_t lda, const void* B, int64
   }
   if (epi == VX_EPI_PATCH) VX_CHECK_ARG(ep->resid && ep->tokens_per_frame > ep->patch_start, "vx_gemm: patch args");
   if (epi == VX_EPI_BF16 || epi == VX_EPI_GELU || epi == VX_EPI_F32) VX_CHECK_ARG(ep->out, "vx_gemm: null out");
-  GemmArgs args;
+  GemmArgs args = {};
   args.M = M;
   args.N = N;
   args.K = K;
@@ -374,5 +547,45 @@ extern "C" int vx_gemm(int epi, const void* A, int64_t lda, const void* B, int64
   if (!make_tmap_2d_bf16(&ta, A, M, K, lda, GEMM_BM, GEMM_BK, 128)) return VX_E_ARG;
   if (!make_tmap_2d_bf16(&tb, B, N, K, ldb, BN, GEMM_BK, 128)) return VX_E_ARG;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  return BN == 256 ? dispatch_epi<256>(epi, ta, tb, args, st) : dispatch_epi<128>(epi, ta, tb, args, st);
+}
+
+extern "C" int vx_gemm_spatial(const void* A, const void* B, int N, int K, const float* bias, const vx_spatial* sp,
+                               void* stream) {
+  using namespace vx;
+  VX_CHECK_ARG(A && B && sp, "vx_gemm_spatial: null pointer");
+  VX_CHECK_ARG(sp->out1 != nullptr || sp->head_odim > 0, "vx_gemm_spatial: no output");
+  VX_CHECK_ARG(sp->F > 0 && sp->H > 0 && sp->W > 0, "vx_gemm_spatial: bad grid");
+  VX_CHECK_ARG(K % GEMM_BK == 0 && N % 32 == 0, "vx_gemm_spatial: K %% 64, N %% 32 required (K=%d N=%d)", K, N);
+  const int s = sp->shuffle < 1 ? 1 : sp->shuffle;
+  VX_CHECK_ARG(N % (s * s) == 0 && (N / (s * s)) % 32 == 0, "vx_gemm_spatial: Cout must be a multiple of 32");
+  VX_CHECK_ARG(!(sp->subsample2 && s > 1), "vx_gemm_spatial: subsample2 and shuffle are exclusive");
+  if (sp->head_odim > 0) VX_CHECK_ARG(N == 32 && sp->head_w && sp->head_b && sp->head_pred && sp->head_conf &&
+                                      sp->head_odim >= 2 && !sp->subsample2 && s == 1,
+                                      "vx_gemm_spatial: fused head needs N == 32 and head pointers");
+  GemmArgs args = {};
+  args.N = N;
+  args.K = K;
+  args.sp = *sp;
+  args.sp.shuffle = s;
+  args.ep.bias = bias;
+  int64_t rows;
+  if (sp->conv3x3) {
+    VX_CHECK_ARG(K % (9 * GEMM_BK) == 0, "vx_gemm_spatial: conv3x3 needs Cin %% 64 == 0 (K=%d)", K);
+    args.conv_cin_blocks = K / (9 * GEMM_BK);
+    args.conv_w2 = sp->W + 2;
+    rows = (int64_t)sp->F * (sp->H + 2) * (sp->W + 2);
+  } else {
+    rows = (int64_t)sp->F * sp->H * sp->W;
+  }
+  VX_CHECK_ARG(rows < (1ll << 31), "vx_gemm_spatial: too many rows");
+  args.M = int(rows);
+  const int BN = (N % 256 == 0 || N > 512) ? 256 : 128;
+  const int64_t lda = sp->conv3x3 ? K / 9 : K;
+  CUtensorMap ta, tb;
+  if (!make_tmap_2d_bf16(&ta, A, rows, lda, lda, GEMM_BM, GEMM_BK, 128)) return VX_E_ARG;
+  if (!make_tmap_2d_bf16(&tb, B, N, K, K, BN, GEMM_BK, 128)) return VX_E_ARG;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int epi = sp->head_odim > 0 ? VX_EPI_HEADOUT : VX_EPI_SPATIAL;
   return BN == 256 ? dispatch_epi<256>(epi, ta, tb, args, st) : dispatch_epi<128>(epi, ta, tb, args, st);
 }

@@ -10,7 +10,8 @@ namespace vx {
 
 __global__ void upsample_bilinear_nhwc_kernel(const __nv_bfloat16* __restrict__ in, int F, int h, int w, int C,
                                               __nv_bfloat16* __restrict__ out, int H, int W,
-                                              const __nv_bfloat16* __restrict__ add_hwc, float sy, float sx) {
+                                              const __nv_bfloat16* __restrict__ add_hwc, float sy, float sx,
+                                              int out_pad) {
   const int cv = C / 8;
   const int64_t total = (int64_t)F * H * W * cv;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -52,14 +53,15 @@ __global__ void upsample_bilinear_nhwc_kernel(const __nv_bfloat16* __restrict__ 
       const float v1 = __bfloat162float(__float2bfloat16_rn(w00 * fa.y + w01 * fb.y + w10 * fc.y + w11 * fd.y));
       o[k] = pack_bf16(v0 + e[k].x, v1 + e[k].y);
     }
-    *reinterpret_cast<uint4*>(out + (((int64_t)f * H + y) * W + x) * C + c8 * 8) = make_uint4(o[0], o[1], o[2], o[3]);
+    const int64_t opix = out_pad ? ((int64_t)(f * (H + 2) + y + 1) * (W + 2) + x + 1) : (((int64_t)f * H + y) * W + x);
+    *reinterpret_cast<uint4*>(out + opix * C + c8 * 8) = make_uint4(o[0], o[1], o[2], o[3]);
   }
 }
 
 }  // namespace vx
 
 extern "C" int vx_upsample_bilinear(const void* in, int F, int h, int w, int C, void* out, int H, int W,
-                                    const void* add_hwc, void* stream) {
+                                    const void* add_hwc, int out_pad, void* stream) {
   using namespace vx;
   VX_CHECK_ARG(in && out && F > 0 && h > 0 && w > 0 && H > 0 && W > 0, "vx_upsample_bilinear: bad args");
   VX_CHECK_ARG(C % 8 == 0, "vx_upsample_bilinear: C=%d must be a multiple of 8", C);
@@ -69,7 +71,7 @@ extern "C" int vx_upsample_bilinear(const void* in, int F, int h, int w, int C, 
   const int grid = int((total + 255) / 256 < 148 * 32 ? (total + 255) / 256 : 148 * 32);
   upsample_bilinear_nhwc_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       reinterpret_cast<const __nv_bfloat16*>(in), F, h, w, C, reinterpret_cast<__nv_bfloat16*>(out), H, W,
-      reinterpret_cast<const __nv_bfloat16*>(add_hwc), sy, sx);
+      reinterpret_cast<const __nv_bfloat16*>(add_hwc), sy, sx, out_pad);
   VX_CHECK_LAUNCH("upsample launch");
   return VX_OK;
 }

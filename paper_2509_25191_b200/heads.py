@@ -4,12 +4,11 @@ Precision policy ("bf16 except MLP in heads", `PAPER.md:81`):
   * camera-head trunk (4 blocks, dim 2C) and AdaLN modulation: bf16 GEMMs on the
     vx tcgen05 kernel with fp32 residual stream; the pose branch MLP, pose
     embedding and activation stay fp32;
-  * DPT heads: LayerNorm + the four 1x1 projections run on the vx kernels
-    (LN + tcgen05 GEMM, NHWC output); the conv / conv-transpose / bilinear
-    stack runs in bf16 channels-last (cuDNN library kernels — a native
-    implicit-GEMM conv is the next §8 row); bilinear resizes
-    (+ fused pos-embed add) run on vx_upsample_bilinear; the final per-pixel
-    1x1 output conv and the activations run in fp32.
+  * DPT heads: entirely on the vx kernels — LayerNorm, 1x1 projections,
+    conv-transposes (GEMM + pixel shuffle), implicit-GEMM 3x3 convolutions with
+    fused ReLU / residual / skip epilogues, bilinear resizes (+ fused pos-embed),
+    bf16 NHWC activations; the final per-pixel 1x1 output conv and the
+    activations run in fp32 inside the last conv's epilogue.
   * heads are evaluated `head_chunk` frames at a time (VGGT-X chunking).
 """
 from __future__ import annotations
@@ -107,6 +106,17 @@ def dpt_pos_embed(c, h, w, img_w, img_h, ratio=0.1):
 
 
 class DPTHeadDevice:
+    """Frame-chunked DPT head on the vx kernels (no library convolutions).
+
+    Per chunk of F views: LayerNorm + 1x1 projections (+ UV pos-embed fused) ->
+    conv-transpose as GEMM + pixel-shuffle epilogue (k4/s4, k2/s2), identity, 3x3/s2
+    conv -> 3x3 layer_rn convs -> 4 fusion blocks (RCU = two implicit-GEMM 3x3 convs
+    with ReLU / residual / skip adds fused in the epilogues, bilinear upsample, 1x1
+    out_conv) -> 3x3 output_conv1 -> bilinear to H x W + pos-embed -> fused
+    [3x3 conv -> ReLU -> fp32 1x1 -> exp / inv_log / expp1] writing the final maps.
+    Activations are bf16 NHWC; 3x3-conv inputs live in zero-bordered buffers.
+    """
+
     def __init__(self, W: DeviceWeights, head: str, activation: str):
         self.W, self.head, self.activation = W, head, activation
         cfg = W.cfg
@@ -114,94 +124,132 @@ class DPTHeadDevice:
         g = cfg.grid
         D = 2 * cfg.embed_dim
         H = Wd = cfg.img_size
-        self.proj_w = [W[f"{head}projects.{i}.weight"].reshape(-1, D).contiguous() for i in range(4)]
-        self.pos_small = [dpt_pos_embed(oc, g, g, Wd, H).to(dev) for oc in cfg.dpt_out_channels]
-        self.pos_full = dpt_pos_embed(cfg.dpt_features // 2, H, Wd, Wd, H).to(dev).to(torch.bfloat16).contiguous()
-        # bf16 channels-last conv weights
+        oc = cfg.dpt_out_channels
+        bf = torch.bfloat16
+
+        def conv_w(name):  # [out, in, 3, 3] -> [out, 9*in], K order (ky, kx, cin)
+            w = W[name + ".weight"]
+            return w.permute(0, 2, 3, 1).reshape(w.shape[0], -1).to(bf).contiguous()
+
+        def lin_w(name):
+            w = W[name + ".weight"]
+            return w.reshape(w.shape[0], -1).to(bf).contiguous()
+
+        def convT_w(name):  # [in, out, s, s] -> [(i*s + j)*out + c, in]
+            w = W[name + ".weight"]
+            return w.permute(2, 3, 1, 0).reshape(-1, w.shape[0]).to(bf).contiguous()
+
+        self.b = {k: v.float().contiguous() for k, v in W.t.items() if k.startswith(head) and k.endswith(".bias")}
+        self.proj_w = [lin_w(f"{head}projects.{i}") for i in range(4)]
+        self.pos_small = [dpt_pos_embed(c, g, g, Wd, H).to(dev, bf).contiguous() for c in oc]
+        self.pos_full = dpt_pos_embed(cfg.dpt_features // 2, H, Wd, Wd, H).to(dev, bf).contiguous()
+        self.convT = [convT_w(head + "resize_layers.0"), convT_w(head + "resize_layers.1")]
         self.cw = {}
-        for k, v in W.t.items():
-            if k.startswith(head) and v.dim() == 4 and "projects" not in k:
-                if "output_conv2.2" in k:
-                    self.cw[k] = v.float()
-                else:
-                    self.cw[k] = v.to(torch.bfloat16).contiguous(memory_format=torch.channels_last)
-        self.cb = {k: v for k, v in W.t.items() if k.startswith(head) and k.endswith(".bias")}
+        for k in W.t:
+            if k.startswith(head) and k.endswith(".weight") and W.t[k].dim() == 4:
+                name = k[: -len(".weight")]
+                if W.t[k].shape[-1] == 3:
+                    self.cw[name] = conv_w(name)
+                elif "out_conv" in name:
+                    self.cw[name] = lin_w(name)
+        hw = W[head + "scratch.output_conv2.2.weight"]
+        self.head_w = hw.reshape(hw.shape[0], -1).float().contiguous()
+        self.head_b = W[head + "scratch.output_conv2.2.bias"].float().contiguous()
 
-    def _conv(self, x, name, stride=1, padding=None, dtype=torch.bfloat16):
-        w = self.cw[name + ".weight"]
-        b = self.cb.get(name + ".bias")
-        pad = (w.shape[-1] // 2) if padding is None else padding
-        return F.conv2d(x, w, None if b is None else b.to(dtype), stride=stride, padding=pad)
+    def _rcu(self, name, x_raw, x_relu, Fr, hs, res2=None, res2_pad=False, dense_out=False):
+        """ResidualConvUnit: conv2(relu(conv1(relu(x)))) + x (+ res2), relu(x) supplied padded."""
+        Fh = self.W.cfg.dpt_features
+        dev = x_raw.device
+        h = torch.zeros(Fr, hs + 2, hs + 2, Fh, device=dev, dtype=torch.bfloat16)
+        ops.gemm_spatial(x_relu.view(-1, Fh), self.cw[name + ".conv1"], self.b[name + ".conv1.bias"], Fr, hs, hs,
+                         conv3x3=True, relu=True, out1=h, out1_pad=True)
+        if dense_out:
+            o = torch.empty(Fr, hs, hs, Fh, device=dev, dtype=torch.bfloat16)
+            o2 = None
+        else:
+            o = torch.zeros(Fr, hs + 2, hs + 2, Fh, device=dev, dtype=torch.bfloat16)
+            o2 = torch.zeros_like(o)
+        ops.gemm_spatial(h.view(-1, Fh), self.cw[name + ".conv2"], self.b[name + ".conv2.bias"], Fr, hs, hs,
+                         conv3x3=True, res1=x_raw, res1_pad=True, res2=res2, res2_pad=res2_pad,
+                         out1=o, out1_pad=not dense_out, out2=o2, out2_pad=True)
+        return o, o2
 
-    def _rcu(self, x, name):
-        out = self._conv(F.relu(x), name + ".conv1")
-        out = self._conv(F.relu(out), name + ".conv2")
-        return out + x
-
-    def _fusion(self, name, x0, x1=None, size=None):
-        out = x0
-        if x1 is not None:
-            out = out + self._rcu(x1, name + ".resConfUnit1")
-        out = self._rcu(out, name + ".resConfUnit2")
-        h, w = out.shape[2:]
-        size = (2 * h, 2 * w) if size is None else tuple(size)
-        out = self._upsample(out, size)
-        return self._conv(out, name + ".out_conv")
-
-    @staticmethod
-    def _upsample(x, size, add=None):
-        """bilinear align_corners=True on channels-last bf16 via vx_upsample_bilinear."""
-        nhwc = x.permute(0, 2, 3, 1)
-        if not nhwc.is_contiguous():
-            nhwc = nhwc.contiguous()
-        return ops.upsample_bilinear(nhwc, size, add=add).permute(0, 3, 1, 2)
-
-    def forward_chunk(self, layers: List[torch.Tensor]):
-        """layers: 4 x (F, N, 2C) bf16 kept tokens -> (F, H, W, odim) fp32 pre-activation."""
+    def forward_chunk(self, layers: List[torch.Tensor], pred: torch.Tensor, conf: torch.Tensor):
+        """layers: 4 x (F, N, 2C) bf16 kept tokens; writes pred (F,H,W,odim-1) and conf (F,H,W)."""
         W, cfg, head = self.W, self.W.cfg, self.head
         g, ps = cfg.grid, cfg.patch_start_idx
         D = 2 * cfg.embed_dim
         Hh = Ww = cfg.img_size
+        oc = cfg.dpt_out_channels
+        Fh = cfg.dpt_features
+        Fr = layers[0].shape[0]
+        dev = layers[0].device
+        bf = torch.bfloat16
+        zeros = lambda *sh: torch.zeros(*sh, device=dev, dtype=bf)
+        empty = lambda *sh: torch.empty(*sh, device=dev, dtype=bf)
+        sizes = [4 * g, 2 * g, g, (g + 1) // 2]
         feats = []
         for i, x in enumerate(layers):
-            Fr = x.shape[0]
             tok = x[:, ps:].reshape(Fr * g * g, D)
             xn = ops.layernorm(tok, W[head + "norm.weight"], W[head + "norm.bias"], cfg.ln_eps)
-            y = ops.gemm(xn, self.proj_w[i], ops.EPI_BF16, bias=W[f"{head}projects.{i}.bias"])
-            y = (y.view(Fr, g, g, -1) + self.pos_small[i].to(torch.bfloat16)).permute(0, 3, 1, 2)
-            if i == 0:
-                y = F.conv_transpose2d(y, self.cw[head + "resize_layers.0.weight"],
-                                       self.cb[head + "resize_layers.0.bias"].to(torch.bfloat16), stride=4)
-            elif i == 1:
-                y = F.conv_transpose2d(y, self.cw[head + "resize_layers.1.weight"],
-                                       self.cb[head + "resize_layers.1.bias"].to(torch.bfloat16), stride=2)
-            elif i == 3:
-                y = self._conv(y, head + "resize_layers.3", stride=2, padding=1)
-            feats.append(y.contiguous(memory_format=torch.channels_last))
+            pb = self.b[f"{head}projects.{i}.bias"]
+            if i < 2:  # 1x1 projection, then conv-transpose (k = s = 4 / 2) as GEMM + pixel shuffle
+                y = empty(Fr, g, g, oc[i])
+                ops.gemm_spatial(xn, self.proj_w[i], pb, Fr, g, g, out1=y, pos=self.pos_small[i])
+                s = 4 if i == 0 else 2
+                f = zeros(Fr, g * s + 2, g * s + 2, oc[i])
+                ops.gemm_spatial(y.view(-1, oc[i]), self.convT[i], self.b[f"{head}resize_layers.{i}.bias"], Fr, g, g,
+                                 shuffle=s, out1=f, out1_pad=True)
+            elif i == 2:  # identity
+                f = zeros(Fr, g + 2, g + 2, oc[i])
+                ops.gemm_spatial(xn, self.proj_w[i], pb, Fr, g, g, out1=f, out1_pad=True, pos=self.pos_small[i])
+            else:  # 3x3 stride-2 conv: stride-1 implicit GEMM keeping even pixels
+                y = zeros(Fr, g + 2, g + 2, oc[i])
+                ops.gemm_spatial(xn, self.proj_w[i], pb, Fr, g, g, out1=y, out1_pad=True, pos=self.pos_small[i])
+                f = zeros(Fr, sizes[3] + 2, sizes[3] + 2, oc[i])
+                ops.gemm_spatial(y.view(-1, oc[i]), self.cw[head + "resize_layers.3"],
+                                 self.b[head + "resize_layers.3.bias"], Fr, g, g, conv3x3=True, subsample2=True,
+                                 out1=f, out1_pad=True)
+            feats.append(f)
         sc = head + "scratch."
-        l1, l2, l3, l4 = [self._conv(f, f"{sc}layer{i + 1}_rn") for i, f in enumerate(feats)]
-        out = self._fusion(sc + "refinenet4", l4, None, size=l3.shape[2:])
-        out = self._fusion(sc + "refinenet3", out, l3, size=l2.shape[2:])
-        out = self._fusion(sc + "refinenet2", out, l2, size=l1.shape[2:])
-        out = self._fusion(sc + "refinenet1", out, l1, size=None)
-        out = self._conv(out, sc + "output_conv1")
-        out = self._upsample(out, (Hh, Ww), add=self.pos_full)        # + UV pos-embed, fused
-        out = F.relu(self._conv(out, sc + "output_conv2.0"))
-        out = self._conv(out.float(), sc + "output_conv2.2", padding=0, dtype=torch.float32)
-        return out.permute(0, 2, 3, 1)
+        L = []
+        for i, f in enumerate(feats):  # layer_rn 3x3 (no bias): raw + relu copies, padded
+            hs = sizes[i]
+            l, lr = zeros(Fr, hs + 2, hs + 2, Fh), zeros(Fr, hs + 2, hs + 2, Fh)
+            ops.gemm_spatial(f.view(-1, oc[i]), self.cw[f"{sc}layer{i + 1}_rn"], None, Fr, hs, hs, conv3x3=True,
+                             out1=l, out1_pad=True, out2=lr, out2_pad=True)
+            L.append((l, lr))
+
+        def out_conv(r, o, hs, target, pad):
+            up = ops.upsample_bilinear(o, (target, target))
+            x = zeros(Fr, target + 2, target + 2, Fh) if pad else empty(Fr, target, target, Fh)
+            ops.gemm_spatial(up.view(-1, Fh), self.cw[f"{sc}refinenet{r}.out_conv"],
+                             self.b[f"{sc}refinenet{r}.out_conv.bias"], Fr, target, target, out1=x, out1_pad=pad)
+            return x
+
+        # refinenet4: RCU2(l4) -> upsample to layer3 size -> out_conv
+        o, _ = self._rcu(f"{sc}refinenet4.resConfUnit2", L[3][0], L[3][1], Fr, sizes[3], dense_out=True)
+        x = out_conv(4, o, sizes[3], sizes[2], False)
+        for r, li, target in ((3, 2, sizes[1]), (2, 1, sizes[0]), (1, 0, 2 * sizes[0])):
+            hs = sizes[li]
+            s_raw, s_relu = self._rcu(f"{sc}refinenet{r}.resConfUnit1", L[li][0], L[li][1], Fr, hs,
+                                      res2=x, res2_pad=False)
+            o, _ = self._rcu(f"{sc}refinenet{r}.resConfUnit2", s_raw, s_relu, Fr, hs, dense_out=True)
+            x = out_conv(r, o, hs, target, pad=(r == 1))
+        t = 2 * sizes[0]
+        y = empty(Fr, t, t, Fh // 2)
+        ops.gemm_spatial(x.view(-1, Fh), self.cw[sc + "output_conv1"], self.b[sc + "output_conv1.bias"], Fr, t, t,
+                         conv3x3=True, out1=y)
+        u = ops.upsample_bilinear(y, (Hh, Ww), add=self.pos_full, out_pad=True)
+        act = 0 if self.activation == "exp" else 1
+        ops.gemm_spatial(u.view(-1, Fh // 2), self.cw[sc + "output_conv2.0"], self.b[sc + "output_conv2.0.bias"],
+                         Fr, Hh, Ww, conv3x3=True, head=(self.head_w, self.head_b, act, pred, conf))
 
     def __call__(self, kept: Dict[int, torch.Tensor], out_pred: torch.Tensor, out_conf: torch.Tensor,
                  chunk: int):
         cfg = self.W.cfg
         layers = [kept[i] for i in cfg.kept_layers]
         S = layers[0].shape[0]
-        with torch.backends.cudnn.flags(enabled=True, allow_tf32=False):
-            for s0 in range(0, S, chunk):
-                s1 = min(S, s0 + chunk)
-                fmap = self.forward_chunk([l[s0:s1] for l in layers])
-                xyz, conf = fmap[..., :-1], fmap[..., -1]
-                if self.activation == "exp":
-                    out_pred[s0:s1] = torch.exp(xyz)
-                else:
-                    out_pred[s0:s1] = torch.sign(xyz) * torch.expm1(xyz.abs())
-                out_conf[s0:s1] = 1 + conf.exp()
+        for s0 in range(0, S, chunk):
+            s1 = min(S, s0 + chunk)
+            self.forward_chunk([l[s0:s1] for l in layers], out_pred[s0:s1], out_conf[s0:s1])

@@ -36,8 +36,18 @@ class Epilogue(ctypes.Structure):
     ]
 
 
+class Spatial(ctypes.Structure):
+    _fields_ = [
+        ("conv3x3", _i32), ("F", _i32), ("H", _i32), ("W", _i32), ("subsample2", _i32), ("shuffle", _i32),
+        ("relu", _i32), ("pos", _vp), ("res1", _vp), ("res1_pad", _i32), ("res2", _vp), ("res2_pad", _i32),
+        ("out1", _vp), ("out1_pad", _i32), ("out2", _vp), ("out2_pad", _i32),
+        ("head_w", _vp), ("head_b", _vp), ("head_odim", _i32), ("head_act", _i32),
+        ("head_pred", _vp), ("head_conf", _vp),
+    ]
+
+
 EXPORTED_SYMBOLS = ("vx_gemm", "vx_attention", "vx_layernorm", "vx_patchify", "vx_special_tokens",
-                    "vx_upsample_bilinear", "vx_num_sms", "vx_last_error", "vx_version")
+                    "vx_upsample_bilinear", "vx_gemm_spatial", "vx_num_sms", "vx_last_error", "vx_version")
 
 _lib = None
 
@@ -57,11 +67,12 @@ def load_library(path: os.PathLike | None = None) -> ctypes.CDLL:
     lib.vx_layernorm.argtypes = [_vp, _i32, _i64, _vp, _i32, _i64, _vp, _vp, _i32, _i32, _f32, _vp]
     lib.vx_patchify.argtypes = [_vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp]
     lib.vx_special_tokens.argtypes = [_vp, _vp, _i32, _i32, _i32, _i32, _vp]
-    lib.vx_upsample_bilinear.argtypes = [_vp, _i32, _i32, _i32, _i32, _vp, _i32, _i32, _vp, _vp]
+    lib.vx_upsample_bilinear.argtypes = [_vp, _i32, _i32, _i32, _i32, _vp, _i32, _i32, _vp, _i32, _vp]
+    lib.vx_gemm_spatial.argtypes = [_vp, _vp, _i32, _i32, _vp, ctypes.POINTER(Spatial), _vp]
     lib.vx_last_error.restype = ctypes.c_char_p
     lib.vx_version.restype = ctypes.c_char_p
     for name in ("vx_gemm", "vx_attention", "vx_layernorm", "vx_patchify", "vx_special_tokens",
-                 "vx_upsample_bilinear", "vx_num_sms"):
+                 "vx_upsample_bilinear", "vx_gemm_spatial", "vx_num_sms"):
         getattr(lib, name).restype = _i32
     if path is None:
         _lib = lib
@@ -217,8 +228,9 @@ def special_tokens(x, tokens, S, tpf):
     return x
 
 
-def upsample_bilinear(x: torch.Tensor, size, add=None, out=None):
-    """NHWC bf16 [F, h, w, C] -> [F, H, W, C], align_corners=True, + optional [H, W, C] add."""
+def upsample_bilinear(x: torch.Tensor, size, add=None, out=None, out_pad: bool = False):
+    """NHWC bf16 [F, h, w, C] -> [F, H, W, C] (or the interior of a zero-bordered
+    [F, H+2, W+2, C] buffer when out_pad), align_corners=True, + optional [H, W, C] add."""
     load_library()
     _req(x, torch.bfloat16, "x")
     if not x.is_contiguous():
@@ -226,11 +238,49 @@ def upsample_bilinear(x: torch.Tensor, size, add=None, out=None):
     F_, h, w, C = x.shape
     H, W = size
     if out is None:
-        out = torch.empty(F_, H, W, C, device=x.device, dtype=torch.bfloat16)
+        shape = (F_, H + 2, W + 2, C) if out_pad else (F_, H, W, C)
+        out = (torch.zeros if out_pad else torch.empty)(shape, device=x.device, dtype=torch.bfloat16)
     if add is not None:
         _req(add, torch.bfloat16, "add")
         if tuple(add.shape) != (H, W, C) or not add.is_contiguous():
             raise ValueError("upsample_bilinear: add must be contiguous [H, W, C]")
-    _check(_lib.vx_upsample_bilinear(_ptr(x), F_, h, w, C, _ptr(out), H, W, _ptr(add), _stream()),
+    _check(_lib.vx_upsample_bilinear(_ptr(x), F_, h, w, C, _ptr(out), H, W, _ptr(add), int(out_pad), _stream()),
            "vx_upsample_bilinear")
     return out
+
+
+def gemm_spatial(a, w, bias, F: int, H: int, W: int, conv3x3=False, out1=None, out1_pad=False, out2=None,
+                 out2_pad=False, relu=False, pos=None, res1=None, res1_pad=False, res2=None, res2_pad=False,
+                 subsample2=False, shuffle=1, head=None):
+    """DPT spatial GEMM (see include/vx_api.h vx_gemm_spatial).
+
+    a: bf16 rows [F*(H+2)*(W+2), Cin] (conv3x3, zero-padded NHWC) or [F*H*W, K];
+    w: bf16 [N, K] (conv3x3: K = 9*Cin ordered (ky, kx, cin)).
+    head = (w_fp32 [odim, 32], b_fp32, act, pred [F,H,W,odim-1], conf [F,H,W]) fuses the output head.
+    """
+    load_library()
+    _req(a, torch.bfloat16, "a")
+    _req(w, torch.bfloat16, "w")
+    if not (a.is_contiguous() and w.is_contiguous()):
+        raise ValueError("gemm_spatial: a and w must be contiguous")
+    N, K = w.shape
+    sp = Spatial()
+    sp.conv3x3, sp.F, sp.H, sp.W = int(conv3x3), F, H, W
+    sp.subsample2, sp.shuffle, sp.relu = int(subsample2), shuffle, int(relu)
+    for name, t in (("pos", pos), ("res1", res1), ("res2", res2), ("out1", out1), ("out2", out2)):
+        if t is not None:
+            _req(t, torch.bfloat16, name)
+            if not t.is_contiguous():
+                raise ValueError(f"gemm_spatial: {name} must be contiguous")
+            setattr(sp, name, t.data_ptr())
+    sp.res1_pad, sp.res2_pad, sp.out1_pad, sp.out2_pad = int(res1_pad), int(res2_pad), int(out1_pad), int(out2_pad)
+    if head is not None:
+        hw, hb, act, pred, conf = head
+        for t, nm in ((hw, "head_w"), (hb, "head_b"), (pred, "head_pred"), (conf, "head_conf")):
+            _req(t, torch.float32, nm)
+        sp.head_w, sp.head_b, sp.head_pred, sp.head_conf = hw.data_ptr(), hb.data_ptr(), pred.data_ptr(), conf.data_ptr()
+        sp.head_odim, sp.head_act = hw.shape[0], act
+    if bias is not None:
+        _req(bias, torch.float32, "bias")
+    _check(_lib.vx_gemm_spatial(_ptr(a), _ptr(w), N, K, _ptr(bias), ctypes.byref(sp), _stream()), "vx_gemm_spatial")
+    return out1

@@ -225,3 +225,106 @@ def test_special_tokens(ops):
     for f in range(1, S):
         assert torch.equal(xv[f, :5], tok[1])
     assert (xv[:, 5:] == 0).all()
+
+
+# ---------------------------------------------------------------------------
+# DPT spatial GEMM (implicit 3x3 conv, conv-transpose shuffle, stride 2, fused head)
+# ---------------------------------------------------------------------------
+def _pad_nhwc(x):  # (F,H,W,C) -> zero-bordered (F,H+2,W+2,C)
+    return F.pad(x, (0, 0, 1, 1, 1, 1)).contiguous()
+
+
+def _conv_w(w):
+    return w.permute(0, 2, 3, 1).reshape(w.shape[0], -1).to(torch.bfloat16).contiguous()
+
+
+@pytest.mark.parametrize("Fr,H,Cin,Cout", [(2, 19, 64, 128), (3, 37, 256, 256), (1, 74, 128, 64), (2, 7, 64, 32)])
+def test_spatial_conv3x3_relu_residuals(ops, Fr, H, Cin, Cout):
+    g = torch.Generator(device="cuda").manual_seed(60)
+    x = torch.randn(Fr, H, H, Cin, device="cuda", generator=g).to(torch.bfloat16)
+    w = torch.randn(Cout, Cin, 3, 3, device="cuda", generator=g) / (9 * Cin) ** 0.5
+    w = w.to(torch.bfloat16).float()
+    b = torch.randn(Cout, device="cuda", generator=g)
+    r1 = torch.randn(Fr, H, H, Cout, device="cuda", generator=g).to(torch.bfloat16)
+    r2 = torch.randn(Fr, H, H, Cout, device="cuda", generator=g).to(torch.bfloat16)
+    out = torch.zeros(Fr, H + 2, H + 2, Cout, device="cuda", dtype=torch.bfloat16)
+    out2 = torch.zeros_like(out)
+    ops.gemm_spatial(_pad_nhwc(x).view(-1, Cin), _conv_w(w), b, Fr, H, H, conv3x3=True, relu=True,
+                     res1=_pad_nhwc(r1), res1_pad=True, res2=r2, res2_pad=False,
+                     out1=out, out1_pad=True, out2=out2, out2_pad=True)
+    ref = F.relu(F.conv2d(x.permute(0, 3, 1, 2).float(), w, b, padding=1)).permute(0, 2, 3, 1) + r1.float() + r2.float()
+    assert rel(out[:, 1:-1, 1:-1], ref) < 5e-3
+    assert rel(out2[:, 1:-1, 1:-1], F.relu(ref)) < 5e-3
+    border = out.clone()
+    border[:, 1:-1, 1:-1] = 0
+    assert border.abs().max().item() == 0
+
+
+def test_spatial_conv3x3_stride2(ops):
+    Fr, H, C = 2, 37, 128
+    x = torch.randn(Fr, H, H, C, device="cuda").to(torch.bfloat16)
+    w = (torch.randn(C, C, 3, 3, device="cuda") / (9 * C) ** 0.5).to(torch.bfloat16).float()
+    b = torch.randn(C, device="cuda")
+    Ho = (H + 1) // 2
+    out = torch.empty(Fr, Ho, Ho, C, device="cuda", dtype=torch.bfloat16)
+    ops.gemm_spatial(_pad_nhwc(x).view(-1, C), _conv_w(w), b, Fr, H, H, conv3x3=True, subsample2=True, out1=out)
+    ref = F.conv2d(x.permute(0, 3, 1, 2).float(), w, b, stride=2, padding=1).permute(0, 2, 3, 1)
+    assert ref.shape == out.shape
+    assert rel(out, ref) < 5e-3
+
+
+@pytest.mark.parametrize("s,Cin,Cout", [(4, 256, 256), (2, 512, 512), (2, 64, 64)])
+def test_spatial_conv_transpose_shuffle(ops, s, Cin, Cout):
+    Fr, H = 2, 9
+    x = torch.randn(Fr, H, H, Cin, device="cuda").to(torch.bfloat16)
+    w = (torch.randn(Cin, Cout, s, s, device="cuda") / Cin ** 0.5).to(torch.bfloat16).float()
+    b = torch.randn(Cout, device="cuda")
+    wB = w.permute(2, 3, 1, 0).reshape(-1, Cin).to(torch.bfloat16).contiguous()
+    out = torch.zeros(Fr, H * s + 2, H * s + 2, Cout, device="cuda", dtype=torch.bfloat16)
+    ops.gemm_spatial(x.view(-1, Cin), wB, b, Fr, H, H, shuffle=s, out1=out, out1_pad=True)
+    ref = F.conv_transpose2d(x.permute(0, 3, 1, 2).float(), w, b, stride=s).permute(0, 2, 3, 1)
+    assert rel(out[:, 1:-1, 1:-1], ref) < 5e-3
+
+
+def test_spatial_pos_embed_1x1(ops):
+    Fr, H, K, N = 3, 37, 512, 256
+    x = torch.randn(Fr * H * H, K, device="cuda").to(torch.bfloat16)
+    w = (torch.randn(N, K, device="cuda") * 0.05).to(torch.bfloat16)
+    b = torch.randn(N, device="cuda")
+    pos = torch.randn(H, H, N, device="cuda").to(torch.bfloat16)
+    out = torch.empty(Fr, H, H, N, device="cuda", dtype=torch.bfloat16)
+    ops.gemm_spatial(x, w, b, Fr, H, H, out1=out, pos=pos)
+    ref = (x.float() @ w.float().T + b).view(Fr, H, H, N) + pos.float()
+    assert rel(out, ref) < 5e-3
+
+
+@pytest.mark.parametrize("act,odim", [(0, 2), (1, 4)])
+def test_spatial_fused_output_head(ops, act, odim):
+    Fr, H, Cin = 2, 40, 128
+    x = torch.randn(Fr, H, H, Cin, device="cuda").to(torch.bfloat16)
+    w = (torch.randn(32, Cin, 3, 3, device="cuda") / (9 * Cin) ** 0.5).to(torch.bfloat16).float()
+    b = torch.randn(32, device="cuda") * 0.1
+    hw = torch.randn(odim, 32, device="cuda") * 0.1
+    hb = torch.randn(odim, device="cuda") * 0.1
+    pred = torch.empty(Fr, H, H, odim - 1, device="cuda")
+    conf = torch.empty(Fr, H, H, device="cuda")
+    ops.gemm_spatial(_pad_nhwc(x).view(-1, Cin), _conv_w(w), b, Fr, H, H, conv3x3=True,
+                     head=(hw, hb, act, pred, conf))
+    h = F.relu(F.conv2d(x.permute(0, 3, 1, 2).float(), w, b, padding=1))
+    o = F.conv2d(h, hw.view(odim, 32, 1, 1), hb).permute(0, 2, 3, 1)
+    xyz, c = o[..., :-1], o[..., -1]
+    ref = torch.exp(xyz) if act == 0 else torch.sign(xyz) * torch.expm1(xyz.abs())
+    assert rel(pred, ref) < 5e-3
+    assert rel(conf, 1 + c.exp()) < 5e-3
+
+
+def test_upsample_bilinear_matches_interpolate(ops):
+    for (h, H, C) in ((19, 37, 256), (148, 296, 64), (296, 518, 128)):
+        x = torch.randn(2, h, h, C, device="cuda").to(torch.bfloat16)
+        add = torch.randn(H, H, C, device="cuda").to(torch.bfloat16)
+        out = ops.upsample_bilinear(x, (H, H), add=add)
+        ref = F.interpolate(x.permute(0, 3, 1, 2).float(), size=(H, H), mode="bilinear",
+                            align_corners=True).permute(0, 2, 3, 1) + add.float()
+        assert rel(out, ref) < 5e-3
+        outp = ops.upsample_bilinear(x, (H, H), out_pad=True)
+        assert rel(outp[:, 1:-1, 1:-1], ref - add.float()) < 5e-3
