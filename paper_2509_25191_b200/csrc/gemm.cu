@@ -4,10 +4,11 @@
 //   fp32 accumulators in TMEM (two BN-column buffers so the epilogue of tile t
 //   overlaps the main loop of tile t+1).
 //
-// Warp roles (256 threads): w0 TMA producer, w1 tcgen05.mma issuer (one elected
-// lane), w2 TMEM allocator, w4..w7 epilogue (thread i of warp 4+e owns TMEM lane /
-// tile row 32e+i, so per-row work such as the per-head q/k LayerNorm and RoPE of
-// the qkv epilogue is entirely thread-local).
+// Warp roles (384 threads): w0 TMA producer, w1 tcgen05.mma issuer (one elected
+// lane), w2 TMEM allocator, w4..w11 epilogue: thread i of warp 4+e owns TMEM lane /
+// tile row 32(e%4)+i and half of the tile's columns, so per-row work such as the
+// per-head q/k LayerNorm and RoPE of the qkv epilogue is entirely thread-local.
+// (K=1024 GEMMs are epilogue-bound with 4 epilogue warps; 8 halve that time.)
 //
 // Replaces the upstream nn.Linear calls of the VGGT Block (SURVEY.md §8a a6, a9,
 // a10) and the conv patch-embed (a2), with the norm/RoPE/LayerScale/residual
@@ -31,7 +32,8 @@ constexpr int VX_EPI_HEADOUT = 7;
 
 constexpr int GEMM_BM = 128;
 constexpr int GEMM_BK = 64;
-constexpr int GEMM_THREADS = 256;
+constexpr int GEMM_THREADS = 384;  // w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4..w11 epilogue
+constexpr int GEMM_EPI_WARPS = 8;  // two warps per TMEM lane quarter, each owning half of the tile columns
 
 template <int BN>
 struct GemmCfg {
@@ -361,7 +363,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 4);
+      mbar_init(&tempty[s], GEMM_EPI_WARPS);
     }
     fence_barrier_init();
   }
@@ -422,7 +424,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
     }
   } else if (warp >= 4) {
-    const int ew = warp - 4;
+    const int ew = (warp - 4) & 3;        // TMEM lane quarter
+    const int c_beg = ((warp - 4) >> 2) * (BN / 2), c_end = c_beg + BN / 2;  // column half
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
@@ -433,7 +436,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const uint32_t taddr = tmem_base + (uint32_t(ew * 32) << 16) + acc * BN;
       if constexpr (EPI == VX_EPI_QKV) {
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += HD) {
+        for (int c0 = c_beg; c0 < c_end; c0 += HD) {
           const int col = n_blk * BN + c0;
           if (col >= N) break;
           uint32_t r[HD];
@@ -448,7 +451,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       } else if constexpr (EPI == VX_EPI_SPATIAL || EPI == VX_EPI_HEADOUT) {
         const PixInfo pi = pix_of_row(args, row);
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 32) {
+        for (int c0 = c_beg; c0 < c_end; c0 += 32) {
           const int col = n_blk * BN + c0;
           if (col >= N) break;
           uint32_t r[32];
@@ -459,7 +462,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         }
       } else {
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 32) {
+        for (int c0 = c_beg; c0 < c_end; c0 += 32) {
           const int col = n_blk * BN + c0;
           if (col >= N) break;
           uint32_t r[32];
