@@ -151,6 +151,20 @@ typedef struct vx_spatial {
 int vx_gemm_spatial(const void* A, const void* B, int N, int K, const float* bias, const vx_spatial* sp,
                     void* stream);
 
+/* Global-Alignment epipolar kernels, fp64, all image pairs in one launch.
+ * Replace pkg/src/epialign/_kernels_cy.pyx pair_residuals (:26-54) / pair_accumulate (:57-116).
+ *   F: [P, 3, 3] unit-Frobenius fundamental matrices; offsets: [P+1] prefix sums partitioning
+ *   the correspondences xy_i, xy_j: [K, 2] (pixels) and weights w: [K].
+ *   mode 0 = algebraic |x'^T F x|, 1 = geometric point-to-line distance (NaN / skipped when
+ *   |(l0, l1)| < 1e-12); residuals < 1e-9 keep their loss but get a zero subgradient.
+ * residuals: e [K], n_deg [P].  accumulate: out [P, 11] = (loss_sum, weight_sum, dL/dF row-major),
+ * n_skipped [P]. */
+int vx_epipolar_residuals(const double* F, const int64_t* offsets, const double* xy_i, const double* xy_j,
+                          int num_pairs, int mode, double* e, int32_t* n_deg, void* stream);
+int vx_epipolar_accumulate(const double* F, const int64_t* offsets, const double* xy_i, const double* xy_j,
+                           const double* w, int num_pairs, int mode, double* out, int32_t* n_skipped,
+                           void* stream);
+
 int vx_num_sms(void);
 const char* vx_last_error(void);
 const char* vx_version(void);

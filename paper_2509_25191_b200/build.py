@@ -35,8 +35,13 @@ def up_to_date() -> bool:
     return all(p.stat().st_mtime <= t for p in sources() + headers())
 
 
+# per-file flags: the fp64 GA kernels follow the reference's un-fused double arithmetic
+# (pkg/src/epialign/_kernels_cy.pyx is compiled without FMA contraction on x86-64)
+EXTRA = {"epipolar.cu": ["-fmad=false"]}
+
+
 def _compile_one(src: Path, obj: Path, log):
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", str(src), "-o", str(obj)]
+    cmd = [NVCC, *ARCH, *FLAGS, *EXTRA.get(src.name, []), "-c", str(src), "-o", str(obj)]
     r = subprocess.run(cmd, capture_output=True, text=True)
     log.write(f"$ {' '.join(cmd)}\n{r.stdout}{r.stderr}\n")
     if r.returncode != 0:

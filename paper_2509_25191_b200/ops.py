@@ -47,7 +47,8 @@ class Spatial(ctypes.Structure):
 
 
 EXPORTED_SYMBOLS = ("vx_gemm", "vx_attention", "vx_layernorm", "vx_patchify", "vx_special_tokens",
-                    "vx_upsample_bilinear", "vx_gemm_spatial", "vx_num_sms", "vx_last_error", "vx_version")
+                    "vx_upsample_bilinear", "vx_gemm_spatial", "vx_epipolar_residuals",
+                    "vx_epipolar_accumulate", "vx_num_sms", "vx_last_error", "vx_version")
 
 _lib = None
 
@@ -69,10 +70,13 @@ def load_library(path: os.PathLike | None = None) -> ctypes.CDLL:
     lib.vx_special_tokens.argtypes = [_vp, _vp, _i32, _i32, _i32, _i32, _vp]
     lib.vx_upsample_bilinear.argtypes = [_vp, _i32, _i32, _i32, _i32, _vp, _i32, _i32, _vp, _i32, _vp]
     lib.vx_gemm_spatial.argtypes = [_vp, _vp, _i32, _i32, _vp, ctypes.POINTER(Spatial), _vp]
+    lib.vx_epipolar_residuals.argtypes = [_vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp]
+    lib.vx_epipolar_accumulate.argtypes = [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp]
     lib.vx_last_error.restype = ctypes.c_char_p
     lib.vx_version.restype = ctypes.c_char_p
     for name in ("vx_gemm", "vx_attention", "vx_layernorm", "vx_patchify", "vx_special_tokens",
-                 "vx_upsample_bilinear", "vx_gemm_spatial", "vx_num_sms"):
+                 "vx_upsample_bilinear", "vx_gemm_spatial", "vx_epipolar_residuals",
+                 "vx_epipolar_accumulate", "vx_num_sms"):
         getattr(lib, name).restype = _i32
     if path is None:
         _lib = lib
@@ -284,3 +288,35 @@ def gemm_spatial(a, w, bias, F: int, H: int, W: int, conv3x3=False, out1=None, o
         _req(bias, torch.float32, "bias")
     _check(_lib.vx_gemm_spatial(_ptr(a), _ptr(w), N, K, _ptr(bias), ctypes.byref(sp), _stream()), "vx_gemm_spatial")
     return out1
+
+
+def epipolar_residuals(F, offsets, xy_i, xy_j, mode: int):
+    """Batched pair_residuals: F [P,3,3] f64, offsets [P+1] int64, xy [K,2] f64 -> (e [K], n_deg [P])."""
+    load_library()
+    for t, nm, dt in ((F, "F", torch.float64), (offsets, "offsets", torch.int64), (xy_i, "xy_i", torch.float64),
+                      (xy_j, "xy_j", torch.float64)):
+        _req(t, dt, nm)
+        if not t.is_contiguous():
+            raise ValueError(f"{nm} must be contiguous")
+    P = F.shape[0]
+    e = torch.empty(xy_i.shape[0], device=F.device, dtype=torch.float64)
+    nd = torch.empty(P, device=F.device, dtype=torch.int32)
+    _check(_lib.vx_epipolar_residuals(_ptr(F), _ptr(offsets), _ptr(xy_i), _ptr(xy_j), P, mode, _ptr(e), _ptr(nd),
+                                      _stream()), "vx_epipolar_residuals")
+    return e, nd
+
+
+def epipolar_accumulate(F, offsets, xy_i, xy_j, w, mode: int):
+    """Batched pair_accumulate -> (out [P, 11] = loss, wsum, G row-major; n_skipped [P])."""
+    load_library()
+    for t, nm, dt in ((F, "F", torch.float64), (offsets, "offsets", torch.int64), (xy_i, "xy_i", torch.float64),
+                      (xy_j, "xy_j", torch.float64), (w, "w", torch.float64)):
+        _req(t, dt, nm)
+        if not t.is_contiguous():
+            raise ValueError(f"{nm} must be contiguous")
+    P = F.shape[0]
+    out = torch.empty(P, 11, device=F.device, dtype=torch.float64)
+    sk = torch.empty(P, device=F.device, dtype=torch.int32)
+    _check(_lib.vx_epipolar_accumulate(_ptr(F), _ptr(offsets), _ptr(xy_i), _ptr(xy_j), _ptr(w), P, mode, _ptr(out),
+                                       _ptr(sk), _stream()), "vx_epipolar_accumulate")
+    return out, sk
