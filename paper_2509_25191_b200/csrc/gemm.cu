@@ -37,7 +37,7 @@ constexpr int GEMM_EPI_WARPS = 8;  // two warps per TMEM lane quarter, each owni
 
 template <int BN>
 struct GemmCfg {
-  static constexpr int STAGES = BN == 256 ? 4 : 6;
+  static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
   static constexpr uint32_t A_BYTES = GEMM_BM * GEMM_BK * 2;
   static constexpr uint32_t B_BYTES = BN * GEMM_BK * 2;
   static constexpr uint32_t SMEM = STAGES * (A_BYTES + B_BYTES) + 1024 /*align*/ + 256 /*barriers*/;
@@ -425,7 +425,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
   } else if (warp >= 4) {
     const int ew = (warp - 4) & 3;        // TMEM lane quarter
-    const int c_beg = ((warp - 4) >> 2) * (BN / 2), c_end = c_beg + BN / 2;  // column half
+    // column half (a 32-wide tile is handled whole by warps 4..7; warps 8..11 only arrive)
+    const int c_beg = BN <= 32 ? ((warp - 4) >> 2) * BN : ((warp - 4) >> 2) * (BN / 2);
+    const int c_end = BN <= 32 ? BN : c_beg + BN / 2;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
@@ -583,12 +585,13 @@ extern "C" int vx_gemm_spatial(const void* A, const void* B, int N, int K, const
   }
   VX_CHECK_ARG(rows < (1ll << 31), "vx_gemm_spatial: too many rows");
   args.M = int(rows);
-  const int BN = (N % 256 == 0 || N > 512) ? 256 : 128;
+  const int BN = sp->head_odim > 0 ? 32 : ((N % 256 == 0 || N > 512) ? 256 : 128);
   const int64_t lda = sp->conv3x3 ? K / 9 : K;
   CUtensorMap ta, tb;
   if (!make_tmap_2d_bf16(&ta, A, rows, lda, lda, GEMM_BM, GEMM_BK, 128)) return VX_E_ARG;
   if (!make_tmap_2d_bf16(&tb, B, N, K, K, BN, GEMM_BK, 128)) return VX_E_ARG;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int epi = sp->head_odim > 0 ? VX_EPI_HEADOUT : VX_EPI_SPATIAL;
+  if (BN == 32) return launch_gemm<32, VX_EPI_HEADOUT, 0>(ta, tb, args, st);  // N == 32 output head
   return BN == 256 ? dispatch_epi<256>(epi, ta, tb, args, st) : dispatch_epi<128>(epi, ta, tb, args, st);
 }
