@@ -13,16 +13,18 @@
 // warps are still turning S_i(j) into P_i(j): the tensor core runs one KV tile
 // ahead of the softmax (aliasing P onto S, as in the first version, serialised them).
 //
-// Warp roles (640 threads):
+// Warp roles (384 threads):
 //   w0      TMA producer: Q tiles once per unit, K/V tiles through a KST-stage ring
 //   w1      tcgen05.mma issuer (one lane): S_i = Q_i K^T (SS), O_i += P_i V (TS: P from TMEM)
 //   w2      TMEM allocator
-//   w4..w19 softmax + epilogue: 4 warpgroups = (Q tile) x (score columns 0-63 | 64-127);
-//           thread = one query row (TMEM lane); partial row maxima / sums of the two
-//           column halves are exchanged through shared memory.
-// Softmax arithmetic: x = s*scale*log2e - m with FFMA2, 1/4 of the exp2 on the FMA pipe
-// (packed degree-3 polynomial), the rest on MUFU; lazy O rescaling (only when the
-// running max grows by > 2^8); row sums with packed FADD2.
+//   w4..w11 softmax + epilogue: one warpgroup per Q tile; thread = one query row = one TMEM
+//           lane owning all 128 score columns of the KV tile (row max / sum thread-local).
+// Softmax arithmetic: x = s*scale*log2e - m with FFMA2 (packed fp32x2), 2 of every 8 exp pairs
+// on the FMA pipe (packed degree-3 polynomial), the rest on MUFU ex2; FMNMX3 max tree; FADD2
+// row sums; lazy rescaling of O only when the running max grows by > 2^8.  The column mask of
+// the last KV tile lives on a separate code path (BoolTag) so the common path carries none.
+// Measured limits (tools/trace_attn.py, profiles/): MUFU saturated during the exp phase; the
+// S-wait / TMEM-load / max / P-hand-off phases (~1000 clk per KV tile) are where it idles.
 //
 // MMA issue order per KV tile j:  S_0(j+1), S_1(j+1) (as soon as S_i(j) was loaded),
 // PV_0(j) (when P_0(j) is written), PV_1(j).
@@ -54,8 +56,7 @@ struct AttnCfg {
   static constexpr uint32_t LAYOUT = D == 64 ? 2 : 4;  // SWIZZLE_128B / SWIZZLE_64B
   static constexpr uint32_t SBO = 8 * ROW_BYTES;       // 8-row core-matrix group
   static constexpr uint32_t BAR_BYTES = 512;
-  static constexpr uint32_t XCH_BYTES = 4096;          // [2 parity][2 tiles][2 halves][128] fp32
-  static constexpr uint32_t SMEM = (2 + 2 * KST) * TILE_BYTES + 1024 + BAR_BYTES + XCH_BYTES;
+  static constexpr uint32_t SMEM = (2 + 2 * KST) * TILE_BYTES + 1024 + BAR_BYTES;
 };
 
 template <bool B>
@@ -63,9 +64,7 @@ struct BoolTag {
   static constexpr bool value = B;
 };
 
-// SPLIT: 4 softmax warpgroups (tile x column half, partial maxima exchanged in smem; 640 threads)
-// or 2 (one per tile, each thread owns all 128 columns of its row; 384 threads)
-__host__ __device__ constexpr int attn_threads(bool split) { return split ? 640 : 384; }
+constexpr int ATTN_THREADS = 384;  // 4 control warps + 2 softmax warpgroups (one per Q tile)
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
 
 // TMEM column offsets of Q tile i
@@ -73,9 +72,9 @@ __host__ __device__ constexpr uint32_t tm_S(int i) { return i * 256; }
 __host__ __device__ constexpr uint32_t tm_P(int i) { return i * 256 + 128; }
 __host__ __device__ constexpr uint32_t tm_O(int i) { return i * 256 + 192; }
 
-// EMU_PAIRS_OF_8: of every 8 exp pairs, this many use the FMA-pipe polynomial (degree PDEG)
-template <int D, int EMU_PAIRS_OF_8, int PDEG, bool SPLIT>
-__global__ void __launch_bounds__(attn_threads(SPLIT), 1)
+// EMU_PAIRS_OF_8: of every 8 exp pairs, this many use the FMA-pipe polynomial
+template <int D, int EMU_PAIRS_OF_8>
+__global__ void __launch_bounds__(ATTN_THREADS, 1)
     fmha_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                 const __grid_constant__ CUtensorMap tmV, const AttnArgs a) {
   using Cfg = AttnCfg<D>;
@@ -100,7 +99,6 @@ __global__ void __launch_bounds__(attn_threads(SPLIT), 1)
   uint64_t* p_free = p_full + 2;     // [2] MMA -> softmax: PV_i(j) done (P reusable, O stable)
   uint64_t* o_empty = p_free + 2;    // [2] softmax -> MMA: O_i read by the epilogue
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
-  float* xch = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bar) + Cfg::BAR_BYTES);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -119,10 +117,10 @@ __global__ void __launch_bounds__(attn_threads(SPLIT), 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_free[i], SPLIT ? 8 : 4);
-      mbar_init(&p_full[i], SPLIT ? 8 : 4);
+      mbar_init(&s_free[i], 4);
+      mbar_init(&p_full[i], 4);
       mbar_init(&p_free[i], 1);
-      mbar_init(&o_empty[i], SPLIT ? 8 : 4);
+      mbar_init(&o_empty[i], 4);
     }
     fence_barrier_init();
   }
@@ -245,7 +243,7 @@ __global__ void __launch_bounds__(attn_threads(SPLIT), 1)
         }
       }
     }
-  } else if (warp >= 4 && !SPLIT) {
+  } else if (warp >= 4) {
     // ------------------------------------------------------------ softmax / epilogue, one WG per tile
     const int tile = (warp - 4) >> 2;
     const int wl = warp & 3;
@@ -307,7 +305,7 @@ __global__ void __launch_bounds__(attn_threads(SPLIT), 1)
               float x0, x1, p0, p1;
               f2_unpack(x, x0, x1);
               if ((c & 7) >= 8 - EMU_PAIRS_OF_8) {
-                ex2_poly2<PDEG>(x0, x1, p0, p1);
+                ex2_poly2<3>(x0, x1, p0, p1);
               } else {
                 p0 = ex2(x0);
                 p1 = ex2(x1);
@@ -371,148 +369,6 @@ __global__ void __launch_bounds__(attn_threads(SPLIT), 1)
         if (a.lse) a.lse[h * a.Tq + orow] = (m_run + __log2f(l_run)) * 0.69314718055994531f;
       }
     }
-  } else if (warp >= 4) {
-    // ------------------------------------------------------------ softmax / epilogue
-    constexpr int DH = D / 2;
-    const int sw = warp - 4;
-    const int tile = sw >> 3;
-    const int half = (sw >> 2) & 1;
-    const int wl = warp & 3;          // TMEM lane quarter
-    const int r = wl * 32 + lane;     // row within the Q tile
-    const uint32_t lane_off = uint32_t(wl * 32) << 16;
-    const uint32_t S_addr = tmem + lane_off + tm_S(tile) + 64 * half;
-    const uint32_t P_addr = tmem + lane_off + tm_P(tile) + 32 * half;
-    const uint32_t Oh_addr = tmem + lane_off + tm_O(tile) + DH * half;
-    // exchange slots: [parity][tile][half][row]
-    float* const xbase = xch + tile * 256 + r;
-    const float sl2 = a.scale_log2;
-    const uint64_t SL2 = f2_pack(sl2, sl2);
-    uint32_t sph = 0;     // s_full parity
-    uint32_t pv_cnt = 0;  // p_free waits (parity)
-    uint32_t xpar = 0;    // exchange buffer parity
-    for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
-      const int h = u / per_head;
-      const int rem = u - h * per_head;
-      const int s = rem / a.q_blocks;
-      const int qb = rem - s * a.q_blocks;
-      const int q_local = qb * 256 + tile * 128 + r;
-      float m_run = -INFINITY;
-      float l_run = 0.f;  // partial row sum over this half's columns
-      for (int j = 0; j < nkv; ++j) {
-        mbar_wait(&s_full[tile], sph);
-        sph ^= 1;
-        tc_fence_after();
-        uint32_t sr[64];
-        tmem_ld32(S_addr, sr);
-        tmem_ld32(S_addr + 32, sr + 32);
-        tmem_wait_ld();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&s_free[tile]);  // the S buffer may now receive S(j+1)
-        const int valid = a.Lk - 128 * j - 64 * half;
-        // Two copies of the step: the column mask (last KV tile only) must not be speculated
-        // into the common path (the compiler otherwise emits 64 ISETP+SEL on every tile).
-        auto step = [&](auto mask_tag) {
-          if constexpr (decltype(mask_tag)::value) {
-#pragma unroll
-            for (int c = 0; c < 64; ++c)
-              if (c >= valid) sr[c] = 0xff800000u;  // -inf
-          }
-          // partial row max over 64 columns: 4 independent FMNMX3 chains + tree
-          float mq[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) mq[q] = fmaxf(__uint_as_float(sr[q]), __uint_as_float(sr[q + 4]));
-#pragma unroll
-          for (int c = 8; c < 64; c += 8)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) mq[q] = max3(mq[q], __uint_as_float(sr[c + q]), __uint_as_float(sr[c + 4 + q]));
-          const float pmax = fmaxf(max3(mq[0], mq[1], mq[2]), mq[3]);
-          float* xs = xbase + xpar * 512;
-          xs[half * 128] = pmax;
-          named_bar_sync(1 + tile, 256);
-          const float mx = fmaxf(pmax, xs[(half ^ 1) * 128]);
-          xpar ^= 1;
-          const float m_new = mx * sl2;
-          const bool need = m_new > m_run + RESCALE_THRESHOLD;
-          const float alpha = need ? ex2(m_run - m_new) : 1.0f;
-          if (need) m_run = m_new;
-          const uint64_t NEGM = f2_pack(-m_run, -m_run);
-          uint32_t pk[32];
-          uint64_t acc[4] = {0, 0, 0, 0};
-#pragma unroll
-          for (int c = 0; c < 32; ++c) {
-            const uint64_t x = f2_fma(f2_pack(__uint_as_float(sr[2 * c]), __uint_as_float(sr[2 * c + 1])), SL2, NEGM);
-            float x0, x1, p0, p1;
-            f2_unpack(x, x0, x1);
-            if ((c & 7) >= 8 - EMU_PAIRS_OF_8) {  // part of the exps on the FMA pipe
-              ex2_poly2<PDEG>(x0, x1, p0, p1);
-            } else {
-              p0 = ex2(x0);
-              p1 = ex2(x1);
-            }
-            acc[c & 3] = f2_add(acc[c & 3], f2_pack(p0, p1));
-            pk[c] = pack_bf16(p0, p1);
-          }
-          {
-            float a0, a1, b0, b1;
-            f2_unpack(f2_add(acc[0], acc[1]), a0, a1);
-            f2_unpack(f2_add(acc[2], acc[3]), b0, b1);
-            l_run = l_run * alpha + ((a0 + a1) + (b0 + b1));
-          }
-          // P_i(j) may overwrite P_i(j-1) only once PV_i(j-1) has completed (this also makes O stable)
-          if (j > 0) {
-            mbar_wait(&p_free[tile], pv_cnt & 1);
-            ++pv_cnt;
-            tc_fence_after();
-          }
-          tmem_st32(P_addr, pk);
-          if (__any_sync(0xffffffff, need) && j > 0) {  // lazy O correction, each half its D/2 columns
-            uint32_t orr[DH];
-            if constexpr (DH == 32) tmem_ld32(Oh_addr, orr);
-            else tmem_ld16(Oh_addr, orr);
-            tmem_wait_ld();
-#pragma unroll
-            for (int c = 0; c < DH; ++c) orr[c] = __float_as_uint(__uint_as_float(orr[c]) * alpha);
-            if constexpr (DH == 32) tmem_st32(Oh_addr, orr);
-            else tmem_st16(Oh_addr, orr);
-          }
-          tmem_wait_st();
-          tc_fence_before();
-          __syncwarp();
-        };
-        if (valid < 64) step(BoolTag<true>{});
-        else step(BoolTag<false>{});
-        if (lane == 0) mbar_arrive(&p_full[tile]);
-      }
-      // ---- epilogue: O[:, half*D/2 : +D/2] / l -> bf16
-      mbar_wait(&p_free[tile], pv_cnt & 1);  // last PV of this unit
-      ++pv_cnt;
-      tc_fence_after();
-      uint32_t orr[DH];
-      if constexpr (DH == 32) tmem_ld32(Oh_addr, orr);
-      else tmem_ld16(Oh_addr, orr);
-      float* xs = xbase + xpar * 512;
-      xs[half * 128] = l_run;
-      tmem_wait_ld();
-      tc_fence_before();
-      named_bar_sync(1 + tile, 256);
-      const float l_tot = l_run + xs[(half ^ 1) * 128];
-      xpar ^= 1;
-      if (lane == 0) mbar_arrive(&o_empty[tile]);
-      if (q_local < a.Lq) {
-        const float inv = 1.0f / l_tot;
-        const int64_t orow = (int64_t)s * a.Lq + q_local;
-        uint4* dst = reinterpret_cast<uint4*>(a.out + orow * a.ldo + h * D + half * DH);
-#pragma unroll
-        for (int c = 0; c < DH / 8; ++c) {
-#define VX_O(i) (__uint_as_float(orr[8 * c + i]) * inv)
-          dst[c] = make_uint4(pack_bf16(VX_O(0), VX_O(1)), pack_bf16(VX_O(2), VX_O(3)),
-                              pack_bf16(VX_O(4), VX_O(5)), pack_bf16(VX_O(6), VX_O(7)));
-#undef VX_O
-        }
-        if (a.lse && half == 0) a.lse[h * a.Tq + orow] = (m_run + __log2f(l_tot)) * 0.69314718055994531f;
-      }
-    }
   }
   tc_fence_before();
   __syncthreads();
@@ -522,14 +378,14 @@ __global__ void __launch_bounds__(attn_threads(SPLIT), 1)
   }
 }
 
-template <int D, int EMU, int PDEG = 3, bool SPLIT = true>
+template <int D, int EMU>
 static int launch_fmha(const void* q, const void* k, const void* v, const AttnArgs& args, cudaStream_t st) {
   using Cfg = AttnCfg<D>;
   CUtensorMap tq, tk, tv;
   if (!make_tmap_2d_bf16(&tq, q, (uint64_t)args.H * args.Tq, D, D, 128, D, Cfg::SWIZZLE)) return VX_E_ARG;
   if (!make_tmap_2d_bf16(&tk, k, (uint64_t)args.H * args.Tk, D, D, 128, D, Cfg::SWIZZLE)) return VX_E_ARG;
   if (!make_tmap_2d_bf16(&tv, v, (uint64_t)args.H * args.Tk, D, D, 128, D, Cfg::SWIZZLE)) return VX_E_ARG;
-  auto kern = fmha_kernel<D, EMU, PDEG, SPLIT>;
+  auto kern = fmha_kernel<D, EMU>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
@@ -537,7 +393,7 @@ static int launch_fmha(const void* q, const void* k, const void* v, const AttnAr
     attr_set = true;
   }
   const int grid = args.units < num_sms() ? args.units : num_sms();
-  kern<<<grid, attn_threads(SPLIT), Cfg::SMEM, st>>>(tq, tk, tv, args);
+  kern<<<grid, ATTN_THREADS, Cfg::SMEM, st>>>(tq, tk, tv, args);
   VX_CHECK_LAUNCH("fmha launch");
   return VX_OK;
 }
@@ -573,36 +429,14 @@ extern "C" int vx_attention(const void* q, const void* k, const void* v, void* o
     const char* e = getenv("VX_FMHA_EMU");  // diagnostic: exp pairs (of 8) on the FMA pipe
     return e ? atoi(e) : 2;
   }();
-  static int pdeg = [] {
-    const char* e = getenv("VX_FMHA_PDEG");  // diagnostic: polynomial degree (2 or 3)
-    return e ? atoi(e) : 3;
-  }();
-  static int split = [] {
-    const char* e = getenv("VX_FMHA_SPLIT");  // diagnostic: 1 = column-split softmax warpgroups
-    return e ? atoi(e) : 0;
-  }();
-  if (D == 64 && !split) {
-    switch (emu) {
-      case 0: return launch_fmha<64, 0, 3, false>(q, k, v, a, st);
-      case 1: return launch_fmha<64, 1, 3, false>(q, k, v, a, st);
-      case 3: return launch_fmha<64, 3, 3, false>(q, k, v, a, st);
-      default: return launch_fmha<64, 2, 3, false>(q, k, v, a, st);
-    }
-  }
   if (D == 64) {
-    if (pdeg == 2) {
-      switch (emu) {
-        case 2: return launch_fmha<64, 2, 2>(q, k, v, a, st);
-        case 3: return launch_fmha<64, 3, 2>(q, k, v, a, st);
-        default: return launch_fmha<64, 4, 2>(q, k, v, a, st);
-      }
-    }
     switch (emu) {
       case 0: return launch_fmha<64, 0>(q, k, v, a, st);
       case 1: return launch_fmha<64, 1>(q, k, v, a, st);
       case 3: return launch_fmha<64, 3>(q, k, v, a, st);
+      case 4: return launch_fmha<64, 4>(q, k, v, a, st);
       default: return launch_fmha<64, 2>(q, k, v, a, st);
     }
   }
-  return launch_fmha<32, 2, 3, false>(q, k, v, a, st);
+  return launch_fmha<32, 2>(q, k, v, a, st);
 }
