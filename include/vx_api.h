@@ -87,7 +87,7 @@ int vx_gemm(int epi, const void* A, int64_t lda, const void* B, int64_t ldb, int
  *   h*Tq + s*Lq .. +Lq (q) and h*Tk + s*Lk .. +Lk (k, v).
  *   out: bf16, row (s*Lq + i), columns h*D .. h*D+D-1, row stride ldo.
  *   lse: optional fp32 [H, Tq] natural-log log-sum-exp of the scaled scores.
- * D in {32, 64}; scale = 1/sqrt(D). */
+ * D in {32, 64, 128} (128: camera-head trunk); scale = 1/sqrt(D). */
 int vx_attention(const void* q, const void* k, const void* v, void* out, int64_t ldo, float* lse,
                  int D, int H, int nseq, int Lq, int Lk, int64_t Tq, int64_t Tk, void* stream);
 

@@ -49,14 +49,20 @@ struct AttnArgs {
 
 template <int D>
 struct AttnCfg {
-  static constexpr int KST = 3;
-  static constexpr uint32_t ROW_BYTES = D * 2;
-  static constexpr uint32_t TILE_BYTES = 128 * ROW_BYTES;
-  static constexpr int SWIZZLE = D == 64 ? 128 : 64;
-  static constexpr uint32_t LAYOUT = D == 64 ? 2 : 4;  // SWIZZLE_128B / SWIZZLE_64B
-  static constexpr uint32_t SBO = 8 * ROW_BYTES;       // 8-row core-matrix group
+  static constexpr int NT = D == 128 ? 1 : 2;             // 128-row Q tiles per CTA (TMEM budget)
+  static constexpr int KST = D == 128 ? 2 : 3;
+  static constexpr int PANEL_COLS = D == 32 ? 32 : 64;     // one swizzle atom wide (<= 128 B)
+  static constexpr int PANELS = D / PANEL_COLS;            // D = 128: two 64-column panels
+  static constexpr uint32_t ROW_BYTES = PANEL_COLS * 2;    // bytes per row inside a panel
+  static constexpr uint32_t PANEL_BYTES = 128 * ROW_BYTES;
+  static constexpr uint32_t TILE_BYTES = PANELS * PANEL_BYTES;
+  static constexpr int SWIZZLE = D == 32 ? 64 : 128;
+  static constexpr uint32_t LAYOUT = D == 32 ? 4 : 2;      // SWIZZLE_64B / SWIZZLE_128B
+  static constexpr uint32_t SBO = 8 * ROW_BYTES;           // 8-row core-matrix group
+  static constexpr int THREADS = 128 + 128 * NT;
+  static constexpr int ROWS = 128 * NT;                    // query rows per work unit
   static constexpr uint32_t BAR_BYTES = 512;
-  static constexpr uint32_t SMEM = (2 + 2 * KST) * TILE_BYTES + 1024 + BAR_BYTES;
+  static constexpr uint32_t SMEM = (NT + 2 * KST) * TILE_BYTES + 1024 + BAR_BYTES;
 };
 
 template <bool B>
@@ -64,7 +70,6 @@ struct BoolTag {
   static constexpr bool value = B;
 };
 
-constexpr int ATTN_THREADS = 384;  // 4 control warps + 2 softmax warpgroups (one per Q tile)
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
 
 // TMEM column offsets of Q tile i
@@ -74,7 +79,7 @@ __host__ __device__ constexpr uint32_t tm_O(int i) { return i * 256 + 192; }
 
 // EMU_PAIRS_OF_8: of every 8 exp pairs, this many use the FMA-pipe polynomial
 template <int D, int EMU_PAIRS_OF_8>
-__global__ void __launch_bounds__(ATTN_THREADS, 1)
+__global__ void __launch_bounds__(AttnCfg<D>::THREADS, 1)
     fmha_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                 const __grid_constant__ CUtensorMap tmV, const AttnArgs a) {
   using Cfg = AttnCfg<D>;
@@ -83,8 +88,9 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
   // 1024-B alignment by offsetting the __shared__ array itself (keeps the shared address space
   // visible to the compiler: LDS/STS instead of generic loads)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* sQ = smem;                                 // 2 tiles
-  uint8_t* sK = sQ + 2 * Cfg::TILE_BYTES;             // KST tiles
+  constexpr int NT = Cfg::NT;
+  uint8_t* sQ = smem;                                 // NT tiles
+  uint8_t* sK = sQ + NT * Cfg::TILE_BYTES;            // KST tiles
   uint8_t* sV = sK + KST * Cfg::TILE_BYTES;           // KST tiles
   uint64_t* bar = reinterpret_cast<uint64_t*>(sV + KST * Cfg::TILE_BYTES);
   uint64_t* q_full = bar;
@@ -145,20 +151,26 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
         const int rem = u - h * per_head;
         const int s = rem / a.q_blocks;
         const int qb = rem - s * a.q_blocks;
-        const int q_row = int(h * a.Tq + (int64_t)s * a.Lq + qb * 256);
+        const int q_row = int(h * a.Tq + (int64_t)s * a.Lq + qb * Cfg::ROWS);
         const int kv_row = int(h * a.Tk + (int64_t)s * a.Lk);
         mbar_wait(q_empty, (n & 1) ^ 1);
-        mbar_expect_tx(q_full, 2 * Cfg::TILE_BYTES);
-        tma_load_2d_hint(sQ, &tmQ, q_full, 0, q_row, pol_q);
-        tma_load_2d_hint(sQ + Cfg::TILE_BYTES, &tmQ, q_full, 0, q_row + 128, pol_q);
+        mbar_expect_tx(q_full, NT * Cfg::TILE_BYTES);
+        for (int i = 0; i < NT; ++i)
+          for (int pn = 0; pn < Cfg::PANELS; ++pn)
+            tma_load_2d_hint(sQ + i * Cfg::TILE_BYTES + pn * Cfg::PANEL_BYTES, &tmQ, q_full, pn * Cfg::PANEL_COLS,
+                             q_row + 128 * i, pol_q);
         for (int j = 0; j < nkv; ++j, ++c) {
           const uint32_t st = c % KST, ph = (c / KST) & 1;
           mbar_wait(&k_empty[st], ph ^ 1);
           mbar_expect_tx(&k_full[st], Cfg::TILE_BYTES);
-          tma_load_2d_hint(sK + st * Cfg::TILE_BYTES, &tmK, &k_full[st], 0, kv_row + 128 * j, pol_kv);
+          for (int pn = 0; pn < Cfg::PANELS; ++pn)
+            tma_load_2d_hint(sK + st * Cfg::TILE_BYTES + pn * Cfg::PANEL_BYTES, &tmK, &k_full[st],
+                             pn * Cfg::PANEL_COLS, kv_row + 128 * j, pol_kv);
           mbar_wait(&v_empty[st], ph ^ 1);
           mbar_expect_tx(&v_full[st], Cfg::TILE_BYTES);
-          tma_load_2d_hint(sV + st * Cfg::TILE_BYTES, &tmV, &v_full[st], 0, kv_row + 128 * j, pol_kv);
+          for (int pn = 0; pn < Cfg::PANELS; ++pn)
+            tma_load_2d_hint(sV + st * Cfg::TILE_BYTES + pn * Cfg::PANEL_BYTES, &tmV, &v_full[st],
+                             pn * Cfg::PANEL_COLS, kv_row + 128 * j, pol_kv);
         }
       }
     }
@@ -167,19 +179,24 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
     if (elect_one()) {
       constexpr uint32_t idesc_qk = make_idesc_bf16(128, 128, 0, 0);
       constexpr uint32_t idesc_pv = make_idesc_bf16(128, D, 0, 1);
-      const uint32_t q0 = smem_u32(sQ), q1 = q0 + Cfg::TILE_BYTES;
+      const uint32_t q0 = smem_u32(sQ);
+      constexpr int KSTEPS_PER_PANEL = Cfg::PANEL_COLS / 16;
       auto issue_qk = [&](int i, uint32_t ks) {
-        const uint32_t qs = i ? q1 : q0;
+        const uint32_t qs = q0 + i * Cfg::TILE_BYTES;
 #pragma unroll
-        for (int k = 0; k < D / 16; ++k)
-          mma_ss(tmem + tm_S(i), make_sdesc(qs + k * 32, 16, Cfg::SBO, Cfg::LAYOUT),
-                 make_sdesc(ks + k * 32, 16, Cfg::SBO, Cfg::LAYOUT), idesc_qk, k > 0);
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off = (k / KSTEPS_PER_PANEL) * Cfg::PANEL_BYTES + (k % KSTEPS_PER_PANEL) * 32;
+          mma_ss(tmem + tm_S(i), make_sdesc(qs + off, 16, Cfg::SBO, Cfg::LAYOUT),
+                 make_sdesc(ks + off, 16, Cfg::SBO, Cfg::LAYOUT), idesc_qk, k > 0);
+        }
       };
+      // V is the MN-major B operand: for D = 128 its two 64-column panels are the two MN atoms (LBO)
       auto issue_pv = [&](int i, uint32_t vs, uint32_t acc) {
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
           mma_ts(tmem + tm_O(i), tmem + tm_P(i) + kk * 8,
-                 make_sdesc(vs + kk * 16 * Cfg::ROW_BYTES, 16, Cfg::SBO, Cfg::LAYOUT), idesc_pv, (acc | kk) != 0);
+                 make_sdesc(vs + kk * 16 * Cfg::ROW_BYTES, Cfg::PANEL_BYTES, Cfg::SBO, Cfg::LAYOUT), idesc_pv,
+                 (acc | kk) != 0);
       };
       uint32_t c = 0;  // global K/V tile counter
       uint32_t n = 0;  // local unit counter
@@ -192,17 +209,13 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
           mbar_wait(&k_full[st], ph);
           tc_fence_after();
           const uint32_t ks = smem_u32(sK + st * Cfg::TILE_BYTES);
-          if (n > 0) mbar_wait(&s_free[0], sfree_ph);
-          tc_fence_after();
-          issue_qk(0, ks);
-          mma_commit(&s_full[0]);
-          if (n > 0) {
-            mbar_wait(&s_free[1], sfree_ph);
-            sfree_ph ^= 1;
+          for (int i = 0; i < NT; ++i) {
+            if (n > 0) mbar_wait(&s_free[i], sfree_ph);
+            tc_fence_after();
+            issue_qk(i, ks);
+            mma_commit(&s_full[i]);
           }
-          tc_fence_after();
-          issue_qk(1, ks);
-          mma_commit(&s_full[1]);
+          if (n > 0) sfree_ph ^= 1;
           mma_commit(&k_empty[st]);
           if (nkv == 1) mma_commit(q_empty);
         }
@@ -212,38 +225,32 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
             const uint32_t nst = (c + 1) % KST, nph = ((c + 1) / KST) & 1;
             mbar_wait(&k_full[nst], nph);
             const uint32_t nks = smem_u32(sK + nst * Cfg::TILE_BYTES);
-            mbar_wait(&s_free[0], sfree_ph);
-            tc_fence_after();
-            issue_qk(0, nks);
-            mma_commit(&s_full[0]);
-            mbar_wait(&s_free[1], sfree_ph);
+            for (int i = 0; i < NT; ++i) {
+              mbar_wait(&s_free[i], sfree_ph);
+              tc_fence_after();
+              issue_qk(i, nks);
+              mma_commit(&s_full[i]);
+            }
             sfree_ph ^= 1;
-            tc_fence_after();
-            issue_qk(1, nks);
-            mma_commit(&s_full[1]);
             mma_commit(&k_empty[nst]);
             if (j + 2 == nkv) mma_commit(q_empty);
           }
           const uint32_t vs = smem_u32(sV + st * Cfg::TILE_BYTES);
           mbar_wait(&v_full[st], ph);
-          if (j == 0) {  // the previous unit's epilogue must have read O
-            mbar_wait(&o_empty[0], (n & 1) ^ 1);
-            mbar_wait(&o_empty[1], (n & 1) ^ 1);
+          if (j == 0)  // the previous unit's epilogue must have read O
+            for (int i = 0; i < NT; ++i) mbar_wait(&o_empty[i], (n & 1) ^ 1);
+          for (int i = 0; i < NT; ++i) {
+            mbar_wait(&p_full[i], pfull_ph);
+            tc_fence_after();
+            issue_pv(i, vs, j > 0);
+            mma_commit(&p_free[i]);
           }
-          mbar_wait(&p_full[0], pfull_ph);
-          tc_fence_after();
-          issue_pv(0, vs, j > 0);
-          mma_commit(&p_free[0]);
-          mbar_wait(&p_full[1], pfull_ph);
           pfull_ph ^= 1;
-          tc_fence_after();
-          issue_pv(1, vs, j > 0);
-          mma_commit(&p_free[1]);
           mma_commit(&v_empty[st]);
         }
       }
     }
-  } else if (warp >= 4) {
+  } else if (warp >= 4 && warp < 4 + 4 * NT) {
     // ------------------------------------------------------------ softmax / epilogue, one WG per tile
     const int tile = (warp - 4) >> 2;
     const int wl = warp & 3;
@@ -260,7 +267,7 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
       const int rem = u - h * per_head;
       const int s = rem / a.q_blocks;
       const int qb = rem - s * a.q_blocks;
-      const int q_local = qb * 256 + tile * 128 + r;
+      const int q_local = qb * Cfg::ROWS + tile * 128 + r;
       float m_run = -INFINITY;
       float l_run = 0.f;
       for (int j = 0; j < nkv; ++j) {
@@ -382,9 +389,10 @@ template <int D, int EMU>
 static int launch_fmha(const void* q, const void* k, const void* v, const AttnArgs& args, cudaStream_t st) {
   using Cfg = AttnCfg<D>;
   CUtensorMap tq, tk, tv;
-  if (!make_tmap_2d_bf16(&tq, q, (uint64_t)args.H * args.Tq, D, D, 128, D, Cfg::SWIZZLE)) return VX_E_ARG;
-  if (!make_tmap_2d_bf16(&tk, k, (uint64_t)args.H * args.Tk, D, D, 128, D, Cfg::SWIZZLE)) return VX_E_ARG;
-  if (!make_tmap_2d_bf16(&tv, v, (uint64_t)args.H * args.Tk, D, D, 128, D, Cfg::SWIZZLE)) return VX_E_ARG;
+  constexpr int PC = Cfg::PANEL_COLS;
+  if (!make_tmap_2d_bf16(&tq, q, (uint64_t)args.H * args.Tq, D, D, 128, PC, Cfg::SWIZZLE)) return VX_E_ARG;
+  if (!make_tmap_2d_bf16(&tk, k, (uint64_t)args.H * args.Tk, D, D, 128, PC, Cfg::SWIZZLE)) return VX_E_ARG;
+  if (!make_tmap_2d_bf16(&tv, v, (uint64_t)args.H * args.Tk, D, D, 128, PC, Cfg::SWIZZLE)) return VX_E_ARG;
   auto kern = fmha_kernel<D, EMU>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -393,7 +401,7 @@ static int launch_fmha(const void* q, const void* k, const void* v, const AttnAr
     attr_set = true;
   }
   const int grid = args.units < num_sms() ? args.units : num_sms();
-  kern<<<grid, ATTN_THREADS, Cfg::SMEM, st>>>(tq, tk, tv, args);
+  kern<<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(tq, tk, tv, args);
   VX_CHECK_LAUNCH("fmha launch");
   return VX_OK;
 }
@@ -404,7 +412,7 @@ extern "C" int vx_attention(const void* q, const void* k, const void* v, void* o
                             int H, int nseq, int Lq, int Lk, int64_t Tq, int64_t Tk, void* stream) {
   using namespace vx;
   VX_CHECK_ARG(q && k && v && out, "vx_attention: null pointer");
-  VX_CHECK_ARG(D == 32 || D == 64, "vx_attention: head_dim %d unsupported (32, 64)", D);
+  VX_CHECK_ARG(D == 32 || D == 64 || D == 128, "vx_attention: head_dim %d unsupported (32, 64, 128)", D);
   VX_CHECK_ARG(H > 0 && nseq > 0 && Lq > 0 && Lk > 0, "vx_attention: empty problem");
   VX_CHECK_ARG((int64_t)nseq * Lq <= Tq && (int64_t)nseq * Lk <= Tk, "vx_attention: sequences exceed buffers");
   VX_CHECK_ARG((int64_t)H * Tq + 512 < (1ll << 31) && (int64_t)H * Tk + 512 < (1ll << 31),
@@ -417,7 +425,8 @@ extern "C" int vx_attention(const void* q, const void* k, const void* v, void* o
   a.Lk = Lk;
   a.Tq = Tq;
   a.Tk = Tk;
-  a.q_blocks = (Lq + 255) / 256;
+  const int rows_per_unit = D == 128 ? AttnCfg<128>::ROWS : 256;
+  a.q_blocks = (Lq + rows_per_unit - 1) / rows_per_unit;
   a.kv_tiles = (Lk + 127) / 128;
   a.units = H * nseq * a.q_blocks;
   a.scale_log2 = (1.0f / sqrtf(float(D))) * 1.4426950408889634f;
@@ -438,5 +447,6 @@ extern "C" int vx_attention(const void* q, const void* k, const void* v, void* o
       default: return launch_fmha<64, 2>(q, k, v, a, st);
     }
   }
+  if (D == 128) return launch_fmha<128, 2>(q, k, v, a, st);
   return launch_fmha<32, 2>(q, k, v, a, st);
 }

@@ -1,7 +1,8 @@
 """Camera head and frame-chunked DPT heads on the device.
 
 Precision policy ("bf16 except MLP in heads", `PAPER.md:81`):
-  * camera-head trunk (4 blocks, dim 2C) and AdaLN modulation: bf16 GEMMs on the
+  * camera-head trunk (4 blocks, dim 2C, attention across the S camera tokens
+    with head_dim 128 on the vx FMHA) and AdaLN modulation: bf16 GEMMs on the
     vx tcgen05 kernel with fp32 residual stream; the pose branch MLP, pose
     embedding and activation stay fp32;
   * DPT heads: entirely on the vx kernels — LayerNorm, 1x1 projections,
@@ -32,10 +33,10 @@ def _trunk_block(W: DeviceWeights, name: str, x: torch.Tensor, num_heads: int, e
     d = D // num_heads
     xn = ops.layernorm(x, W[name + ".norm1.weight"], W[name + ".norm1.bias"], eps)
     qkv = ops.gemm(xn, W[name + ".attn.qkv.weight"], ops.EPI_BF16, bias=W[name + ".attn.qkv.bias"])
-    q, k, v = qkv.view(S, 3, num_heads, d).permute(1, 2, 0, 3).unbind(0)
-    # attention across the S camera tokens, head_dim 128: library SDPA (tiny: S x S per head)
-    o = F.scaled_dot_product_attention(q[None], k[None], v[None])[0]
-    o = o.permute(1, 0, 2).reshape(S, D).contiguous()
+    q, k, v = (t.contiguous() for t in qkv.view(S, 3, num_heads, d).permute(1, 2, 0, 3).unbind(0))
+    # attention across the S camera tokens (head_dim 128) on the vx FMHA
+    o = torch.empty(S, D, device=x.device, dtype=torch.bfloat16)
+    ops.attention(q, k, v, o, nseq=1, Lq=S, Lk=S)
     ops.gemm(o, W[name + ".attn.proj.weight"], ops.EPI_RESID, bias=W[name + ".attn.proj.bias"], resid=x,
              gamma=W[name + ".ls1.gamma"])
     xn = ops.layernorm(x, W[name + ".norm2.weight"], W[name + ".norm2.bias"], eps)
