@@ -16,6 +16,7 @@
 #include "../../include/vx_api.h"
 #include "common.cuh"
 #include "host_util.h"
+#include <stdlib.h>
 
 namespace vx {
 
@@ -330,7 +331,10 @@ VX_DEVICE void epi_headout(const GemmArgs& a, const PixInfo& pi, const uint32_t*
 // ---------------------------------------------------------------------------
 // kernel
 // ---------------------------------------------------------------------------
-template <int BN, int EPI, int HD>
+// MC: clusters of 2 CTAs on adjacent M tiles (same N tile); each CTA TMA-loads half of the
+// B tile and multicasts it to both, halving the per-SM L2->SMEM traffic of the main loop
+// (a 128x256 tile needs ~94 B/clk/SM from L2 otherwise — above the chip's L2 throughput).
+template <int BN, int EPI, int HD, bool MC>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const GemmArgs args) {
@@ -351,15 +355,24 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int M = args.M, N = args.N, K = args.K;
   const int num_n = (N + BN - 1) / BN;
   const int num_m = (M + GEMM_BM - 1) / GEMM_BM;
-  const int tiles = num_m * num_n;
   const int kblocks = K / GEMM_BK;
+  // work decomposition: MC clusters walk (M-tile pair, N tile) units; otherwise single tiles
+  const uint32_t crank = MC ? cluster_ctarank() : 0;
+  const int units = MC ? ((num_m + 1) / 2) * num_n : num_m * num_n;
+  const int unit0 = MC ? int(blockIdx.x >> 1) : int(blockIdx.x);
+  const int ustep = MC ? int(gridDim.x >> 1) : int(gridDim.x);
+  auto tile_mn = [&](int u, int& m_blk, int& n_blk) {
+    const int mu = u / num_n;
+    n_blk = u - mu * num_n;
+    m_blk = MC ? 2 * mu + int(crank) : mu;
+  };
 
   if (warp == 0 && elect_one()) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], MC ? 2 : 1);  // MC: released by both CTAs' MMA warps
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
@@ -370,6 +383,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   if (warp == 2) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
   tc_fence_before();
   __syncthreads();
+  if constexpr (MC) cluster_sync();  // peer barriers initialised before any multicast / remote arrive
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -378,8 +392,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const uint64_t pol_b = policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-        const int m_blk = tile / num_n, n_blk = tile - m_blk * num_n;
+      for (int u = unit0; u < units; u += ustep) {
+        int m_blk, n_blk;
+        tile_mn(u, m_blk, n_blk);
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], Cfg::A_BYTES + Cfg::B_BYTES);
@@ -390,7 +405,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             a_row += (t / 3) * args.conv_w2 + (t % 3);
           }
           tma_load_2d(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], a_col, a_row);
-          tma_load_2d_hint(sB + stage * Cfg::B_BYTES, &tmB, &full[stage], kb * GEMM_BK, n_blk * BN, pol_b);
+          if constexpr (MC) {  // my half of the B tile, multicast to both CTAs of the pair
+            tma_load_2d_mc(sB + stage * Cfg::B_BYTES + crank * (Cfg::B_BYTES / 2), &tmB, &full[stage], kb * GEMM_BK,
+                           n_blk * BN + int(crank) * (BN / 2), 0x3, pol_b);
+          } else {
+            tma_load_2d_hint(sB + stage * Cfg::B_BYTES, &tmB, &full[stage], kb * GEMM_BK, n_blk * BN, pol_b);
+          }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -402,7 +422,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+      for (int u = unit0; u < units; u += ustep) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -416,7 +436,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             mma_ss(d_tmem, make_sdesc(a0 + k * 32, 16, 1024, 2), make_sdesc(b0 + k * 32, 16, 1024, 2), idesc,
                    (kb | k) != 0);
           }
-          mma_commit(&empty[stage]);
+          if constexpr (MC) mma_commit_mc(&empty[stage], 0x3);  // stage free in both CTAs' producers
+          else mma_commit(&empty[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
         mma_commit(&tfull[acc]);
@@ -430,8 +451,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const int c_end = BN <= 32 ? BN : c_beg + BN / 2;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-      const int m_blk = tile / num_n, n_blk = tile - m_blk * num_n;
+    for (int u = unit0; u < units; u += ustep) {
+      int m_blk, n_blk;
+      tile_mn(u, m_blk, n_blk);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int row = m_blk * GEMM_BM + ew * 32 + lane;
@@ -481,47 +503,77 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (MC) cluster_sync();  // no CTA leaves while its peer may still multicast / arrive
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
   }
 }
 
-template <int BN, int EPI, int HD>
+template <int BN, int EPI, int HD, bool MC = false>
 static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& args, cudaStream_t st) {
   using Cfg = GemmCfg<BN>;
-  auto kern = gemm_kernel<BN, EPI, HD>;
+  auto kern = gemm_kernel<BN, EPI, HD, MC>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     if (e != cudaSuccess) return fail_cuda(e, "gemm: cudaFuncSetAttribute");
     attr_set = true;
   }
-  const int tiles = ((args.M + GEMM_BM - 1) / GEMM_BM) * ((args.N + BN - 1) / BN);
-  const int grid = tiles < num_sms() ? tiles : num_sms();
-  kern<<<grid, GEMM_THREADS, Cfg::SMEM, st>>>(ta, tb, args);
+  const int num_m = (args.M + GEMM_BM - 1) / GEMM_BM, num_n = (args.N + BN - 1) / BN;
+  if constexpr (MC) {
+    const int units = ((num_m + 1) / 2) * num_n;
+    const int clusters = units < num_sms() / 2 ? units : num_sms() / 2;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * clusters);
+    cfg.blockDim = dim3(GEMM_THREADS);
+    cfg.dynamicSmemBytes = Cfg::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, args);
+    if (e != cudaSuccess) return fail_cuda(e, "gemm cluster launch");
+  } else {
+    const int tiles = num_m * num_n;
+    const int grid = tiles < num_sms() ? tiles : num_sms();
+    kern<<<grid, GEMM_THREADS, Cfg::SMEM, st>>>(ta, tb, args);
+  }
   VX_CHECK_LAUNCH("gemm launch");
   return VX_OK;
 }
 
-template <int BN>
+template <int BN, bool MC = false>
 static int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, cudaStream_t st) {
   switch (epi) {
-    case VX_EPI_BF16: return launch_gemm<BN, VX_EPI_BF16, 0>(ta, tb, a, st);
-    case VX_EPI_GELU: return launch_gemm<BN, VX_EPI_GELU, 0>(ta, tb, a, st);
-    case VX_EPI_RESID: return launch_gemm<BN, VX_EPI_RESID, 0>(ta, tb, a, st);
-    case VX_EPI_PATCH: return launch_gemm<BN, VX_EPI_PATCH, 0>(ta, tb, a, st);
-    case VX_EPI_F32: return launch_gemm<BN, VX_EPI_F32, 0>(ta, tb, a, st);
-    case VX_EPI_SPATIAL: return launch_gemm<BN, VX_EPI_SPATIAL, 0>(ta, tb, a, st);
-    case VX_EPI_HEADOUT: return launch_gemm<BN, VX_EPI_HEADOUT, 0>(ta, tb, a, st);
+    case VX_EPI_BF16: return launch_gemm<BN, VX_EPI_BF16, 0, MC>(ta, tb, a, st);
+    case VX_EPI_GELU: return launch_gemm<BN, VX_EPI_GELU, 0, MC>(ta, tb, a, st);
+    case VX_EPI_RESID: return launch_gemm<BN, VX_EPI_RESID, 0, MC>(ta, tb, a, st);
+    case VX_EPI_PATCH: return launch_gemm<BN, VX_EPI_PATCH, 0, MC>(ta, tb, a, st);
+    case VX_EPI_F32: return launch_gemm<BN, VX_EPI_F32, 0, MC>(ta, tb, a, st);
+    case VX_EPI_SPATIAL: return launch_gemm<BN, VX_EPI_SPATIAL, 0, MC>(ta, tb, a, st);
+    case VX_EPI_HEADOUT: return launch_gemm<BN, VX_EPI_HEADOUT, 0, MC>(ta, tb, a, st);
     case VX_EPI_QKV:
-      if (a.ep.head_dim == 64) return launch_gemm<BN, VX_EPI_QKV, 64>(ta, tb, a, st);
-      if (a.ep.head_dim == 32) return launch_gemm<BN, VX_EPI_QKV, 32>(ta, tb, a, st);
+      if (a.ep.head_dim == 64) return launch_gemm<BN, VX_EPI_QKV, 64, MC>(ta, tb, a, st);
+      if (a.ep.head_dim == 32) return launch_gemm<BN, VX_EPI_QKV, 32, MC>(ta, tb, a, st);
       set_error("vx_gemm: qkv epilogue needs head_dim 32 or 64 (got %d)", a.ep.head_dim);
       return VX_E_ARG;
   }
   set_error("vx_gemm: unknown epilogue %d", epi);
   return VX_E_ARG;
+}
+
+// B-multicast clusters for the large 256-wide-N GEMMs (enough M tiles to pair up)
+static bool use_multicast(int BN, int M) {
+  static int env = [] {
+    const char* e = getenv("VX_GEMM_MC");  // diagnostic: 0 disables the B-tile multicast
+    return e ? atoi(e) : 1;
+  }();
+  return env && BN == 256 && M >= 8 * GEMM_BM;
 }
 
 }  // namespace vx
@@ -548,10 +600,12 @@ extern "C" int vx_gemm(int epi, const void* A, int64_t lda, const void* B, int64
   args.K = K;
   args.ep = *ep;
   const int BN = (N % 256 == 0 || N > 512) ? 256 : 128;
+  const bool mc = use_multicast(BN, M);
   CUtensorMap ta, tb;
   if (!make_tmap_2d_bf16(&ta, A, M, K, lda, GEMM_BM, GEMM_BK, 128)) return VX_E_ARG;
-  if (!make_tmap_2d_bf16(&tb, B, N, K, ldb, BN, GEMM_BK, 128)) return VX_E_ARG;
+  if (!make_tmap_2d_bf16(&tb, B, N, K, ldb, mc ? BN / 2 : BN, GEMM_BK, 128)) return VX_E_ARG;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (mc) return dispatch_epi<256, true>(epi, ta, tb, args, st);
   return BN == 256 ? dispatch_epi<256>(epi, ta, tb, args, st) : dispatch_epi<128>(epi, ta, tb, args, st);
 }
 
@@ -587,11 +641,13 @@ extern "C" int vx_gemm_spatial(const void* A, const void* B, int N, int K, const
   args.M = int(rows);
   const int BN = sp->head_odim > 0 ? 32 : ((N % 256 == 0 || N > 512) ? 256 : 128);
   const int64_t lda = sp->conv3x3 ? K / 9 : K;
+  const bool mc = use_multicast(BN, int(rows));
   CUtensorMap ta, tb;
   if (!make_tmap_2d_bf16(&ta, A, rows, lda, lda, GEMM_BM, GEMM_BK, 128)) return VX_E_ARG;
-  if (!make_tmap_2d_bf16(&tb, B, N, K, K, BN, GEMM_BK, 128)) return VX_E_ARG;
+  if (!make_tmap_2d_bf16(&tb, B, N, K, K, mc ? BN / 2 : BN, GEMM_BK, 128)) return VX_E_ARG;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int epi = sp->head_odim > 0 ? VX_EPI_HEADOUT : VX_EPI_SPATIAL;
   if (BN == 32) return launch_gemm<32, VX_EPI_HEADOUT, 0>(ta, tb, args, st);  // N == 32 output head
+  if (mc) return launch_gemm<256, VX_EPI_SPATIAL, 0, true>(ta, tb, args, st);
   return BN == 256 ? dispatch_epi<256>(epi, ta, tb, args, st) : dispatch_epi<128>(epi, ta, tb, args, st);
 }
