@@ -47,22 +47,31 @@ struct AttnArgs {
   float* lse;
 };
 
-template <int D>
+template <int D, int NT_ = (D == 128 ? 1 : 2), int BKV_ = 128>
 struct AttnCfg {
-  static constexpr int NT = D == 128 ? 1 : 2;             // 128-row Q tiles per CTA (TMEM budget)
-  static constexpr int KST = D == 128 ? 2 : 3;
+  static constexpr int NT = NT_;                           // 128-row Q tiles per CTA (TMEM budget)
+  static constexpr int BKV = BKV_;                         // KV rows per tile (score columns)
+  static constexpr int KST = D == 128 ? 2 : (BKV == 64 ? 4 : 3);
   static constexpr int PANEL_COLS = D == 32 ? 32 : 64;     // one swizzle atom wide (<= 128 B)
   static constexpr int PANELS = D / PANEL_COLS;            // D = 128: two 64-column panels
   static constexpr uint32_t ROW_BYTES = PANEL_COLS * 2;    // bytes per row inside a panel
-  static constexpr uint32_t PANEL_BYTES = 128 * ROW_BYTES;
-  static constexpr uint32_t TILE_BYTES = PANELS * PANEL_BYTES;
+  static constexpr uint32_t QPANEL_BYTES = 128 * ROW_BYTES;
+  static constexpr uint32_t KVPANEL_BYTES = BKV * ROW_BYTES;
+  static constexpr uint32_t Q_TILE_BYTES = PANELS * QPANEL_BYTES;
+  static constexpr uint32_t KV_TILE_BYTES = PANELS * KVPANEL_BYTES;
   static constexpr int SWIZZLE = D == 32 ? 64 : 128;
   static constexpr uint32_t LAYOUT = D == 32 ? 4 : 2;      // SWIZZLE_64B / SWIZZLE_128B
   static constexpr uint32_t SBO = 8 * ROW_BYTES;           // 8-row core-matrix group
   static constexpr int THREADS = 128 + 128 * NT;
   static constexpr int ROWS = 128 * NT;                    // query rows per work unit
   static constexpr uint32_t BAR_BYTES = 512;
-  static constexpr uint32_t SMEM = (NT + 2 * KST) * TILE_BYTES + 1024 + BAR_BYTES;
+  static constexpr uint32_t SMEM = NT * Q_TILE_BYTES + 2 * KST * KV_TILE_BYTES + 1024 + BAR_BYTES;
+  // TMEM columns: S_i [BKV fp32] ... | P_i [BKV/2] ... | O_i [D fp32] ...
+  static constexpr uint32_t O_BASE = ((NT * BKV + NT * BKV / 2) + 63) / 64 * 64;
+  static_assert(O_BASE + NT * D <= 512, "TMEM budget");
+  static __host__ __device__ constexpr uint32_t tS(int i) { return i * BKV; }
+  static __host__ __device__ constexpr uint32_t tP(int i) { return NT * BKV + i * (BKV / 2); }
+  static __host__ __device__ constexpr uint32_t tO(int i) { return O_BASE + i * D; }
 };
 
 template <bool B>
@@ -72,17 +81,14 @@ struct BoolTag {
 
 constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
 
-// TMEM column offsets of Q tile i
-__host__ __device__ constexpr uint32_t tm_S(int i) { return i * 256; }
-__host__ __device__ constexpr uint32_t tm_P(int i) { return i * 256 + 128; }
-__host__ __device__ constexpr uint32_t tm_O(int i) { return i * 256 + 192; }
 
 // EMU_PAIRS_OF_8: of every 8 exp pairs, this many use the FMA-pipe polynomial
-template <int D, int EMU_PAIRS_OF_8>
-__global__ void __launch_bounds__(AttnCfg<D>::THREADS, 1)
+template <int D, int EMU_PAIRS_OF_8, int NT_, int BKV_>
+__global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_>::THREADS, 1)
     fmha_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                 const __grid_constant__ CUtensorMap tmV, const AttnArgs a) {
-  using Cfg = AttnCfg<D>;
+  using Cfg = AttnCfg<D, NT_, BKV_>;
+  constexpr int BKV = Cfg::BKV;
   constexpr int KST = Cfg::KST;
   extern __shared__ uint8_t smem_raw[];
   // 1024-B alignment by offsetting the __shared__ array itself (keeps the shared address space
@@ -90,21 +96,21 @@ __global__ void __launch_bounds__(AttnCfg<D>::THREADS, 1)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   constexpr int NT = Cfg::NT;
   uint8_t* sQ = smem;                                 // NT tiles
-  uint8_t* sK = sQ + NT * Cfg::TILE_BYTES;            // KST tiles
-  uint8_t* sV = sK + KST * Cfg::TILE_BYTES;           // KST tiles
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sV + KST * Cfg::TILE_BYTES);
+  uint8_t* sK = sQ + NT * Cfg::Q_TILE_BYTES;          // KST tiles
+  uint8_t* sV = sK + KST * Cfg::KV_TILE_BYTES;        // KST tiles
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sV + KST * Cfg::KV_TILE_BYTES);
   uint64_t* q_full = bar;
   uint64_t* q_empty = bar + 1;
   uint64_t* k_full = bar + 2;
   uint64_t* k_empty = k_full + KST;
   uint64_t* v_full = k_empty + KST;
   uint64_t* v_empty = v_full + KST;
-  uint64_t* s_full = v_empty + KST;  // [2] MMA -> softmax: S_i(j) computed
-  uint64_t* s_free = s_full + 2;     // [2] softmax -> MMA: S_i(j) loaded, buffer reusable
-  uint64_t* p_full = s_free + 2;     // [2] softmax -> MMA: P_i(j) written (O rescaled)
-  uint64_t* p_free = p_full + 2;     // [2] MMA -> softmax: PV_i(j) done (P reusable, O stable)
-  uint64_t* o_empty = p_free + 2;    // [2] softmax -> MMA: O_i read by the epilogue
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
+  uint64_t* s_full = v_empty + KST;  // [NT] MMA -> softmax: S_i(j) computed
+  uint64_t* s_free = s_full + NT;    // [NT] softmax -> MMA: S_i(j) loaded, buffer reusable
+  uint64_t* p_full = s_free + NT;    // [NT] softmax -> MMA: P_i(j) written (O rescaled)
+  uint64_t* p_free = p_full + NT;    // [NT] MMA -> softmax: PV_i(j) done (P reusable, O stable)
+  uint64_t* o_empty = p_free + NT;   // [NT] softmax -> MMA: O_i read by the epilogue
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + NT);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -121,7 +127,7 @@ __global__ void __launch_bounds__(AttnCfg<D>::THREADS, 1)
       mbar_init(&v_full[s], 1);
       mbar_init(&v_empty[s], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NT; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&s_free[i], 4);
       mbar_init(&p_full[i], 4);
@@ -154,48 +160,50 @@ __global__ void __launch_bounds__(AttnCfg<D>::THREADS, 1)
         const int q_row = int(h * a.Tq + (int64_t)s * a.Lq + qb * Cfg::ROWS);
         const int kv_row = int(h * a.Tk + (int64_t)s * a.Lk);
         mbar_wait(q_empty, (n & 1) ^ 1);
-        mbar_expect_tx(q_full, NT * Cfg::TILE_BYTES);
+        mbar_expect_tx(q_full, NT * Cfg::Q_TILE_BYTES);
         for (int i = 0; i < NT; ++i)
           for (int pn = 0; pn < Cfg::PANELS; ++pn)
-            tma_load_2d_hint(sQ + i * Cfg::TILE_BYTES + pn * Cfg::PANEL_BYTES, &tmQ, q_full, pn * Cfg::PANEL_COLS,
-                             q_row + 128 * i, pol_q);
+            tma_load_2d_hint(sQ + i * Cfg::Q_TILE_BYTES + pn * Cfg::QPANEL_BYTES, &tmQ, q_full,
+                             pn * Cfg::PANEL_COLS, q_row + 128 * i, pol_q);
         for (int j = 0; j < nkv; ++j, ++c) {
           const uint32_t st = c % KST, ph = (c / KST) & 1;
           mbar_wait(&k_empty[st], ph ^ 1);
-          mbar_expect_tx(&k_full[st], Cfg::TILE_BYTES);
+          mbar_expect_tx(&k_full[st], Cfg::KV_TILE_BYTES);
           for (int pn = 0; pn < Cfg::PANELS; ++pn)
-            tma_load_2d_hint(sK + st * Cfg::TILE_BYTES + pn * Cfg::PANEL_BYTES, &tmK, &k_full[st],
-                             pn * Cfg::PANEL_COLS, kv_row + 128 * j, pol_kv);
+            tma_load_2d_hint(sK + st * Cfg::KV_TILE_BYTES + pn * Cfg::KVPANEL_BYTES, &tmK, &k_full[st],
+                             pn * Cfg::PANEL_COLS, kv_row + BKV * j, pol_kv);
           mbar_wait(&v_empty[st], ph ^ 1);
-          mbar_expect_tx(&v_full[st], Cfg::TILE_BYTES);
+          mbar_expect_tx(&v_full[st], Cfg::KV_TILE_BYTES);
           for (int pn = 0; pn < Cfg::PANELS; ++pn)
-            tma_load_2d_hint(sV + st * Cfg::TILE_BYTES + pn * Cfg::PANEL_BYTES, &tmV, &v_full[st],
-                             pn * Cfg::PANEL_COLS, kv_row + 128 * j, pol_kv);
+            tma_load_2d_hint(sV + st * Cfg::KV_TILE_BYTES + pn * Cfg::KVPANEL_BYTES, &tmV, &v_full[st],
+                             pn * Cfg::PANEL_COLS, kv_row + BKV * j, pol_kv);
         }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     if (elect_one()) {
-      constexpr uint32_t idesc_qk = make_idesc_bf16(128, 128, 0, 0);
+      constexpr uint32_t idesc_qk = make_idesc_bf16(128, BKV, 0, 0);
       constexpr uint32_t idesc_pv = make_idesc_bf16(128, D, 0, 1);
       const uint32_t q0 = smem_u32(sQ);
       constexpr int KSTEPS_PER_PANEL = Cfg::PANEL_COLS / 16;
       auto issue_qk = [&](int i, uint32_t ks) {
-        const uint32_t qs = q0 + i * Cfg::TILE_BYTES;
+        const uint32_t qs = q0 + i * Cfg::Q_TILE_BYTES;
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
-          const uint32_t off = (k / KSTEPS_PER_PANEL) * Cfg::PANEL_BYTES + (k % KSTEPS_PER_PANEL) * 32;
-          mma_ss(tmem + tm_S(i), make_sdesc(qs + off, 16, Cfg::SBO, Cfg::LAYOUT),
-                 make_sdesc(ks + off, 16, Cfg::SBO, Cfg::LAYOUT), idesc_qk, k > 0);
+          const uint32_t kstep = (k % KSTEPS_PER_PANEL) * 32;
+          const uint32_t qoff = (k / KSTEPS_PER_PANEL) * Cfg::QPANEL_BYTES + kstep;
+          const uint32_t koff = (k / KSTEPS_PER_PANEL) * Cfg::KVPANEL_BYTES + kstep;
+          mma_ss(tmem + Cfg::tS(i), make_sdesc(qs + qoff, 16, Cfg::SBO, Cfg::LAYOUT),
+                 make_sdesc(ks + koff, 16, Cfg::SBO, Cfg::LAYOUT), idesc_qk, k > 0);
         }
       };
       // V is the MN-major B operand: for D = 128 its two 64-column panels are the two MN atoms (LBO)
       auto issue_pv = [&](int i, uint32_t vs, uint32_t acc) {
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          mma_ts(tmem + tm_O(i), tmem + tm_P(i) + kk * 8,
-                 make_sdesc(vs + kk * 16 * Cfg::ROW_BYTES, Cfg::PANEL_BYTES, Cfg::SBO, Cfg::LAYOUT), idesc_pv,
+        for (int kk = 0; kk < BKV / 16; ++kk)
+          mma_ts(tmem + Cfg::tO(i), tmem + Cfg::tP(i) + kk * 8,
+                 make_sdesc(vs + kk * 16 * Cfg::ROW_BYTES, Cfg::KVPANEL_BYTES, Cfg::SBO, Cfg::LAYOUT), idesc_pv,
                  (acc | kk) != 0);
       };
       uint32_t c = 0;  // global K/V tile counter
@@ -208,7 +216,7 @@ __global__ void __launch_bounds__(AttnCfg<D>::THREADS, 1)
           const uint32_t st = c % KST, ph = (c / KST) & 1;
           mbar_wait(&k_full[st], ph);
           tc_fence_after();
-          const uint32_t ks = smem_u32(sK + st * Cfg::TILE_BYTES);
+          const uint32_t ks = smem_u32(sK + st * Cfg::KV_TILE_BYTES);
           for (int i = 0; i < NT; ++i) {
             if (n > 0) mbar_wait(&s_free[i], sfree_ph);
             tc_fence_after();
@@ -224,7 +232,7 @@ __global__ void __launch_bounds__(AttnCfg<D>::THREADS, 1)
           if (j + 1 < nkv) {  // run one KV tile ahead: S(j+1) as soon as S(j) has been loaded
             const uint32_t nst = (c + 1) % KST, nph = ((c + 1) / KST) & 1;
             mbar_wait(&k_full[nst], nph);
-            const uint32_t nks = smem_u32(sK + nst * Cfg::TILE_BYTES);
+            const uint32_t nks = smem_u32(sK + nst * Cfg::KV_TILE_BYTES);
             for (int i = 0; i < NT; ++i) {
               mbar_wait(&s_free[i], sfree_ph);
               tc_fence_after();
@@ -235,7 +243,7 @@ __global__ void __launch_bounds__(AttnCfg<D>::THREADS, 1)
             mma_commit(&k_empty[nst]);
             if (j + 2 == nkv) mma_commit(q_empty);
           }
-          const uint32_t vs = smem_u32(sV + st * Cfg::TILE_BYTES);
+          const uint32_t vs = smem_u32(sV + st * Cfg::KV_TILE_BYTES);
           mbar_wait(&v_full[st], ph);
           if (j == 0)  // the previous unit's epilogue must have read O
             for (int i = 0; i < NT; ++i) mbar_wait(&o_empty[i], (n & 1) ^ 1);
@@ -256,9 +264,9 @@ __global__ void __launch_bounds__(AttnCfg<D>::THREADS, 1)
     const int wl = warp & 3;
     const int r = wl * 32 + lane;
     const uint32_t lane_off = uint32_t(wl * 32) << 16;
-    const uint32_t S_addr = tmem + lane_off + tm_S(tile);
-    const uint32_t P_addr = tmem + lane_off + tm_P(tile);
-    const uint32_t O_addr = tmem + lane_off + tm_O(tile);
+    const uint32_t S_addr = tmem + lane_off + Cfg::tS(tile);
+    const uint32_t P_addr = tmem + lane_off + Cfg::tP(tile);
+    const uint32_t O_addr = tmem + lane_off + Cfg::tO(tile);
     const float sl2 = a.scale_log2;
     const uint64_t SL2 = f2_pack(sl2, sl2);
     uint32_t sph = 0, pv_cnt = 0;
@@ -274,28 +282,31 @@ __global__ void __launch_bounds__(AttnCfg<D>::THREADS, 1)
         mbar_wait(&s_full[tile], sph);
         sph ^= 1;
         tc_fence_after();
-        uint32_t sr[128];
+        uint32_t sr[BKV];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) tmem_ld32(S_addr + 32 * c, sr + 32 * c);
+        for (int c = 0; c < BKV / 32; ++c) tmem_ld32(S_addr + 32 * c, sr + 32 * c);
         tmem_wait_ld();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&s_free[tile]);
-        const int valid = a.Lk - 128 * j;
+        const int valid = a.Lk - BKV * j;
         auto step = [&](auto mask_tag) {
           if constexpr (decltype(mask_tag)::value) {
 #pragma unroll
-            for (int c = 0; c < 128; ++c)
+            for (int c = 0; c < BKV; ++c)
               if (c >= valid) sr[c] = 0xff800000u;
           }
-          float mq[8];
+          constexpr int CH = BKV / 16;  // independent FMNMX3 chains
+          float mq[CH];
 #pragma unroll
-          for (int q = 0; q < 8; ++q) mq[q] = fmaxf(__uint_as_float(sr[q]), __uint_as_float(sr[q + 8]));
+          for (int q = 0; q < CH; ++q) mq[q] = fmaxf(__uint_as_float(sr[q]), __uint_as_float(sr[q + CH]));
 #pragma unroll
-          for (int c = 16; c < 128; c += 16)
+          for (int c = 2 * CH; c < BKV; c += 2 * CH)
 #pragma unroll
-            for (int q = 0; q < 8; ++q) mq[q] = max3(mq[q], __uint_as_float(sr[c + q]), __uint_as_float(sr[c + 8 + q]));
-          const float mx = fmaxf(max3(mq[0], mq[1], mq[2]), max3(max3(mq[3], mq[4], mq[5]), mq[6], mq[7]));
+            for (int q = 0; q < CH; ++q) mq[q] = max3(mq[q], __uint_as_float(sr[c + q]), __uint_as_float(sr[c + CH + q]));
+          float mx = mq[0];
+#pragma unroll
+          for (int q = 1; q < CH; ++q) mx = fmaxf(mx, mq[q]);
           const float m_new = mx * sl2;
           const bool need = m_new > m_run + RESCALE_THRESHOLD;
           const float alpha = need ? ex2(m_run - m_new) : 1.0f;
@@ -303,7 +314,7 @@ __global__ void __launch_bounds__(AttnCfg<D>::THREADS, 1)
           const uint64_t NEGM = f2_pack(-m_run, -m_run);
           uint64_t acc[4] = {0, 0, 0, 0};
 #pragma unroll
-          for (int hf = 0; hf < 2; ++hf) {
+          for (int hf = 0; hf < BKV / 64; ++hf) {
             uint32_t pk[32];
 #pragma unroll
             for (int c = 0; c < 32; ++c) {
@@ -345,7 +356,7 @@ __global__ void __launch_bounds__(AttnCfg<D>::THREADS, 1)
             }
           }
         };
-        if (valid < 128) step(BoolTag<true>{});
+        if (valid < BKV) step(BoolTag<true>{});
         else step(BoolTag<false>{});
         tmem_wait_st();
         tc_fence_before();
@@ -385,15 +396,18 @@ __global__ void __launch_bounds__(AttnCfg<D>::THREADS, 1)
   }
 }
 
-template <int D, int EMU>
-static int launch_fmha(const void* q, const void* k, const void* v, const AttnArgs& args, cudaStream_t st) {
-  using Cfg = AttnCfg<D>;
+template <int D, int EMU, int NT = (D == 128 ? 1 : 2), int BKV = 128>
+static int launch_fmha(const void* q, const void* k, const void* v, AttnArgs args, cudaStream_t st) {
+  using Cfg = AttnCfg<D, NT, BKV>;
   CUtensorMap tq, tk, tv;
   constexpr int PC = Cfg::PANEL_COLS;
   if (!make_tmap_2d_bf16(&tq, q, (uint64_t)args.H * args.Tq, D, D, 128, PC, Cfg::SWIZZLE)) return VX_E_ARG;
-  if (!make_tmap_2d_bf16(&tk, k, (uint64_t)args.H * args.Tk, D, D, 128, PC, Cfg::SWIZZLE)) return VX_E_ARG;
-  if (!make_tmap_2d_bf16(&tv, v, (uint64_t)args.H * args.Tk, D, D, 128, PC, Cfg::SWIZZLE)) return VX_E_ARG;
-  auto kern = fmha_kernel<D, EMU>;
+  if (!make_tmap_2d_bf16(&tk, k, (uint64_t)args.H * args.Tk, D, D, BKV, PC, Cfg::SWIZZLE)) return VX_E_ARG;
+  if (!make_tmap_2d_bf16(&tv, v, (uint64_t)args.H * args.Tk, D, D, BKV, PC, Cfg::SWIZZLE)) return VX_E_ARG;
+  args.q_blocks = (args.Lq + Cfg::ROWS - 1) / Cfg::ROWS;
+  args.kv_tiles = (args.Lk + BKV - 1) / BKV;
+  args.units = args.H * args.nseq * args.q_blocks;
+  auto kern = fmha_kernel<D, EMU, NT, BKV>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
@@ -425,10 +439,7 @@ extern "C" int vx_attention(const void* q, const void* k, const void* v, void* o
   a.Lk = Lk;
   a.Tq = Tq;
   a.Tk = Tk;
-  const int rows_per_unit = D == 128 ? AttnCfg<128>::ROWS : 256;
-  a.q_blocks = (Lq + rows_per_unit - 1) / rows_per_unit;
-  a.kv_tiles = (Lk + 127) / 128;
-  a.units = H * nseq * a.q_blocks;
+  // q_blocks / kv_tiles / units depend on the kernel configuration: set in launch_fmha
   a.scale_log2 = (1.0f / sqrtf(float(D))) * 1.4426950408889634f;
   a.out = reinterpret_cast<__nv_bfloat16*>(out);
   a.ldo = ldo;
@@ -438,13 +449,18 @@ extern "C" int vx_attention(const void* q, const void* k, const void* v, void* o
     const char* e = getenv("VX_FMHA_EMU");  // diagnostic: exp pairs (of 8) on the FMA pipe
     return e ? atoi(e) : 2;
   }();
-  if (D == 64) {
+  static int cfg2 = [] {
+    const char* e = getenv("VX_FMHA_2X128");  // diagnostic: 2 Q tiles x 128-wide KV tiles
+    return e ? atoi(e) : 0;
+  }();
+  if (D == 64 && cfg2) return launch_fmha<64, 2, 2, 128>(q, k, v, a, st);
+  if (D == 64) {  // default: 3 Q tiles x 64-wide KV tiles (3 softmax warps per SM sub-partition)
     switch (emu) {
-      case 0: return launch_fmha<64, 0>(q, k, v, a, st);
-      case 1: return launch_fmha<64, 1>(q, k, v, a, st);
-      case 3: return launch_fmha<64, 3>(q, k, v, a, st);
-      case 4: return launch_fmha<64, 4>(q, k, v, a, st);
-      default: return launch_fmha<64, 2>(q, k, v, a, st);
+      case 0: return launch_fmha<64, 0, 3, 64>(q, k, v, a, st);
+      case 1: return launch_fmha<64, 1, 3, 64>(q, k, v, a, st);
+      case 3: return launch_fmha<64, 3, 3, 64>(q, k, v, a, st);
+      case 4: return launch_fmha<64, 4, 3, 64>(q, k, v, a, st);
+      default: return launch_fmha<64, 2, 3, 64>(q, k, v, a, st);
     }
   }
   if (D == 128) return launch_fmha<128, 2>(q, k, v, a, st);
