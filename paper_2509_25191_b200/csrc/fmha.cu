@@ -47,8 +47,11 @@ struct AttnArgs {
   float* lse;
 };
 
-template <int D, int NT_ = (D == 128 ? 1 : 2), int BKV_ = 128>
+template <int D, int NT_ = (D == 128 ? 1 : 2), int BKV_ = 128, bool ALIAS_ = false>
 struct AttnCfg {
+  // ALIAS: P is written over the first BKV/2 columns of S (4 tiles fit TMEM); S_i(j+1) is then
+  // issued after PV_i(j) instead of running ahead
+  static constexpr bool ALIAS = ALIAS_;
   static constexpr int NT = NT_;                           // 128-row Q tiles per CTA (TMEM budget)
   static constexpr int BKV = BKV_;                         // KV rows per tile (score columns)
   static constexpr int KST = D == 128 ? 2 : (BKV == 64 ? 4 : 3);
@@ -67,10 +70,10 @@ struct AttnCfg {
   static constexpr uint32_t BAR_BYTES = 512;
   static constexpr uint32_t SMEM = NT * Q_TILE_BYTES + 2 * KST * KV_TILE_BYTES + 1024 + BAR_BYTES;
   // TMEM columns: S_i [BKV fp32] ... | P_i [BKV/2] ... | O_i [D fp32] ...
-  static constexpr uint32_t O_BASE = ((NT * BKV + NT * BKV / 2) + 63) / 64 * 64;
+  static constexpr uint32_t O_BASE = ((NT * BKV + (ALIAS ? 0 : NT * BKV / 2)) + 63) / 64 * 64;
   static_assert(O_BASE + NT * D <= 512, "TMEM budget");
   static __host__ __device__ constexpr uint32_t tS(int i) { return i * BKV; }
-  static __host__ __device__ constexpr uint32_t tP(int i) { return NT * BKV + i * (BKV / 2); }
+  static __host__ __device__ constexpr uint32_t tP(int i) { return ALIAS ? i * BKV : NT * BKV + i * (BKV / 2); }
   static __host__ __device__ constexpr uint32_t tO(int i) { return O_BASE + i * D; }
 };
 
@@ -83,11 +86,12 @@ constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
 
 
 // EMU_PAIRS_OF_8: of every 8 exp pairs, this many use the FMA-pipe polynomial
-template <int D, int EMU_PAIRS_OF_8, int NT_, int BKV_>
-__global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_>::THREADS, 1)
+template <int D, int EMU_PAIRS_OF_8, int NT_, int BKV_, bool ALIAS_>
+__global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_>::THREADS, 1)
     fmha_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                 const __grid_constant__ CUtensorMap tmV, const AttnArgs a) {
-  using Cfg = AttnCfg<D, NT_, BKV_>;
+  using Cfg = AttnCfg<D, NT_, BKV_, ALIAS_>;
+  constexpr bool ALIAS = ALIAS_;
   constexpr int BKV = Cfg::BKV;
   constexpr int KST = Cfg::KST;
   extern __shared__ uint8_t smem_raw[];
@@ -209,52 +213,99 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_>::THREADS, 1)
       uint32_t c = 0;  // global K/V tile counter
       uint32_t n = 0;  // local unit counter
       uint32_t sfree_ph = 0, pfull_ph = 0;
-      for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++n) {
-        mbar_wait(q_full, n & 1);
-        tc_fence_after();
-        {  // S(0) of both tiles; the S buffers were released by the previous unit's last s_free
-          const uint32_t st = c % KST, ph = (c / KST) & 1;
-          mbar_wait(&k_full[st], ph);
+      if constexpr (ALIAS) {
+        for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++n) {
+          mbar_wait(q_full, n & 1);
           tc_fence_after();
-          const uint32_t ks = smem_u32(sK + st * Cfg::KV_TILE_BYTES);
-          for (int i = 0; i < NT; ++i) {
-            if (n > 0) mbar_wait(&s_free[i], sfree_ph);
+          {  // S(0): the previous unit's P / S columns were consumed by its last PVs (in order)
+            const uint32_t st = c % KST, ph = (c / KST) & 1;
+            mbar_wait(&k_full[st], ph);
             tc_fence_after();
-            issue_qk(i, ks);
-            mma_commit(&s_full[i]);
-          }
-          if (n > 0) sfree_ph ^= 1;
-          mma_commit(&k_empty[st]);
-          if (nkv == 1) mma_commit(q_empty);
-        }
-        for (int j = 0; j < nkv; ++j, ++c) {
-          const uint32_t st = c % KST, ph = (c / KST) & 1;
-          if (j + 1 < nkv) {  // run one KV tile ahead: S(j+1) as soon as S(j) has been loaded
-            const uint32_t nst = (c + 1) % KST, nph = ((c + 1) / KST) & 1;
-            mbar_wait(&k_full[nst], nph);
-            const uint32_t nks = smem_u32(sK + nst * Cfg::KV_TILE_BYTES);
+            const uint32_t ks = smem_u32(sK + st * Cfg::KV_TILE_BYTES);
             for (int i = 0; i < NT; ++i) {
-              mbar_wait(&s_free[i], sfree_ph);
-              tc_fence_after();
-              issue_qk(i, nks);
+              issue_qk(i, ks);
               mma_commit(&s_full[i]);
             }
-            sfree_ph ^= 1;
-            mma_commit(&k_empty[nst]);
-            if (j + 2 == nkv) mma_commit(q_empty);
+            mma_commit(&k_empty[st]);
+            if (nkv == 1) mma_commit(q_empty);
           }
-          const uint32_t vs = smem_u32(sV + st * Cfg::KV_TILE_BYTES);
-          mbar_wait(&v_full[st], ph);
-          if (j == 0)  // the previous unit's epilogue must have read O
-            for (int i = 0; i < NT; ++i) mbar_wait(&o_empty[i], (n & 1) ^ 1);
-          for (int i = 0; i < NT; ++i) {
-            mbar_wait(&p_full[i], pfull_ph);
+          for (int j = 0; j < nkv; ++j, ++c) {
+            const uint32_t st = c % KST, ph = (c / KST) & 1;
+            const bool has_next = j + 1 < nkv;
+            const uint32_t nst = (c + 1) % KST, nph = ((c + 1) / KST) & 1;
+            const uint32_t vs = smem_u32(sV + st * Cfg::KV_TILE_BYTES);
+            const uint32_t nks = smem_u32(sK + nst * Cfg::KV_TILE_BYTES);
+            mbar_wait(&v_full[st], ph);
+            if (has_next) mbar_wait(&k_full[nst], nph);
+            if (j == 0)
+              for (int i = 0; i < NT; ++i) mbar_wait(&o_empty[i], (n & 1) ^ 1);
+            for (int i = 0; i < NT; ++i) {
+              mbar_wait(&p_full[i], pfull_ph);
+              tc_fence_after();
+              issue_pv(i, vs, j > 0);
+              if (has_next) {  // overwrites P_i(j): executes after PV_i(j) (tcgen05 issue order)
+                issue_qk(i, nks);
+                mma_commit(&s_full[i]);
+              } else {
+                mma_commit(&p_free[i]);  // last PV of the unit
+              }
+            }
+            pfull_ph ^= 1;
+            mma_commit(&v_empty[st]);
+            if (has_next) {
+              mma_commit(&k_empty[nst]);
+              if (j + 2 == nkv) mma_commit(q_empty);
+            }
+          }
+        }
+      } else {
+        for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++n) {
+          mbar_wait(q_full, n & 1);
+          tc_fence_after();
+          {  // S(0) of both tiles; the S buffers were released by the previous unit's last s_free
+            const uint32_t st = c % KST, ph = (c / KST) & 1;
+            mbar_wait(&k_full[st], ph);
             tc_fence_after();
-            issue_pv(i, vs, j > 0);
-            mma_commit(&p_free[i]);
+            const uint32_t ks = smem_u32(sK + st * Cfg::KV_TILE_BYTES);
+            for (int i = 0; i < NT; ++i) {
+              if (n > 0) mbar_wait(&s_free[i], sfree_ph);
+              tc_fence_after();
+              issue_qk(i, ks);
+              mma_commit(&s_full[i]);
+            }
+            if (n > 0) sfree_ph ^= 1;
+            mma_commit(&k_empty[st]);
+            if (nkv == 1) mma_commit(q_empty);
           }
-          pfull_ph ^= 1;
-          mma_commit(&v_empty[st]);
+          for (int j = 0; j < nkv; ++j, ++c) {
+            const uint32_t st = c % KST, ph = (c / KST) & 1;
+            if (j + 1 < nkv) {  // run one KV tile ahead: S(j+1) as soon as S(j) has been loaded
+              const uint32_t nst = (c + 1) % KST, nph = ((c + 1) / KST) & 1;
+              mbar_wait(&k_full[nst], nph);
+              const uint32_t nks = smem_u32(sK + nst * Cfg::KV_TILE_BYTES);
+              for (int i = 0; i < NT; ++i) {
+                mbar_wait(&s_free[i], sfree_ph);
+                tc_fence_after();
+                issue_qk(i, nks);
+                mma_commit(&s_full[i]);
+              }
+              sfree_ph ^= 1;
+              mma_commit(&k_empty[nst]);
+              if (j + 2 == nkv) mma_commit(q_empty);
+            }
+            const uint32_t vs = smem_u32(sV + st * Cfg::KV_TILE_BYTES);
+            mbar_wait(&v_full[st], ph);
+            if (j == 0)  // the previous unit's epilogue must have read O
+              for (int i = 0; i < NT; ++i) mbar_wait(&o_empty[i], (n & 1) ^ 1);
+            for (int i = 0; i < NT; ++i) {
+              mbar_wait(&p_full[i], pfull_ph);
+              tc_fence_after();
+              issue_pv(i, vs, j > 0);
+              mma_commit(&p_free[i]);
+            }
+            pfull_ph ^= 1;
+            mma_commit(&v_empty[st]);
+          }
         }
       }
     }
@@ -286,9 +337,11 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_>::THREADS, 1)
 #pragma unroll
         for (int c = 0; c < BKV / 32; ++c) tmem_ld32(S_addr + 32 * c, sr + 32 * c);
         tmem_wait_ld();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&s_free[tile]);
+        if constexpr (!ALIAS) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&s_free[tile]);
+        }
         const int valid = a.Lk - BKV * j;
         auto step = [&](auto mask_tag) {
           if constexpr (decltype(mask_tag)::value) {
@@ -331,7 +384,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_>::THREADS, 1)
               acc[c & 3] = f2_add(acc[c & 3], f2_pack(p0, p1));
               pk[c] = pack_bf16(p0, p1);
             }
-            if (hf == 0 && j > 0) {  // P_i(j-1) consumed and O stable (waited after the first exps)
+            if (!ALIAS && hf == 0 && j > 0) {  // P_i(j-1) consumed and O stable (waited after the first exps)
               mbar_wait(&p_free[tile], pv_cnt & 1);
               ++pv_cnt;
               tc_fence_after();
@@ -396,9 +449,9 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_>::THREADS, 1)
   }
 }
 
-template <int D, int EMU, int NT = (D == 128 ? 1 : 2), int BKV = 128>
+template <int D, int EMU, int NT = (D == 128 ? 1 : 2), int BKV = 128, bool ALIAS = false>
 static int launch_fmha(const void* q, const void* k, const void* v, AttnArgs args, cudaStream_t st) {
-  using Cfg = AttnCfg<D, NT, BKV>;
+  using Cfg = AttnCfg<D, NT, BKV, ALIAS>;
   CUtensorMap tq, tk, tv;
   constexpr int PC = Cfg::PANEL_COLS;
   if (!make_tmap_2d_bf16(&tq, q, (uint64_t)args.H * args.Tq, D, D, 128, PC, Cfg::SWIZZLE)) return VX_E_ARG;
@@ -407,7 +460,7 @@ static int launch_fmha(const void* q, const void* k, const void* v, AttnArgs arg
   args.q_blocks = (args.Lq + Cfg::ROWS - 1) / Cfg::ROWS;
   args.kv_tiles = (args.Lk + BKV - 1) / BKV;
   args.units = args.H * args.nseq * args.q_blocks;
-  auto kern = fmha_kernel<D, EMU, NT, BKV>;
+  auto kern = fmha_kernel<D, EMU, NT, BKV, ALIAS>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
@@ -449,17 +502,24 @@ extern "C" int vx_attention(const void* q, const void* k, const void* v, void* o
     const char* e = getenv("VX_FMHA_EMU");  // diagnostic: exp pairs (of 8) on the FMA pipe
     return e ? atoi(e) : 2;
   }();
-  static int cfg2 = [] {
-    const char* e = getenv("VX_FMHA_2X128");  // diagnostic: 2 Q tiles x 128-wide KV tiles
+  static int cfg = [] {
+    const char* e = getenv("VX_FMHA_CFG");  // diagnostic: 0 auto, 1 = 2x128, 3 = 3x64, 4 = 4x64-alias
     return e ? atoi(e) : 0;
   }();
-  if (D == 64 && cfg2) return launch_fmha<64, 2, 2, 128>(q, k, v, a, st);
-  if (D == 64) {  // default: 3 Q tiles x 64-wide KV tiles (3 softmax warps per SM sub-partition)
+  if (D == 64) {
+    // long KV sequences (global layers): 4 Q tiles x 64-wide KV tiles, P aliased onto S
+    // (4 softmax warps per sub-partition); short ones (frame layers, 11-22 KV tiles): 3 Q tiles
+    // with separate P columns so S(j+1) runs ahead of the softmax.
+    const int c = cfg ? cfg : (Lk >= 4096 ? 4 : 3);
+    if (c == 1) return launch_fmha<64, 2, 2, 128>(q, k, v, a, st);
+    if (c == 4) {
+      if (emu == 3) return launch_fmha<64, 3, 4, 64, true>(q, k, v, a, st);
+      return launch_fmha<64, 2, 4, 64, true>(q, k, v, a, st);
+    }
     switch (emu) {
       case 0: return launch_fmha<64, 0, 3, 64>(q, k, v, a, st);
       case 1: return launch_fmha<64, 1, 3, 64>(q, k, v, a, st);
       case 3: return launch_fmha<64, 3, 3, 64>(q, k, v, a, st);
-      case 4: return launch_fmha<64, 4, 3, 64>(q, k, v, a, st);
       default: return launch_fmha<64, 2, 3, 64>(q, k, v, a, st);
     }
   }

@@ -146,7 +146,8 @@ def _sdpa_ref(q, k, v, nseq, Lq, Lk):
 
 @pytest.mark.parametrize("D,H,nseq,L", [(64, 16, 3, 1374), (64, 2, 1, 5000), (64, 4, 5, 69), (32, 4, 8, 69),
                                         (32, 4, 1, 552), (64, 1, 2, 128), (64, 3, 1, 300), (64, 2, 1, 17),
-                                        (128, 16, 1, 200), (128, 4, 1, 1000), (128, 2, 3, 77), (128, 16, 1, 8)])
+                                        (128, 16, 1, 200), (128, 4, 1, 1000), (128, 2, 3, 77), (128, 16, 1, 8),
+                                        (64, 2, 2, 4099), (64, 1, 1, 8192)])
 def test_attention_matches_sdpa(ops, D, H, nseq, L):
     T = nseq * L
     q = _bf(H, T, D, seed=20)
@@ -160,9 +161,10 @@ def test_attention_matches_sdpa(ops, D, H, nseq, L):
     assert (lse - lse_ref).abs().max().item() < 1e-2
 
 
-def test_attention_large_logits_rescale(ops):
-    # peaked scores force the lazy O-rescaling path
-    H, L, D = 2, 2000, 64
+@pytest.mark.parametrize("L", [2000, 4500])
+def test_attention_large_logits_rescale(ops, L):
+    # peaked scores force the lazy O-rescaling path (both the short- and long-KV kernel variants)
+    H, D = 2, 64
     q = _bf(H, L, D, scale=4.0, seed=30)
     k = _bf(H, L, D, scale=4.0, seed=31)
     v = _bf(H, L, D, seed=32)
@@ -172,9 +174,10 @@ def test_attention_large_logits_rescale(ops):
     assert rel(out, ref) < 1e-2
 
 
-def test_attention_cross_lengths(ops):
+@pytest.mark.parametrize("Lq,Lk", [(700, 1900), (333, 6000), (4200, 257)])
+def test_attention_cross_lengths(ops, Lq, Lk):
     # ring-step shape: local queries against a remote K/V shard of another length
-    H, Lq, Lk, D = 4, 700, 1900, 64
+    H, D = 4, 64
     q = _bf(H, Lq, D, seed=40)
     k = _bf(H, Lk, D, seed=41)
     v = _bf(H, Lk, D, seed=42)
