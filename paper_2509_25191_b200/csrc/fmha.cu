@@ -513,8 +513,12 @@ extern "C" int vx_attention(const void* q, const void* k, const void* v, void* o
     const int c = cfg ? cfg : (Lk >= 4096 ? 4 : 3);
     if (c == 1) return launch_fmha<64, 2, 2, 128>(q, k, v, a, st);
     if (c == 4) {
-      if (emu == 3) return launch_fmha<64, 3, 4, 64, true>(q, k, v, a, st);
-      return launch_fmha<64, 2, 4, 64, true>(q, k, v, a, st);
+      switch (emu) {
+        case 0: return launch_fmha<64, 0, 4, 64, true>(q, k, v, a, st);
+        case 1: return launch_fmha<64, 1, 4, 64, true>(q, k, v, a, st);
+        case 3: return launch_fmha<64, 3, 4, 64, true>(q, k, v, a, st);
+        default: return launch_fmha<64, 2, 4, 64, true>(q, k, v, a, st);
+      }
     }
     switch (emu) {
       case 0: return launch_fmha<64, 0, 3, 64>(q, k, v, a, st);
