@@ -165,6 +165,60 @@ int vx_epipolar_accumulate(const double* F, const int64_t* offsets, const double
                            const double* w, int num_pairs, int mode, double* out, int32_t* n_skipped,
                            void* stream);
 
+/* Global-Alignment optimiser on the device ("plus the on-device chain rule and
+ * Adam over 300 iterations").  Replaces the per-pair host loops of pkg/src/epialign/aligner.py:
+ * _Problem._decode (:160-174), _pair_F (:176-185), residuals (:189-207), loss_and_gradient
+ * (:209-278) and the adaptive-moment loop of align (:408-417).  All fp64, row-major 3x3 matrices.
+ * Every pointer is device memory owned by the caller. */
+typedef struct vx_ga_problem {
+  int n_frames, n_pairs;
+  int dim;          /* 9, or 10 with the log-focal parameter (optimize_focal) */
+  int mode;         /* 0 algebraic, 1 geometric */
+  int gauge;        /* gauge frame: its parameters never move */
+  const int32_t* pair_ij;     /* [P, 2] frame indices (i, j) */
+  const int64_t* offsets;     /* [P+1] correspondence prefix sums */
+  const double* xy_i;         /* [K, 2] */
+  const double* xy_j;         /* [K, 2] */
+  const double* w;            /* [K] weights (residual calls ignore it) */
+  const int32_t* frame_ptr;   /* [n+1] CSR over (pair, role) entries touching each frame */
+  const int32_t* frame_ent;   /* [2P] entry = 2*pair + (frame is j), ascending pair order */
+  const double* base_R;       /* [n, 9] canonical-gauge rotations */
+  const double* base_t;       /* [n, 3] canonical-gauge translations */
+  const double* base_Kinv;    /* [n, 9] inverse intrinsics */
+  double* params;             /* [n, dim] pose residual blocks (6D rotation, translation, log focal) */
+  double* adam_m;             /* [n, dim] first moments */
+  double* adam_v;             /* [n, dim] second moments */
+  double* Rs;                 /* [n, 9] decoded rotations (scratch, kept current by the calls) */
+  double* ts;                 /* [n, 3] */
+  double* Kinv;               /* [n, 9] */
+  double* geom;               /* [P, 32] per-pair geometry: R_ij, t_ij, E, F/|F|, |F|, valid (scratch) */
+  double* payload;            /* [P, 32] per-pair gradient contributions (scratch) */
+  double* scalars;            /* [4 + 3*ceil(P/64)]: num, den, skipped (this evaluation), spare; then
+                                 per-block partial sums (scratch) */
+  int32_t* status;            /* [2]: [0] bit 0 degenerate 6D rotation, bit 1 zero total weight;
+                                 [1] block counter, must be 0 on entry (left 0 on exit) */
+} vx_ga_problem;
+
+/* Rs/ts/Kinv <- decode(params). */
+int vx_ga_decode(const vx_ga_problem* pb, void* stream);
+/* Residuals at the decoded cameras: e [K] (NaN for degenerate lines and for every correspondence of
+ * a pair whose fundamental matrix vanishes), deg_pair [P] (1 = pair degenerate), n_deg [P]. */
+int vx_ga_residuals(const vx_ga_problem* pb, double* e, int32_t* deg_pair, int32_t* n_deg, void* stream);
+/* One loss/gradient evaluation at the decoded cameras: grad [n, dim] (gauge block exactly 0),
+ * scalars = (num, den, skipped). */
+int vx_ga_loss_grad(const vx_ga_problem* pb, double* grad, void* stream);
+/* `iters` full-batch adaptive-moment steps t = t0+1 .. t0+iters (1-based, as aligner.py:408):
+ * loss trace -> trace[t-1]; bias corrections bc1[t-1] = 1 - beta1^t, bc2[t-1] = 1 - beta2^t;
+ * skipped correspondences accumulated into *skipped_total.  Launched as one CUDA graph when
+ * use_graph != 0.  Leaves params, moments and the decoded cameras current. */
+int vx_ga_adam(const vx_ga_problem* pb, int t0, int iters, double lr, const double* bc1, const double* bc2,
+               double* trace, double* skipped_total, int use_graph, void* stream);
+/* Adaptive weights (pkg/src/epialign/weighting.py:56-109): histogram of the finite residuals clipped
+ * to [edges[0], edges[n_bins]], density floor 1e-6, w = (f(e)/mean f)^alpha (0 for NaN residuals).
+ * scratch: [n_bins] int64 counts; out_stats [2 + n_bins] = (avg density, finite count, densities). */
+int vx_ga_adaptive_weights(const double* e, int64_t K, const double* edges, int n_bins, double alpha, double* w,
+                           int64_t* counts, double* out_stats, void* stream);
+
 int vx_num_sms(void);
 const char* vx_last_error(void);
 const char* vx_version(void);

@@ -37,7 +37,7 @@ def up_to_date() -> bool:
 
 # per-file flags: the fp64 GA kernels follow the reference's un-fused double arithmetic
 # (pkg/src/epialign/_kernels_cy.pyx is compiled without FMA contraction on x86-64)
-EXTRA = {"epipolar.cu": ["-fmad=false"]}
+EXTRA = {"epipolar.cu": ["-fmad=false"], "ga.cu": ["-fmad=false"]}
 
 
 def _compile_one(src: Path, obj: Path, log):
@@ -57,8 +57,16 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     logpath = objdir / "nvcc.log"
     with open(logpath, "w") as log:
         objs = [objdir / (s.stem + ".o") for s in sources()]
+        newest_header = max((p.stat().st_mtime for p in headers()), default=0.0)
+        build_py = Path(__file__).stat().st_mtime
+
+        def stale(src, obj):  # per-object rebuild: source, any header or this recipe newer than the object
+            return force or not obj.exists() or obj.stat().st_mtime < max(src.stat().st_mtime, newest_header,
+                                                                          build_py)
+
+        todo = [(s, o) for s, o in zip(sources(), objs) if stale(s, o)]
         with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
-            list(ex.map(lambda so: _compile_one(so[0], so[1], log), zip(sources(), objs)))
+            list(ex.map(lambda so: _compile_one(so[0], so[1], log), todo))
         tmp = LIB.with_suffix(".so.tmp")
         cmd = [NVCC, *ARCH, "-shared", "-o", str(tmp), *map(str, objs)]
         r = subprocess.run(cmd, capture_output=True, text=True)

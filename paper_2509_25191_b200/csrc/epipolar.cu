@@ -6,50 +6,21 @@
 // launch covers every pair: one CTA per pair, threads strided over its correspondences,
 // fp64 arithmetic with the reference's formulas and thresholds (LINE_NORMAL_EPS = 1e-12,
 // GRAD_DEADZONE = 1e-9), deterministic fixed-order block reductions.
-#include <math.h>
-
 #include "../../include/vx_api.h"
-#include "common.cuh"
+#include "epipolar.cuh"
 #include "host_util.h"
 
 namespace vx {
-
-constexpr double LINE_EPS = 1e-12;
-constexpr double DEADZONE = 1e-9;
-constexpr int EPI_THREADS = 128;
-
-VX_DEVICE double warp_sum(double v) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffff, v, o);
-  return v;
-}
 
 __global__ void __launch_bounds__(EPI_THREADS) epipolar_residuals_kernel(
     const double* __restrict__ F, const int64_t* __restrict__ off, const double* __restrict__ xi,
     const double* __restrict__ xj, int mode, double* __restrict__ e, int32_t* __restrict__ n_deg) {
   const int p = blockIdx.x;
-  const double* f = F + 9 * p;
-  const double f00 = f[0], f01 = f[1], f02 = f[2], f10 = f[3], f11 = f[4], f12 = f[5], f20 = f[6], f21 = f[7],
-               f22 = f[8];
+  double f[9];
+#pragma unroll
+  for (int q = 0; q < 9; ++q) f[q] = F[9 * p + q];
   int deg = 0;
-  for (int64_t m = off[p] + threadIdx.x; m < off[p + 1]; m += EPI_THREADS) {
-    const double u = xi[2 * m], v = xi[2 * m + 1];
-    const double l0 = f00 * u + f01 * v + f02;
-    const double l1 = f10 * u + f11 * v + f12;
-    const double l2 = f20 * u + f21 * v + f22;
-    const double s = xj[2 * m] * l0 + xj[2 * m + 1] * l1 + l2;
-    if (mode == 0) {
-      e[m] = fabs(s);
-    } else {
-      const double n = sqrt(l0 * l0 + l1 * l1);
-      if (n < LINE_EPS) {
-        e[m] = NAN;
-        ++deg;
-      } else {
-        e[m] = fabs(s) / n;
-      }
-    }
-  }
+  for (int64_t m = off[p] + threadIdx.x; m < off[p + 1]; m += EPI_THREADS) e[m] = epi_residual(f, xi, xj, m, mode, deg);
   __shared__ int sdeg[EPI_THREADS / 32];
 #pragma unroll
   for (int o = 16; o; o >>= 1) deg += __shfl_xor_sync(0xffffffff, deg, o);
@@ -68,74 +39,18 @@ __global__ void __launch_bounds__(EPI_THREADS) epipolar_accumulate_kernel(
     const double* __restrict__ xj, const double* __restrict__ w, int mode, double* __restrict__ out,
     int32_t* __restrict__ n_skipped) {
   const int p = blockIdx.x;
-  const double* f = F + 9 * p;
-  const double f00 = f[0], f01 = f[1], f02 = f[2], f10 = f[3], f11 = f[4], f12 = f[5], f20 = f[6], f21 = f[7],
-               f22 = f[8];
+  double f[9];
+#pragma unroll
+  for (int q = 0; q < 9; ++q) f[q] = F[9 * p + q];
   double acc[11];
 #pragma unroll
   for (int q = 0; q < 11; ++q) acc[q] = 0.0;
   int skipped = 0;
-  for (int64_t m = off[p] + threadIdx.x; m < off[p + 1]; m += EPI_THREADS) {
-    const double u = xi[2 * m], v = xi[2 * m + 1];
-    const double up = xj[2 * m], vp = xj[2 * m + 1];
-    const double l0 = f00 * u + f01 * v + f02;
-    const double l1 = f10 * u + f11 * v + f12;
-    const double l2 = f20 * u + f21 * v + f22;
-    const double s = up * l0 + vp * l1 + l2;
-    double n, err;
-    if (mode == 0) {
-      n = 1.0;
-      err = fabs(s);
-    } else {
-      n = sqrt(l0 * l0 + l1 * l1);
-      if (n < LINE_EPS) {
-        ++skipped;
-        continue;
-      }
-      err = fabs(s) / n;
-    }
-    const double wk = w[m];
-    acc[0] += wk * err;
-    acc[1] += wk;
-    if (err < DEADZONE) continue;
-    const double sgn = s > 0 ? 1.0 : (s < 0 ? -1.0 : 0.0);
-    const double c1 = wk * sgn / n;
-    acc[2] += c1 * up * u;
-    acc[3] += c1 * up * v;
-    acc[4] += c1 * up;
-    acc[5] += c1 * vp * u;
-    acc[6] += c1 * vp * v;
-    acc[7] += c1 * vp;
-    acc[8] += c1 * u;
-    acc[9] += c1 * v;
-    acc[10] += c1;
-    if (mode == 1) {
-      const double c2 = wk * fabs(s) / (n * n * n);
-      acc[2] -= c2 * l0 * u;
-      acc[3] -= c2 * l0 * v;
-      acc[4] -= c2 * l0;
-      acc[5] -= c2 * l1 * u;
-      acc[6] -= c2 * l1 * v;
-      acc[7] -= c2 * l1;
-    }
-  }
-  __shared__ double sacc[EPI_THREADS / 32][12];
-#pragma unroll
-  for (int q = 0; q < 11; ++q) acc[q] = warp_sum(acc[q]);
-#pragma unroll
-  for (int o = 16; o; o >>= 1) skipped += __shfl_xor_sync(0xffffffff, skipped, o);
-  if ((threadIdx.x & 31) == 0) {
-#pragma unroll
-    for (int q = 0; q < 11; ++q) sacc[threadIdx.x >> 5][q] = acc[q];
-    sacc[threadIdx.x >> 5][11] = double(skipped);
-  }
-  __syncthreads();
-  if (threadIdx.x < 12) {
-    double t = 0.0;
-    for (int wq = 0; wq < EPI_THREADS / 32; ++wq) t += sacc[wq][threadIdx.x];
-    if (threadIdx.x < 11) out[11 * (int64_t)p + threadIdx.x] = t;
-    else n_skipped[p] = int32_t(t);
-  }
+  epi_accumulate<EPI_THREADS>(f, xi, xj, w, off[p], off[p + 1], mode, acc, skipped);
+  __shared__ double red[EPI_THREADS / 32][12];
+  epi_block_reduce<EPI_THREADS>(acc, skipped, red);
+  if (threadIdx.x < 11) out[11 * (int64_t)p + threadIdx.x] = red[0][threadIdx.x];
+  else if (threadIdx.x == 11) n_skipped[p] = int32_t(red[0][11]);
 }
 
 }  // namespace vx

@@ -46,9 +46,21 @@ class Spatial(ctypes.Structure):
     ]
 
 
+class GaProblem(ctypes.Structure):
+    """vx_ga_problem (include/vx_api.h)."""
+    _fields_ = [
+        ("n_frames", _i32), ("n_pairs", _i32), ("dim", _i32), ("mode", _i32), ("gauge", _i32),
+        ("pair_ij", _vp), ("offsets", _vp), ("xy_i", _vp), ("xy_j", _vp), ("w", _vp),
+        ("frame_ptr", _vp), ("frame_ent", _vp), ("base_R", _vp), ("base_t", _vp), ("base_Kinv", _vp),
+        ("params", _vp), ("adam_m", _vp), ("adam_v", _vp), ("Rs", _vp), ("ts", _vp), ("Kinv", _vp),
+        ("geom", _vp), ("payload", _vp), ("scalars", _vp), ("status", _vp),
+    ]
+
+
 EXPORTED_SYMBOLS = ("vx_gemm", "vx_attention", "vx_layernorm", "vx_patchify", "vx_special_tokens",
                     "vx_upsample_bilinear", "vx_gemm_spatial", "vx_epipolar_residuals",
-                    "vx_epipolar_accumulate", "vx_num_sms", "vx_last_error", "vx_version")
+                    "vx_epipolar_accumulate", "vx_ga_decode", "vx_ga_residuals", "vx_ga_loss_grad",
+                    "vx_ga_adam", "vx_ga_adaptive_weights", "vx_num_sms", "vx_last_error", "vx_version")
 
 _lib = None
 
@@ -72,11 +84,18 @@ def load_library(path: os.PathLike | None = None) -> ctypes.CDLL:
     lib.vx_gemm_spatial.argtypes = [_vp, _vp, _i32, _i32, _vp, ctypes.POINTER(Spatial), _vp]
     lib.vx_epipolar_residuals.argtypes = [_vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp]
     lib.vx_epipolar_accumulate.argtypes = [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp]
+    _pb = ctypes.POINTER(GaProblem)
+    _f64 = ctypes.c_double
+    lib.vx_ga_decode.argtypes = [_pb, _vp]
+    lib.vx_ga_residuals.argtypes = [_pb, _vp, _vp, _vp, _vp]
+    lib.vx_ga_loss_grad.argtypes = [_pb, _vp, _vp]
+    lib.vx_ga_adam.argtypes = [_pb, _i32, _i32, _f64, _vp, _vp, _vp, _vp, _i32, _vp]
+    lib.vx_ga_adaptive_weights.argtypes = [_vp, _i64, _vp, _i32, _f64, _vp, _vp, _vp, _vp]
     lib.vx_last_error.restype = ctypes.c_char_p
     lib.vx_version.restype = ctypes.c_char_p
-    for name in ("vx_gemm", "vx_attention", "vx_layernorm", "vx_patchify", "vx_special_tokens",
-                 "vx_upsample_bilinear", "vx_gemm_spatial", "vx_epipolar_residuals",
-                 "vx_epipolar_accumulate", "vx_num_sms"):
+    for name in EXPORTED_SYMBOLS:
+        if name in ("vx_last_error", "vx_version"):
+            continue
         getattr(lib, name).restype = _i32
     if path is None:
         _lib = lib
@@ -320,3 +339,38 @@ def epipolar_accumulate(F, offsets, xy_i, xy_j, w, mode: int):
     _check(_lib.vx_epipolar_accumulate(_ptr(F), _ptr(offsets), _ptr(xy_i), _ptr(xy_j), _ptr(w), P, mode, _ptr(out),
                                        _ptr(sk), _stream()), "vx_epipolar_accumulate")
     return out, sk
+
+
+# ---------------------------------------------------------------------------
+# Global-Alignment optimiser (ga.cu); the problem struct is built by paper_2509_25191_b200.ga
+
+
+def ga_decode(pb: GaProblem):
+    load_library()
+    _check(_lib.vx_ga_decode(ctypes.byref(pb), _stream()), "vx_ga_decode")
+
+
+def ga_residuals(pb: GaProblem, e, deg_pair, n_deg):
+    load_library()
+    _check(_lib.vx_ga_residuals(ctypes.byref(pb), _ptr(e), _ptr(deg_pair), _ptr(n_deg), _stream()),
+           "vx_ga_residuals")
+
+
+def ga_loss_grad(pb: GaProblem, grad):
+    load_library()
+    _check(_lib.vx_ga_loss_grad(ctypes.byref(pb), _ptr(grad), _stream()), "vx_ga_loss_grad")
+
+
+def ga_adam(pb: GaProblem, t0: int, iters: int, lr: float, bc1, bc2, trace, skipped, use_graph: bool = True):
+    load_library()
+    _check(_lib.vx_ga_adam(ctypes.byref(pb), t0, iters, float(lr), _ptr(bc1), _ptr(bc2), _ptr(trace), _ptr(skipped),
+                           int(use_graph), _stream()), "vx_ga_adam")
+
+
+def ga_adaptive_weights(e, edges, alpha: float, w, counts, stats):
+    load_library()
+    for t, nm, dt in ((e, "e", torch.float64), (edges, "edges", torch.float64), (w, "w", torch.float64),
+                      (counts, "counts", torch.int64), (stats, "stats", torch.float64)):
+        _req(t, dt, nm)
+    _check(_lib.vx_ga_adaptive_weights(_ptr(e), e.numel(), _ptr(edges), edges.numel() - 1, float(alpha), _ptr(w),
+                                       _ptr(counts), _ptr(stats), _stream()), "vx_ga_adaptive_weights")
