@@ -219,6 +219,33 @@ int vx_ga_adam(const vx_ga_problem* pb, int t0, int iters, double lr, const doub
 int vx_ga_adaptive_weights(const double* e, int64_t K, const double* edges, int n_bins, double alpha, double* w,
                            int64_t* counts, double* out_stats, void* stream);
 
+/* Scene-level consumers of the predictions, csrc/scene.cu.
+ *
+ * vx_matched_points — pkg/src/epialign/pointcloud.py:91-130 select_matched_points with
+ *   sample_depth (:66-88) and geometry.py:341-348 unproject.  Depth maps: `depth` holds every map
+ *   (fp32 if depth_f32 else fp64) at element offsets map_offset[k], shape map_hw[2k] x map_hw[2k+1];
+ *   frame f uses map slot[f].  Cameras R [n,9], t [n,3], Kinv [n,9] (fp64, world-to-camera).
+ *   Per correspondence m: state[m] = 0 weight <= threshold, 1 emitted (points[m] = (p_i, p_j),
+ *   gap[m] = |p_i - p_j|), 2 skipped (a depth sample <= 0), 3 non-finite depth sample. */
+int vx_matched_points(const void* depth, int depth_f32, const int64_t* map_offset, const int32_t* map_hw,
+                      const int32_t* slot, const double* R, const double* t, const double* Kinv,
+                      const int32_t* pair_ij, const int64_t* offsets, int n_pairs, const double* xy_i,
+                      const double* xy_j, const double* w, double threshold, double* points, double* gap,
+                      int8_t* state, void* stream);
+/* Dense world-point maps of VGGT depth: out[s, y, x] = R_s^T (depth[s,y,x] K_s^-1 (x, y, 1) - t_s),
+ * fp32; extrinsic [S,3,4] world-to-camera, intrinsic [S,3,3]. */
+int vx_unproject_depth(const float* depth, int S, int H, int W, const float* extrinsic, const float* intrinsic,
+                       float* out, void* stream);
+/* pairing.py:88-109: view angle (degrees) between the optical axes (third rows of R [n,9]) of every
+ * pair i < j, in row-major upper-triangle order (n(n-1)/2 entries); flag = angle <= threshold. */
+int vx_select_pairs(const double* R, int n, double threshold_deg, int8_t* flag, double* angle, void* stream);
+/* metrics.py:89-118: RRE / RTE (degrees) of every pair i < j of the predicted rig against the ground
+ * truth (gt_of[i] = ground-truth index of predicted frame i), upper-triangle order; with
+ * order_invariant each pair writes (i, j) then (j, i).  zero_baseline = 1 where RTE was forced to 0. */
+int vx_pairwise_errors(const double* Rp, const double* tp, const double* Rg, const double* tg,
+                       const int32_t* gt_of, int n, int order_invariant, double* rre, double* rte,
+                       uint8_t* zero_baseline, void* stream);
+
 int vx_num_sms(void);
 const char* vx_last_error(void);
 const char* vx_version(void);

@@ -37,7 +37,7 @@ def up_to_date() -> bool:
 
 # per-file flags: the fp64 GA kernels follow the reference's un-fused double arithmetic
 # (pkg/src/epialign/_kernels_cy.pyx is compiled without FMA contraction on x86-64)
-EXTRA = {"epipolar.cu": ["-fmad=false"], "ga.cu": ["-fmad=false"]}
+EXTRA = {"epipolar.cu": ["-fmad=false"], "ga.cu": ["-fmad=false"], "scene.cu": ["-fmad=false"]}
 
 
 def _compile_one(src: Path, obj: Path, log):

@@ -60,7 +60,8 @@ class GaProblem(ctypes.Structure):
 EXPORTED_SYMBOLS = ("vx_gemm", "vx_attention", "vx_layernorm", "vx_patchify", "vx_special_tokens",
                     "vx_upsample_bilinear", "vx_gemm_spatial", "vx_epipolar_residuals",
                     "vx_epipolar_accumulate", "vx_ga_decode", "vx_ga_residuals", "vx_ga_loss_grad",
-                    "vx_ga_adam", "vx_ga_adaptive_weights", "vx_num_sms", "vx_last_error", "vx_version")
+                    "vx_ga_adam", "vx_ga_adaptive_weights", "vx_matched_points", "vx_unproject_depth",
+                    "vx_select_pairs", "vx_pairwise_errors", "vx_num_sms", "vx_last_error", "vx_version")
 
 _lib = None
 
@@ -91,6 +92,11 @@ def load_library(path: os.PathLike | None = None) -> ctypes.CDLL:
     lib.vx_ga_loss_grad.argtypes = [_pb, _vp, _vp]
     lib.vx_ga_adam.argtypes = [_pb, _i32, _i32, _f64, _vp, _vp, _vp, _vp, _i32, _vp]
     lib.vx_ga_adaptive_weights.argtypes = [_vp, _i64, _vp, _i32, _f64, _vp, _vp, _vp, _vp]
+    lib.vx_matched_points.argtypes = [_vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _f64,
+                                      _vp, _vp, _vp, _vp]
+    lib.vx_unproject_depth.argtypes = [_vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp]
+    lib.vx_select_pairs.argtypes = [_vp, _i32, _f64, _vp, _vp, _vp]
+    lib.vx_pairwise_errors.argtypes = [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp]
     lib.vx_last_error.restype = ctypes.c_char_p
     lib.vx_version.restype = ctypes.c_char_p
     for name in EXPORTED_SYMBOLS:
@@ -374,3 +380,64 @@ def ga_adaptive_weights(e, edges, alpha: float, w, counts, stats):
         _req(t, dt, nm)
     _check(_lib.vx_ga_adaptive_weights(_ptr(e), e.numel(), _ptr(edges), edges.numel() - 1, float(alpha), _ptr(w),
                                        _ptr(counts), _ptr(stats), _stream()), "vx_ga_adaptive_weights")
+
+
+# ---------------------------------------------------------------------------
+# scene-level consumers (scene.cu); paper_2509_25191_b200.scene builds the arguments
+
+
+def matched_points(depth, map_offset, map_hw, slot, R, t, Kinv, pair_ij, offsets, xy_i, xy_j, w, threshold: float):
+    """-> (points [K, 6], gap [K], state int8 [K]) per correspondence."""
+    load_library()
+    K = xy_i.shape[0]
+    dev = xy_i.device
+    points = torch.empty(K, 6, device=dev, dtype=torch.float64)
+    gap = torch.empty(K, device=dev, dtype=torch.float64)
+    state = torch.empty(K, device=dev, dtype=torch.int8)
+    if depth.dtype not in (torch.float32, torch.float64):
+        raise TypeError("depth maps must be float32 or float64")
+    _check(_lib.vx_matched_points(_ptr(depth), int(depth.dtype == torch.float32), _ptr(map_offset), _ptr(map_hw),
+                                  _ptr(slot), _ptr(R), _ptr(t), _ptr(Kinv), _ptr(pair_ij), _ptr(offsets),
+                                  pair_ij.shape[0], _ptr(xy_i), _ptr(xy_j), _ptr(w), float(threshold), _ptr(points),
+                                  _ptr(gap), _ptr(state), _stream()), "vx_matched_points")
+    return points, gap, state
+
+
+def unproject_depth(depth, extrinsic, intrinsic, out=None):
+    """depth fp32 [S, H, W], extrinsic [S, 3, 4], intrinsic [S, 3, 3] -> world points fp32 [S, H, W, 3]."""
+    load_library()
+    for x, nm in ((depth, "depth"), (extrinsic, "extrinsic"), (intrinsic, "intrinsic")):
+        _req(x, torch.float32, nm)
+        if not x.is_contiguous():
+            raise ValueError(f"{nm} must be contiguous")
+    S, H, W = depth.shape
+    if out is None:
+        out = torch.empty(S, H, W, 3, device=depth.device, dtype=torch.float32)
+    _check(_lib.vx_unproject_depth(_ptr(depth), S, H, W, _ptr(extrinsic), _ptr(intrinsic), _ptr(out), _stream()),
+           "vx_unproject_depth")
+    return out
+
+
+def select_pairs(R, threshold_deg: float):
+    """R fp64 [n, 9] -> (flag int8 [n(n-1)/2], angle fp64 [n(n-1)/2]) in upper-triangle order."""
+    load_library()
+    n = R.shape[0]
+    m = n * (n - 1) // 2
+    flag = torch.zeros(max(m, 1), device=R.device, dtype=torch.int8)
+    angle = torch.empty(max(m, 1), device=R.device, dtype=torch.float64)
+    _check(_lib.vx_select_pairs(_ptr(R), n, float(threshold_deg), _ptr(flag), _ptr(angle), _stream()),
+           "vx_select_pairs")
+    return flag[:m], angle[:m]
+
+
+def pairwise_errors(Rp, tp, Rg, tg, gt_of, order_invariant: bool):
+    load_library()
+    n = Rp.shape[0]
+    m = n * (n - 1) // 2 * (2 if order_invariant else 1)
+    dev = Rp.device
+    rre = torch.empty(max(m, 1), device=dev, dtype=torch.float64)
+    rte = torch.empty(max(m, 1), device=dev, dtype=torch.float64)
+    flag = torch.empty(max(m, 1), device=dev, dtype=torch.uint8)
+    _check(_lib.vx_pairwise_errors(_ptr(Rp), _ptr(tp), _ptr(Rg), _ptr(tg), _ptr(gt_of), n, int(order_invariant),
+                                   _ptr(rre), _ptr(rte), _ptr(flag), _stream()), "vx_pairwise_errors")
+    return rre[:m], rte[:m], flag[:m]
