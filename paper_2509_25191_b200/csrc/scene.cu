@@ -99,12 +99,13 @@ __global__ void __launch_bounds__(128) matched_points_kernel(
   }
 }
 
-// dense world points, 4 consecutive pixels of one row segment per thread (W % 4 == 0 path) or 1
+// dense world points: 4 consecutive pixels of the flattened H*W image per thread (16-byte depth load,
+// three 16-byte point stores when H*W % 4 == 0, scalar tail otherwise)
 __global__ void unproject_depth_kernel(const float* __restrict__ depth, int S, int H, int W,
                                        const float* __restrict__ extri, const float* __restrict__ intri,
                                        float* __restrict__ out) {
   const int s = blockIdx.y;
-  const int64_t HW = (int64_t)H * W;
+  const int HW = H * W;
   const float* E = extri + 12 * s;
   const float* K = intri + 9 * s;
   const float fx = K[0], fy = K[4], cx = K[2], cy = K[5];
@@ -112,14 +113,14 @@ __global__ void unproject_depth_kernel(const float* __restrict__ depth, int S, i
   const float r00 = E[0], r01 = E[1], r02 = E[2], t0 = E[3];
   const float r10 = E[4], r11 = E[5], r12 = E[6], t1 = E[7];
   const float r20 = E[8], r21 = E[9], r22 = E[10], t2 = E[11];
-  const int64_t q0 = 4 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+  const int q0 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);
   if (q0 >= HW) return;
-  const float* dp = depth + s * HW;
-  float* op = out + 3 * (s * HW);
+  const float* dp = depth + (int64_t)s * HW;
+  float* op = out + 3 * ((int64_t)s * HW);
+  const bool vec = (HW % 4 == 0);
   float z[4];
-  const bool vec = (W % 4 == 0) && (q0 + 3 < HW);
   if (vec) {
-    const float4 d4 = *reinterpret_cast<const float4*>(dp + q0);
+    const float4 d4 = __ldcs(reinterpret_cast<const float4*>(dp + q0));
     z[0] = d4.x;
     z[1] = d4.y;
     z[2] = d4.z;
@@ -128,27 +129,30 @@ __global__ void unproject_depth_kernel(const float* __restrict__ depth, int S, i
 #pragma unroll
     for (int k = 0; k < 4; ++k) z[k] = q0 + k < HW ? dp[q0 + k] : 0.0f;
   }
+  int v = q0 / W, u = q0 - v * W;
   float res[12];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    const int64_t q = q0 + k;
-    const float u = float(q % W), v = float(q / W);
-    const float x0 = z[k] * ((u - cx) * ifx) - t0;
-    const float x1 = z[k] * ((v - cy) * ify) - t1;
+    const float x0 = z[k] * ((float(u) - cx) * ifx) - t0;
+    const float x1 = z[k] * ((float(v) - cy) * ify) - t1;
     const float x2 = z[k] - t2;
     res[3 * k + 0] = r00 * x0 + r10 * x1 + r20 * x2;
     res[3 * k + 1] = r01 * x0 + r11 * x1 + r21 * x2;
     res[3 * k + 2] = r02 * x0 + r12 * x1 + r22 * x2;
+    if (++u == W) {
+      u = 0;
+      ++v;
+    }
   }
   if (vec) {
-    float4* o4 = reinterpret_cast<float4*>(op + 3 * q0);
-    o4[0] = make_float4(res[0], res[1], res[2], res[3]);
-    o4[1] = make_float4(res[4], res[5], res[6], res[7]);
-    o4[2] = make_float4(res[8], res[9], res[10], res[11]);
+    float4* o4 = reinterpret_cast<float4*>(op + 3 * (int64_t)q0);
+    __stcs(o4 + 0, make_float4(res[0], res[1], res[2], res[3]));
+    __stcs(o4 + 1, make_float4(res[4], res[5], res[6], res[7]));
+    __stcs(o4 + 2, make_float4(res[8], res[9], res[10], res[11]));
   } else {
     for (int k = 0; k < 4; ++k)
       if (q0 + k < HW)
-        for (int c = 0; c < 3; ++c) op[3 * (q0 + k) + c] = res[3 * k + c];
+        for (int c = 0; c < 3; ++c) op[3 * ((int64_t)q0 + k) + c] = res[3 * k + c];
   }
 }
 
@@ -246,7 +250,8 @@ extern "C" int vx_matched_points(const void* depth, int depth_f32, const int64_t
 extern "C" int vx_unproject_depth(const float* depth, int S, int H, int W, const float* extrinsic,
                                   const float* intrinsic, float* out, void* stream) {
   using namespace vx;
-  VX_CHECK_ARG(S >= 0 && H > 0 && W > 0 && S <= 65535, "vx_unproject_depth: bad shape");
+  VX_CHECK_ARG(S >= 0 && H > 0 && W > 0 && S <= 65535 && (int64_t)H * W < (1ll << 31) - 4,
+               "vx_unproject_depth: bad shape");
   if (S == 0) return VX_OK;
   VX_CHECK_ARG(depth && extrinsic && intrinsic && out, "vx_unproject_depth: null pointer");
   const int64_t quads = ((int64_t)H * W + 3) / 4;
