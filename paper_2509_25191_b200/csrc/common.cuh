@@ -227,6 +227,10 @@ VX_DEVICE void tmem_st16(uint32_t taddr, const uint32_t* r) {
       VX_W8(r, 0), VX_W8(r, 8)
       : "memory");
 }
+VX_DEVICE void tmem_st8(uint32_t taddr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), VX_W8(r, 0)
+               : "memory");
+}
 VX_DEVICE void tmem_st32(uint32_t taddr, const uint32_t* r) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"

@@ -4,30 +4,26 @@
 // (frame blocks, batch S*16 sequences of 1374 tokens; a8:
 // global blocks, 16 sequences of S*1374 tokens).  Non-causal, d in {32, 64}.
 //
-// One CTA = one work unit = 256 query rows (two 128-row Q tiles) of one
-// (head, sequence); persistent grid over units, head-major so concurrently
-// running CTAs share K/V through L2.
+// One CTA = one work unit = NT 128-row Q tiles of one (head, sequence); persistent grid over
+// units, head-major so concurrently running CTAs share K/V through L2.
 //
-// TMEM (512 columns), per Q tile i:  S_i [128 fp32] | P_i [64 = 128 bf16] | O_i [D fp32].
-// P has its own columns, so the MMA warp computes S_i(j+1) while the softmax
-// warps are still turning S_i(j) into P_i(j): the tensor core runs one KV tile
-// ahead of the softmax (aliasing P onto S, as in the first version, serialised them).
+// d = 64 (default): NT = 4 tiles x 48-wide KV tiles.  TMEM (512 columns) per Q tile i:
+//   S_i [48 fp32, P_i bf16 written over it] | O_i [64 + 16 fp32].
+// V is extended by a constant panel of ones, so the PV MMA also accumulates the row sums of P
+// into O_i[:, 64] (same lazy rescaling as O; no FADD row sums).  With P aliased onto S the MMA
+// issuer runs PV_i(j) then S_i(j+1) into the same columns (tcgen05 executes in issue order).
+// Other shapes (d = 32 / 128, diagnostics): separate P columns, S(j+1) issued ahead of the softmax.
 //
-// Warp roles (384 threads):
+// Warp roles (128 + 128*NT threads):
 //   w0      TMA producer: Q tiles once per unit, K/V tiles through a KST-stage ring
 //   w1      tcgen05.mma issuer (one lane): S_i = Q_i K^T (SS), O_i += P_i V (TS: P from TMEM)
 //   w2      TMEM allocator
-//   w4..w11 softmax + epilogue: one warpgroup per Q tile; thread = one query row = one TMEM
-//           lane owning all 128 score columns of the KV tile (row max / sum thread-local).
+//   w4..    softmax + epilogue: one warpgroup per Q tile; thread = one query row = one TMEM
+//           lane owning all score columns of the KV tile (row max / sum thread-local).
 // Softmax arithmetic: x = s*scale*log2e - m with FFMA2 (packed fp32x2), 2 of every 8 exp pairs
-// on the FMA pipe (packed degree-3 polynomial), the rest on MUFU ex2; FMNMX3 max tree; FADD2
-// row sums; lazy rescaling of O only when the running max grows by > 2^8.  The column mask of
-// the last KV tile lives on a separate code path (BoolTag) so the common path carries none.
-// Measured limits (tools/trace_attn.py, profiles/): MUFU saturated during the exp phase; the
-// S-wait / TMEM-load / max / P-hand-off phases (~1000 clk per KV tile) are where it idles.
-//
-// MMA issue order per KV tile j:  S_0(j+1), S_1(j+1) (as soon as S_i(j) was loaded),
-// PV_0(j) (when P_0(j) is written), PV_1(j).
+// on the FMA pipe (packed degree-3 polynomial), the rest on MUFU ex2; FMNMX3 max tree; lazy
+// rescaling of O only when the running max grows by > 2^8.  The column mask of the last KV tile
+// lives on a separate code path (BoolTag) so the common path carries none.
 #include <math.h>
 #include <stdlib.h>
 
@@ -47,14 +43,18 @@ struct AttnArgs {
   float* lse;
 };
 
-template <int D, int NT_ = (D == 128 ? 1 : 2), int BKV_ = 128, bool ALIAS_ = false>
+template <int D, int NT_ = (D == 128 ? 1 : 2), int BKV_ = 128, bool ALIAS_ = false, bool SUMV_ = false>
 struct AttnCfg {
   // ALIAS: P is written over the first BKV/2 columns of S (4 tiles fit TMEM); S_i(j+1) is then
   // issued after PV_i(j) instead of running ahead
   static constexpr bool ALIAS = ALIAS_;
+  // SUMV: the row sums come out of the PV MMA: V is extended by a panel of ones (N = D + 16), so
+  // O_i[:, D] accumulates sum_k P_ik with the same lazy rescaling as O — no FADD row sums
+  static constexpr bool SUMV = SUMV_;
+  static constexpr int DO = D + (SUMV ? 16 : 0);           // O accumulator columns
   static constexpr int NT = NT_;                           // 128-row Q tiles per CTA (TMEM budget)
   static constexpr int BKV = BKV_;                         // KV rows per tile (score columns)
-  static constexpr int KST = D == 128 ? 2 : (BKV == 64 ? 4 : 3);
+  static constexpr int KST = D == 128 ? 2 : (BKV <= 64 ? 4 : 3);
   static constexpr int PANEL_COLS = D == 32 ? 32 : 64;     // one swizzle atom wide (<= 128 B)
   static constexpr int PANELS = D / PANEL_COLS;            // D = 128: two 64-column panels
   static constexpr uint32_t ROW_BYTES = PANEL_COLS * 2;    // bytes per row inside a panel
@@ -62,20 +62,40 @@ struct AttnCfg {
   static constexpr uint32_t KVPANEL_BYTES = BKV * ROW_BYTES;
   static constexpr uint32_t Q_TILE_BYTES = PANELS * QPANEL_BYTES;
   static constexpr uint32_t KV_TILE_BYTES = PANELS * KVPANEL_BYTES;
+  static constexpr uint32_t V_STAGE_BYTES = KV_TILE_BYTES + (SUMV ? KVPANEL_BYTES : 0);  // + ones panel
   static constexpr int SWIZZLE = D == 32 ? 64 : 128;
   static constexpr uint32_t LAYOUT = D == 32 ? 4 : 2;      // SWIZZLE_64B / SWIZZLE_128B
   static constexpr uint32_t SBO = 8 * ROW_BYTES;           // 8-row core-matrix group
   static constexpr int THREADS = 128 + 128 * NT;
   static constexpr int ROWS = 128 * NT;                    // query rows per work unit
   static constexpr uint32_t BAR_BYTES = 512;
-  static constexpr uint32_t SMEM = NT * Q_TILE_BYTES + 2 * KST * KV_TILE_BYTES + 1024 + BAR_BYTES;
-  // TMEM columns: S_i [BKV fp32] ... | P_i [BKV/2] ... | O_i [D fp32] ...
+  static constexpr uint32_t SMEM = NT * Q_TILE_BYTES + KST * (KV_TILE_BYTES + V_STAGE_BYTES) + 1024 + BAR_BYTES;
+  // TMEM columns: S_i [BKV fp32] ... | P_i [BKV/2] ... | O_i [DO fp32] ...
   static constexpr uint32_t O_BASE = ((NT * BKV + (ALIAS ? 0 : NT * BKV / 2)) + 63) / 64 * 64;
-  static_assert(O_BASE + NT * D <= 512, "TMEM budget");
+  static_assert(O_BASE + NT * DO <= 512, "TMEM budget");
+  static_assert(!SUMV || (ALIAS && D == 64), "SUMV is implemented for the aliased d=64 kernel");
+  static_assert(BKV % 16 == 0 && (BKV <= 64 || BKV % 64 == 0), "KV tile width");
   static __host__ __device__ constexpr uint32_t tS(int i) { return i * BKV; }
   static __host__ __device__ constexpr uint32_t tP(int i) { return ALIAS ? i * BKV : NT * BKV + i * (BKV / 2); }
-  static __host__ __device__ constexpr uint32_t tO(int i) { return O_BASE + i * D; }
+  static __host__ __device__ constexpr uint32_t tO(int i) { return O_BASE + i * DO; }
 };
+
+// TMEM <-> register helpers for column counts that are multiples of 8
+template <int N>
+VX_DEVICE void tmem_ld_n(uint32_t taddr, uint32_t* r) {
+  static_assert(N % 16 == 0, "ld width");
+#pragma unroll
+  for (int c = 0; c + 32 <= N; c += 32) tmem_ld32(taddr + c, r + c);
+  if constexpr (N % 32 == 16) tmem_ld16(taddr + N - 16, r + N - 16);
+}
+template <int N>
+VX_DEVICE void tmem_st_n(uint32_t taddr, const uint32_t* r) {
+  static_assert(N % 8 == 0, "st width");
+#pragma unroll
+  for (int c = 0; c + 32 <= N; c += 32) tmem_st32(taddr + c, r + c);
+  if constexpr (N % 32 >= 16) tmem_st16(taddr + N / 32 * 32, r + N / 32 * 32);
+  if constexpr (N % 16 == 8) tmem_st8(taddr + N - 8, r + N - 8);
+}
 
 template <bool B>
 struct BoolTag {
@@ -86,12 +106,14 @@ constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
 
 
 // EMU_PAIRS_OF_8: of every 8 exp pairs, this many use the FMA-pipe polynomial
-template <int D, int EMU_PAIRS_OF_8, int NT_, int BKV_, bool ALIAS_>
-__global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_>::THREADS, 1)
+template <int D, int EMU_PAIRS_OF_8, int NT_, int BKV_, bool ALIAS_, bool SUMV_>
+__global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS, 1)
     fmha_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                 const __grid_constant__ CUtensorMap tmV, const AttnArgs a) {
-  using Cfg = AttnCfg<D, NT_, BKV_, ALIAS_>;
+  using Cfg = AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>;
   constexpr bool ALIAS = ALIAS_;
+  constexpr bool SUMV = SUMV_;
+  constexpr int DO = Cfg::DO;
   constexpr int BKV = Cfg::BKV;
   constexpr int KST = Cfg::KST;
   extern __shared__ uint8_t smem_raw[];
@@ -101,8 +123,8 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_>::THREADS, 1)
   constexpr int NT = Cfg::NT;
   uint8_t* sQ = smem;                                 // NT tiles
   uint8_t* sK = sQ + NT * Cfg::Q_TILE_BYTES;          // KST tiles
-  uint8_t* sV = sK + KST * Cfg::KV_TILE_BYTES;        // KST tiles
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sV + KST * Cfg::KV_TILE_BYTES);
+  uint8_t* sV = sK + KST * Cfg::KV_TILE_BYTES;        // KST stages (V tile [+ ones panel])
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sV + KST * Cfg::V_STAGE_BYTES);
   uint64_t* q_full = bar;
   uint64_t* q_empty = bar + 1;
   uint64_t* k_full = bar + 2;
@@ -141,6 +163,15 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_>::THREADS, 1)
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, 512);
+  if constexpr (SUMV) {  // the constant ones panel of every V stage (read by the tensor core)
+    const uint32_t ones = 0x3f803f80u;  // bf16x2 (1, 1)
+    for (uint32_t o = threadIdx.x * 16; o < KST * Cfg::KVPANEL_BYTES; o += Cfg::THREADS * 16) {
+      const uint32_t st = o / Cfg::KVPANEL_BYTES, off = o % Cfg::KVPANEL_BYTES;
+      *reinterpret_cast<uint4*>(sV + st * Cfg::V_STAGE_BYTES + Cfg::KV_TILE_BYTES + off) =
+          make_uint4(ones, ones, ones, ones);
+    }
+    fence_proxy_async_smem();
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -179,7 +210,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_>::THREADS, 1)
           mbar_wait(&v_empty[st], ph ^ 1);
           mbar_expect_tx(&v_full[st], Cfg::KV_TILE_BYTES);
           for (int pn = 0; pn < Cfg::PANELS; ++pn)
-            tma_load_2d_hint(sV + st * Cfg::KV_TILE_BYTES + pn * Cfg::KVPANEL_BYTES, &tmV, &v_full[st],
+            tma_load_2d_hint(sV + st * Cfg::V_STAGE_BYTES + pn * Cfg::KVPANEL_BYTES, &tmV, &v_full[st],
                              pn * Cfg::PANEL_COLS, kv_row + BKV * j, pol_kv);
         }
       }
@@ -188,7 +219,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_>::THREADS, 1)
     // ------------------------------------------------------------ MMA issuer
     if (elect_one()) {
       constexpr uint32_t idesc_qk = make_idesc_bf16(128, BKV, 0, 0);
-      constexpr uint32_t idesc_pv = make_idesc_bf16(128, D, 0, 1);
+      constexpr uint32_t idesc_pv = make_idesc_bf16(128, DO, 0, 1);
       const uint32_t q0 = smem_u32(sQ);
       constexpr int KSTEPS_PER_PANEL = Cfg::PANEL_COLS / 16;
       auto issue_qk = [&](int i, uint32_t ks) {
@@ -233,7 +264,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_>::THREADS, 1)
             const uint32_t st = c % KST, ph = (c / KST) & 1;
             const bool has_next = j + 1 < nkv;
             const uint32_t nst = (c + 1) % KST, nph = ((c + 1) / KST) & 1;
-            const uint32_t vs = smem_u32(sV + st * Cfg::KV_TILE_BYTES);
+            const uint32_t vs = smem_u32(sV + st * Cfg::V_STAGE_BYTES);
             const uint32_t nks = smem_u32(sK + nst * Cfg::KV_TILE_BYTES);
             mbar_wait(&v_full[st], ph);
             if (has_next) mbar_wait(&k_full[nst], nph);
@@ -293,7 +324,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_>::THREADS, 1)
               mma_commit(&k_empty[nst]);
               if (j + 2 == nkv) mma_commit(q_empty);
             }
-            const uint32_t vs = smem_u32(sV + st * Cfg::KV_TILE_BYTES);
+            const uint32_t vs = smem_u32(sV + st * Cfg::V_STAGE_BYTES);
             mbar_wait(&v_full[st], ph);
             if (j == 0)  // the previous unit's epilogue must have read O
               for (int i = 0; i < NT; ++i) mbar_wait(&o_empty[i], (n & 1) ^ 1);
@@ -334,8 +365,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_>::THREADS, 1)
         sph ^= 1;
         tc_fence_after();
         uint32_t sr[BKV];
-#pragma unroll
-        for (int c = 0; c < BKV / 32; ++c) tmem_ld32(S_addr + 32 * c, sr + 32 * c);
+        tmem_ld_n<BKV>(S_addr, sr);
         tmem_wait_ld();
         if constexpr (!ALIAS) {
           tc_fence_before();
@@ -366,11 +396,13 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_>::THREADS, 1)
           if (need) m_run = m_new;
           const uint64_t NEGM = f2_pack(-m_run, -m_run);
           uint64_t acc[4] = {0, 0, 0, 0};
+          constexpr int NCHUNK = (BKV + 63) / 64;
 #pragma unroll
-          for (int hf = 0; hf < BKV / 64; ++hf) {
-            uint32_t pk[32];
+          for (int hf = 0; hf < NCHUNK; ++hf) {
+            constexpr int PAIRS = BKV >= 64 ? 32 : BKV / 2;  // column pairs in this chunk
+            uint32_t pk[PAIRS];
 #pragma unroll
-            for (int c = 0; c < 32; ++c) {
+            for (int c = 0; c < PAIRS; ++c) {
               const int e = 64 * hf + 2 * c;
               const uint64_t x = f2_fma(f2_pack(__uint_as_float(sr[e]), __uint_as_float(sr[e + 1])), SL2, NEGM);
               float x0, x1, p0, p1;
@@ -381,7 +413,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_>::THREADS, 1)
                 p0 = ex2(x0);
                 p1 = ex2(x1);
               }
-              acc[c & 3] = f2_add(acc[c & 3], f2_pack(p0, p1));
+              if constexpr (!SUMV) acc[c & 3] = f2_add(acc[c & 3], f2_pack(p0, p1));
               pk[c] = pack_bf16(p0, p1);
             }
             if (!ALIAS && hf == 0 && j > 0) {  // P_i(j-1) consumed and O stable (waited after the first exps)
@@ -389,9 +421,9 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_>::THREADS, 1)
               ++pv_cnt;
               tc_fence_after();
             }
-            tmem_st32(P_addr + 32 * hf, pk);
+            tmem_st_n<PAIRS>(P_addr + 32 * hf, pk);
           }
-          {
+          if constexpr (!SUMV) {
             float a0, a1, b0, b1;
             f2_unpack(f2_add(acc[0], acc[1]), a0, a1);
             f2_unpack(f2_add(acc[2], acc[3]), b0, b1);
@@ -400,12 +432,15 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_>::THREADS, 1)
           if (__any_sync(0xffffffff, need) && j > 0) {
             uint32_t orr[32];
 #pragma unroll
-            for (int c0 = 0; c0 < D; c0 += 32) {
-              tmem_ld32(O_addr + c0, orr);
+            for (int c0 = 0; c0 < DO; c0 += 32) {
+              const int w = DO - c0 >= 32 ? 32 : 16;
+              if (w == 32) tmem_ld32(O_addr + c0, orr);
+              else tmem_ld16(O_addr + c0, orr);
               tmem_wait_ld();
 #pragma unroll
               for (int c = 0; c < 32; ++c) orr[c] = __float_as_uint(__uint_as_float(orr[c]) * alpha);
-              tmem_st32(O_addr + c0, orr);
+              if (w == 32) tmem_st32(O_addr + c0, orr);
+              else tmem_st16(O_addr + c0, orr);
             }
           }
         };
@@ -419,10 +454,10 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_>::THREADS, 1)
       mbar_wait(&p_free[tile], pv_cnt & 1);
       ++pv_cnt;
       tc_fence_after();
-      uint32_t orr[D];
-#pragma unroll
-      for (int c0 = 0; c0 < D; c0 += 32) tmem_ld32(O_addr + c0, orr + c0);
+      uint32_t orr[DO];
+      tmem_ld_n<DO>(O_addr, orr);
       tmem_wait_ld();
+      if constexpr (SUMV) l_run = __uint_as_float(orr[D]);  // sum_k P_ik from the ones panel
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&o_empty[tile]);
@@ -449,9 +484,9 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_>::THREADS, 1)
   }
 }
 
-template <int D, int EMU, int NT = (D == 128 ? 1 : 2), int BKV = 128, bool ALIAS = false>
+template <int D, int EMU, int NT = (D == 128 ? 1 : 2), int BKV = 128, bool ALIAS = false, bool SUMV = false>
 static int launch_fmha(const void* q, const void* k, const void* v, AttnArgs args, cudaStream_t st) {
-  using Cfg = AttnCfg<D, NT, BKV, ALIAS>;
+  using Cfg = AttnCfg<D, NT, BKV, ALIAS, SUMV>;
   CUtensorMap tq, tk, tv;
   constexpr int PC = Cfg::PANEL_COLS;
   if (!make_tmap_2d_bf16(&tq, q, (uint64_t)args.H * args.Tq, D, D, 128, PC, Cfg::SWIZZLE)) return VX_E_ARG;
@@ -460,7 +495,7 @@ static int launch_fmha(const void* q, const void* k, const void* v, AttnArgs arg
   args.q_blocks = (args.Lq + Cfg::ROWS - 1) / Cfg::ROWS;
   args.kv_tiles = (args.Lk + BKV - 1) / BKV;
   args.units = args.H * args.nseq * args.q_blocks;
-  auto kern = fmha_kernel<D, EMU, NT, BKV, ALIAS>;
+  auto kern = fmha_kernel<D, EMU, NT, BKV, ALIAS, SUMV>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
@@ -503,28 +538,24 @@ extern "C" int vx_attention(const void* q, const void* k, const void* v, void* o
     return e ? atoi(e) : 2;
   }();
   static int cfg = [] {
-    const char* e = getenv("VX_FMHA_CFG");  // diagnostic: 0 auto, 1 = 2x128, 3 = 3x64, 4 = 4x64-alias
+    const char* e = getenv("VX_FMHA_CFG");  // diagnostic: 0 default (4x48 + ones panel), 1 = 2x128, 3 = 3x64,
+                                            // 4 = 4x64 aliased
     return e ? atoi(e) : 0;
   }();
   if (D == 64) {
-    // long KV sequences (global layers): 4 Q tiles x 64-wide KV tiles, P aliased onto S
-    // (4 softmax warps per sub-partition); short ones (frame layers, 11-22 KV tiles): 3 Q tiles
-    // with separate P columns so S(j+1) runs ahead of the softmax.
-    const int c = cfg ? cfg : (Lk >= 4096 ? 4 : 3);
-    if (c == 1) return launch_fmha<64, 2, 2, 128>(q, k, v, a, st);
-    if (c == 4) {
-      switch (emu) {
-        case 0: return launch_fmha<64, 0, 4, 64, true>(q, k, v, a, st);
-        case 1: return launch_fmha<64, 1, 4, 64, true>(q, k, v, a, st);
-        case 3: return launch_fmha<64, 3, 4, 64, true>(q, k, v, a, st);
-        default: return launch_fmha<64, 2, 4, 64, true>(q, k, v, a, st);
-      }
+    // default (frame and global layers): 4 Q tiles x 48-wide KV tiles, P aliased onto S, row sums
+    // from a ones panel appended to V (tools/sweep_sumv.sh: global 1013 / frame 740 TFLOP/s at 20
+    // views vs 991 / 719 for 4x64-aliased and 971 / 733 for 3x64 run-ahead)
+    switch (cfg) {
+      case 1: return launch_fmha<64, 2, 2, 128>(q, k, v, a, st);
+      case 3: return launch_fmha<64, 2, 3, 64>(q, k, v, a, st);
+      case 4: return launch_fmha<64, 2, 4, 64, true>(q, k, v, a, st);
+      default: break;
     }
     switch (emu) {
-      case 0: return launch_fmha<64, 0, 3, 64>(q, k, v, a, st);
-      case 1: return launch_fmha<64, 1, 3, 64>(q, k, v, a, st);
-      case 3: return launch_fmha<64, 3, 3, 64>(q, k, v, a, st);
-      default: return launch_fmha<64, 2, 3, 64>(q, k, v, a, st);
+      case 1: return launch_fmha<64, 1, 4, 48, true, true>(q, k, v, a, st);
+      case 3: return launch_fmha<64, 3, 4, 48, true, true>(q, k, v, a, st);
+      default: return launch_fmha<64, 2, 4, 48, true, true>(q, k, v, a, st);
     }
   }
   if (D == 128) return launch_fmha<128, 2>(q, k, v, a, st);
