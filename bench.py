@@ -241,7 +241,9 @@ def main():
         tp = os.path.join(ROOT, "profiles", "fmha_traffic.json")
         if os.path.exists(tp):
             with open(tp) as f:
-                traffic = json.load(f).get("dram_bytes_per_launch")
+                tj = json.load(f)
+            if tj.get("views") == S:  # measured for this workload's launch only
+                traffic = tj.get("dram_bytes_per_launch")
         roofline = {"bound": "tensor", "kernel": "vx fmha_kernel<64> (global attention)",
                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                     "peak_source": peaks["source"] + " bf16_tflops_sustained",
