@@ -69,7 +69,7 @@ VX_DEVICE void epi_chunk32(const GemmArgs& a, int row, int col, const uint32_t* 
     for (int j = 0; j < 4; ++j) {
       float t[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) t[u] = (EPI == VX_EPI_GELU) ? gelu_erf(v[8 * j + u]) : v[8 * j + u];
+      for (int u = 0; u < 8; ++u) t[u] = (EPI == VX_EPI_GELU) ? gelu_erf_fast(v[8 * j + u]) : v[8 * j + u];
       dst[j] = make_uint4(pack_bf16(t[0], t[1]), pack_bf16(t[2], t[3]), pack_bf16(t[4], t[5]),
                           pack_bf16(t[6], t[7]));
     }
@@ -142,8 +142,16 @@ VX_DEVICE void epi_qkv_head(const GemmArgs& a, int row, int col, float* v) {
         var += d * d;
       }
       const float rstd = rsqrtf(var * (1.0f / D) + e.eps);
+      const float4* w4 = reinterpret_cast<const float4*>(nw);
+      const float4* b4 = reinterpret_cast<const float4*>(nb);
 #pragma unroll
-      for (int j = 0; j < D; ++j) v[j] = (v[j] - mean) * rstd * __ldg(nw + j) + __ldg(nb + j);
+      for (int j = 0; j < D / 4; ++j) {  // 16-byte uniform loads of the affine parameters
+        const float4 w = __ldg(w4 + j), b = __ldg(b4 + j);
+        v[4 * j + 0] = (v[4 * j + 0] - mean) * rstd * w.x + b.x;
+        v[4 * j + 1] = (v[4 * j + 1] - mean) * rstd * w.y + b.y;
+        v[4 * j + 2] = (v[4 * j + 2] - mean) * rstd * w.z + b.z;
+        v[4 * j + 3] = (v[4 * j + 3] - mean) * rstd * w.w + b.w;
+      }
     }
     if (e.rope_cos) {
       const int t = row % e.tokens_per_frame;
@@ -154,22 +162,24 @@ VX_DEVICE void epi_qkv_head(const GemmArgs& a, int row, int col, float* v) {
         px = p - (py - 1) * e.grid_w + 1;
       }
       constexpr int Q4 = D / 4;
-      const float* cy = e.rope_cos + py * Q4;
-      const float* sy = e.rope_sin + py * Q4;
-      const float* cx = e.rope_cos + px * Q4;
-      const float* sx = e.rope_sin + px * Q4;
+      static_assert(Q4 % 4 == 0, "rope quarter must be a multiple of 4");
+      const float4* cy = reinterpret_cast<const float4*>(e.rope_cos + py * Q4);
+      const float4* sy = reinterpret_cast<const float4*>(e.rope_sin + py * Q4);
+      const float4* cx = reinterpret_cast<const float4*>(e.rope_cos + px * Q4);
+      const float4* sx = reinterpret_cast<const float4*>(e.rope_sin + px * Q4);
+      auto rot = [&](int j0, const float4 c4, const float4 s4) {  // (x0, x1) = (v[j], v[j + Q4]) rotated
+        const float cc[4] = {c4.x, c4.y, c4.z, c4.w}, ss[4] = {s4.x, s4.y, s4.z, s4.w};
 #pragma unroll
-      for (int j = 0; j < Q4; ++j) {
-        float c = __ldg(cy + j), s = __ldg(sy + j);
-        float x0 = v[j], x1 = v[j + Q4];
-        v[j] = x0 * c - x1 * s;
-        v[j + Q4] = x1 * c + x0 * s;
-        c = __ldg(cx + j);
-        s = __ldg(sx + j);
-        x0 = v[2 * Q4 + j];
-        x1 = v[3 * Q4 + j];
-        v[2 * Q4 + j] = x0 * c - x1 * s;
-        v[3 * Q4 + j] = x1 * c + x0 * s;
+        for (int u = 0; u < 4; ++u) {
+          const float x0 = v[j0 + u], x1 = v[j0 + u + Q4];
+          v[j0 + u] = x0 * cc[u] - x1 * ss[u];
+          v[j0 + u + Q4] = x1 * cc[u] + x0 * ss[u];
+        }
+      };
+#pragma unroll
+      for (int j = 0; j < Q4 / 4; ++j) {  // y rotation on the first half, x rotation on the second
+        rot(4 * j, __ldg(cy + j), __ldg(sy + j));
+        rot(2 * Q4 + 4 * j, __ldg(cx + j), __ldg(sx + j));
       }
     }
   }

@@ -81,6 +81,20 @@ def gemm(views, res):
             fn = lambda: ops.gemm(A, w, epi, bias=bias, out=out)
         t = timeit(fn)
         res[f"gemm_{name}_S{views}"] = {"ms": t, "tflops": fl / t / 1e9}
+        if name == "qkv":  # the real fused epilogue: per-head LayerNorm + 2D RoPE + scatter to [H, T, d]
+            H, d = 16, 64
+            q, k, v = (torch.empty(H, M, d, device="cuda", dtype=torch.bfloat16) for _ in range(3))
+            nw = [torch.rand(d, device="cuda") + 0.5 for _ in range(4)]
+            from paper_2509_25191_b200.aggregator import rope_tables
+            rope = tuple(r.cuda() for r in rope_tables(64, 38, 100.0))
+            fnq = lambda: ops.gemm(A, w, ops.EPI_QKV, bias=bias, qkv=(q, k, v), qk_norm=tuple(nw), rope=rope,
+                                   head_dim=d, tokens_total=M, tokens_per_frame=1374, patch_start=5, grid_w=37)
+            t = timeit(fnq)
+            res[f"gemm_qkv_fused_S{views}"] = {"ms": t, "tflops": fl / t / 1e9}
+        if name == "fc1":  # same GEMM without GELU: the epilogue's share
+            out2 = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+            t = timeit(lambda: ops.gemm(A, w, ops.EPI_BF16, bias=bias, out=out2))
+            res[f"gemm_fc1_nogelu_S{views}"] = {"ms": t, "tflops": fl / t / 1e9}
         Ac = A.contiguous()
         t = timeit(lambda: torch.matmul(Ac, w.t()))
         res[f"cublas_{name}_S{views}"] = {"ms": t, "tflops": fl / t / 1e9}
