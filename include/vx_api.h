@@ -95,6 +95,12 @@ int vx_attention(const void* q, const void* k, const void* v, void* out, int64_t
  * x_dtype / y_dtype: 0 = fp32, 1 = bf16.  w/b may be NULL (no affine). (norm1/norm2, a5) */
 int vx_layernorm(const void* x, int x_dtype, int64_t ldx, void* y, int y_dtype, int64_t ldy,
                  const float* w, const float* b, int rows, int cols, float eps, void* stream);
+/* Same, reading output row r from input row (r / group_rows) * group_stride + group_offset +
+ * r % group_rows — e.g. the DPT heads' patch tokens of each frame (group_rows = patches,
+ * group_stride = tokens per frame, group_offset = patch_start) without a gather copy. */
+int vx_layernorm_gather(const void* x, int x_dtype, int64_t ldx, void* y, int y_dtype, int64_t ldy,
+                        const float* w, const float* b, int rows, int cols, float eps, int group_rows,
+                        int group_stride, int group_offset, void* stream);
 
 /* ResNet-normalise + im2col of (S,3,H,W) fp32 images into bf16 [S*P, Kpad] with
  * K order (c, ky, kx) and zero padding K..Kpad-1.  (Aggregator normalize + PatchEmbed, a1/a2) */

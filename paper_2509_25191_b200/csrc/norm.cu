@@ -37,12 +37,15 @@ VX_DEVICE void store4<__nv_bfloat16>(__nv_bfloat16* p, const float (&o)[4]) {
 template <typename TI, typename TO, int NV>
 __global__ void __launch_bounds__(256) layernorm_kernel(const TI* __restrict__ x, int64_t ldx, TO* __restrict__ y,
                                                         int64_t ldy, const float* __restrict__ w,
-                                                        const float* __restrict__ b, int rows, float eps) {
+                                                        const float* __restrict__ b, int rows, float eps,
+                                                        int g_rows, int g_stride, int g_off) {
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= rows) return;
   constexpr int cols = 128 * NV;
-  const TI* xr = x + (size_t)row * ldx;
+  // input row gather: output row r reads row (r / g_rows) * g_stride + g_off + r % g_rows
+  const int g = row / g_rows;
+  const TI* xr = x + ((size_t)g * g_stride + g_off + (row - g * g_rows)) * ldx;
   float v[NV][4];
 #pragma unroll
   for (int i = 0; i < NV; ++i) load4<TI>(xr + (i * 32 + lane) * 4, v[i]);
@@ -85,13 +88,15 @@ __global__ void __launch_bounds__(256) layernorm_kernel(const TI* __restrict__ x
 
 template <typename TI, typename TO>
 static int ln_dispatch(const void* x, int64_t ldx, void* y, int64_t ldy, const float* w, const float* b, int rows,
-                       int cols, float eps, cudaStream_t st) {
+                       int cols, float eps, cudaStream_t st, int g_rows, int g_stride, int g_off) {
   const int grid = (rows + 7) / 8;
   const TI* xi = reinterpret_cast<const TI*>(x);
   TO* yo = reinterpret_cast<TO*>(y);
   switch (cols / 128) {
 #define VX_LN_CASE(nv) \
-  case nv: layernorm_kernel<TI, TO, nv><<<grid, 256, 0, st>>>(xi, ldx, yo, ldy, w, b, rows, eps); break;
+  case nv:                 \
+    layernorm_kernel<TI, TO, nv><<<grid, 256, 0, st>>>(xi, ldx, yo, ldy, w, b, rows, eps, g_rows, g_stride, g_off); \
+    break;
     VX_LN_CASE(1)
     VX_LN_CASE(2)
     VX_LN_CASE(4)
@@ -152,21 +157,33 @@ __global__ void special_tokens_kernel(float* __restrict__ x, const float* __rest
 
 }  // namespace vx
 
-extern "C" int vx_layernorm(const void* x, int x_dtype, int64_t ldx, void* y, int y_dtype, int64_t ldy,
-                            const float* w, const float* b, int rows, int cols, float eps, void* stream) {
+extern "C" int vx_layernorm_gather(const void* x, int x_dtype, int64_t ldx, void* y, int y_dtype, int64_t ldy,
+                                   const float* w, const float* b, int rows, int cols, float eps, int group_rows,
+                                   int group_stride, int group_offset, void* stream) {
   using namespace vx;
   VX_CHECK_ARG(x && y, "vx_layernorm: null pointer");
   VX_CHECK_ARG(rows >= 0 && cols > 0 && cols % 128 == 0, "vx_layernorm: cols=%d must be a multiple of 128", cols);
   VX_CHECK_ARG(ldx % 8 == 0 && ldy % 8 == 0, "vx_layernorm: ld must be a multiple of 8");
+  VX_CHECK_ARG(group_rows > 0 && group_offset >= 0 && group_stride >= group_rows + group_offset,
+               "vx_layernorm: bad row gather (%d, %d, %d)", group_rows, group_stride, group_offset);
   if (rows == 0) return VX_OK;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if (x_dtype == 0 && y_dtype == 1) return ln_dispatch<float, __nv_bfloat16>(x, ldx, y, ldy, w, b, rows, cols, eps, st);
+  const int gr = group_rows, gs = group_stride, go = group_offset;
+  if (x_dtype == 0 && y_dtype == 1)
+    return ln_dispatch<float, __nv_bfloat16>(x, ldx, y, ldy, w, b, rows, cols, eps, st, gr, gs, go);
   if (x_dtype == 1 && y_dtype == 1)
-    return ln_dispatch<__nv_bfloat16, __nv_bfloat16>(x, ldx, y, ldy, w, b, rows, cols, eps, st);
-  if (x_dtype == 0 && y_dtype == 0) return ln_dispatch<float, float>(x, ldx, y, ldy, w, b, rows, cols, eps, st);
-  if (x_dtype == 1 && y_dtype == 0) return ln_dispatch<__nv_bfloat16, float>(x, ldx, y, ldy, w, b, rows, cols, eps, st);
+    return ln_dispatch<__nv_bfloat16, __nv_bfloat16>(x, ldx, y, ldy, w, b, rows, cols, eps, st, gr, gs, go);
+  if (x_dtype == 0 && y_dtype == 0) return ln_dispatch<float, float>(x, ldx, y, ldy, w, b, rows, cols, eps, st, gr, gs, go);
+  if (x_dtype == 1 && y_dtype == 0)
+    return ln_dispatch<__nv_bfloat16, float>(x, ldx, y, ldy, w, b, rows, cols, eps, st, gr, gs, go);
   set_error("vx_layernorm: bad dtypes %d -> %d", x_dtype, y_dtype);
   return VX_E_ARG;
+}
+
+extern "C" int vx_layernorm(const void* x, int x_dtype, int64_t ldx, void* y, int y_dtype, int64_t ldy,
+                            const float* w, const float* b, int rows, int cols, float eps, void* stream) {
+  return vx_layernorm_gather(x, x_dtype, ldx, y, y_dtype, ldy, w, b, rows, cols, eps, rows > 0 ? rows : 1,
+                             rows > 0 ? rows : 1, 0, stream);
 }
 
 extern "C" int vx_patchify(const float* images, void* out, int S, int H, int W, int patch, int Kpad, void* stream) {

@@ -120,6 +120,7 @@ class DPTHeadDevice:
 
     def __init__(self, W: DeviceWeights, head: str, activation: str):
         self.W, self.head, self.activation = W, head, activation
+        self._bufs: Dict[tuple, torch.Tensor] = {}  # zero-bordered activation buffers, see _pad
         cfg = W.cfg
         dev = W.patch_w.device
         g = cfg.grid
@@ -157,19 +158,30 @@ class DPTHeadDevice:
         self.head_w = hw.reshape(hw.shape[0], -1).float().contiguous()
         self.head_b = W[head + "scratch.output_conv2.2.bias"].float().contiguous()
 
+    def _pad(self, slot: str, Fr: int, H: int, W: int, C: int, dev) -> torch.Tensor:
+        """Zero-bordered NHWC buffer [Fr, H+2, W+2, C] for `slot`, cached across frame chunks and calls:
+        the producing kernels overwrite the whole interior, so the border is zeroed once at allocation
+        instead of zero-filling every buffer of every chunk."""
+        key = (slot, H, W, C)
+        buf = self._bufs.get(key)
+        if buf is None or buf.shape[0] < Fr or buf.device != torch.device(dev):
+            buf = torch.zeros(Fr, H + 2, W + 2, C, device=dev, dtype=torch.bfloat16)
+            self._bufs[key] = buf
+        return buf[:Fr]
+
     def _rcu(self, name, x_raw, x_relu, Fr, hs, res2=None, res2_pad=False, dense_out=False):
         """ResidualConvUnit: conv2(relu(conv1(relu(x)))) + x (+ res2), relu(x) supplied padded."""
         Fh = self.W.cfg.dpt_features
         dev = x_raw.device
-        h = torch.zeros(Fr, hs + 2, hs + 2, Fh, device=dev, dtype=torch.bfloat16)
+        h = self._pad(name + ".h", Fr, hs, hs, Fh, dev)
         ops.gemm_spatial(x_relu.view(-1, Fh), self.cw[name + ".conv1"], self.b[name + ".conv1.bias"], Fr, hs, hs,
                          conv3x3=True, relu=True, out1=h, out1_pad=True)
         if dense_out:
             o = torch.empty(Fr, hs, hs, Fh, device=dev, dtype=torch.bfloat16)
             o2 = None
         else:
-            o = torch.zeros(Fr, hs + 2, hs + 2, Fh, device=dev, dtype=torch.bfloat16)
-            o2 = torch.zeros_like(o)
+            o = self._pad(name + ".o", Fr, hs, hs, Fh, dev)
+            o2 = self._pad(name + ".o2", Fr, hs, hs, Fh, dev)
         ops.gemm_spatial(h.view(-1, Fh), self.cw[name + ".conv2"], self.b[name + ".conv2.bias"], Fr, hs, hs,
                          conv3x3=True, res1=x_raw, res1_pad=True, res2=res2, res2_pad=res2_pad,
                          out1=o, out1_pad=not dense_out, out2=o2, out2_pad=True)
@@ -186,28 +198,27 @@ class DPTHeadDevice:
         Fr = layers[0].shape[0]
         dev = layers[0].device
         bf = torch.bfloat16
-        zeros = lambda *sh: torch.zeros(*sh, device=dev, dtype=bf)
         empty = lambda *sh: torch.empty(*sh, device=dev, dtype=bf)
+        pad = lambda slot, h_, w_, c_: self._pad(slot, Fr, h_, w_, c_, dev)
         sizes = [4 * g, 2 * g, g, (g + 1) // 2]
         feats = []
         for i, x in enumerate(layers):
-            tok = x[:, ps:].reshape(Fr * g * g, D)
-            xn = ops.layernorm(tok, W[head + "norm.weight"], W[head + "norm.bias"], cfg.ln_eps)
+            xn = ops.layernorm_tokens(x, ps, W[head + "norm.weight"], W[head + "norm.bias"], cfg.ln_eps)
             pb = self.b[f"{head}projects.{i}.bias"]
             if i < 2:  # 1x1 projection, then conv-transpose (k = s = 4 / 2) as GEMM + pixel shuffle
                 y = empty(Fr, g, g, oc[i])
                 ops.gemm_spatial(xn, self.proj_w[i], pb, Fr, g, g, out1=y, pos=self.pos_small[i])
                 s = 4 if i == 0 else 2
-                f = zeros(Fr, g * s + 2, g * s + 2, oc[i])
+                f = pad(f"f{i}", g * s, g * s, oc[i])
                 ops.gemm_spatial(y.view(-1, oc[i]), self.convT[i], self.b[f"{head}resize_layers.{i}.bias"], Fr, g, g,
                                  shuffle=s, out1=f, out1_pad=True)
             elif i == 2:  # identity
-                f = zeros(Fr, g + 2, g + 2, oc[i])
+                f = pad(f"f{i}", g, g, oc[i])
                 ops.gemm_spatial(xn, self.proj_w[i], pb, Fr, g, g, out1=f, out1_pad=True, pos=self.pos_small[i])
             else:  # 3x3 stride-2 conv: stride-1 implicit GEMM keeping even pixels
-                y = zeros(Fr, g + 2, g + 2, oc[i])
+                y = pad(f"y{i}", g, g, oc[i])
                 ops.gemm_spatial(xn, self.proj_w[i], pb, Fr, g, g, out1=y, out1_pad=True, pos=self.pos_small[i])
-                f = zeros(Fr, sizes[3] + 2, sizes[3] + 2, oc[i])
+                f = pad(f"f{i}", sizes[3], sizes[3], oc[i])
                 ops.gemm_spatial(y.view(-1, oc[i]), self.cw[head + "resize_layers.3"],
                                  self.b[head + "resize_layers.3.bias"], Fr, g, g, conv3x3=True, subsample2=True,
                                  out1=f, out1_pad=True)
@@ -216,16 +227,16 @@ class DPTHeadDevice:
         L = []
         for i, f in enumerate(feats):  # layer_rn 3x3 (no bias): raw + relu copies, padded
             hs = sizes[i]
-            l, lr = zeros(Fr, hs + 2, hs + 2, Fh), zeros(Fr, hs + 2, hs + 2, Fh)
+            l, lr = pad(f"l{i}", hs, hs, Fh), pad(f"lr{i}", hs, hs, Fh)
             ops.gemm_spatial(f.view(-1, oc[i]), self.cw[f"{sc}layer{i + 1}_rn"], None, Fr, hs, hs, conv3x3=True,
                              out1=l, out1_pad=True, out2=lr, out2_pad=True)
             L.append((l, lr))
 
-        def out_conv(r, o, hs, target, pad):
+        def out_conv(r, o, hs, target, padded):
             up = ops.upsample_bilinear(o, (target, target))
-            x = zeros(Fr, target + 2, target + 2, Fh) if pad else empty(Fr, target, target, Fh)
+            x = pad(f"oc{r}", target, target, Fh) if padded else empty(Fr, target, target, Fh)
             ops.gemm_spatial(up.view(-1, Fh), self.cw[f"{sc}refinenet{r}.out_conv"],
-                             self.b[f"{sc}refinenet{r}.out_conv.bias"], Fr, target, target, out1=x, out1_pad=pad)
+                             self.b[f"{sc}refinenet{r}.out_conv.bias"], Fr, target, target, out1=x, out1_pad=padded)
             return x
 
         # refinenet4: RCU2(l4) -> upsample to layer3 size -> out_conv
@@ -236,12 +247,12 @@ class DPTHeadDevice:
             s_raw, s_relu = self._rcu(f"{sc}refinenet{r}.resConfUnit1", L[li][0], L[li][1], Fr, hs,
                                       res2=x, res2_pad=False)
             o, _ = self._rcu(f"{sc}refinenet{r}.resConfUnit2", s_raw, s_relu, Fr, hs, dense_out=True)
-            x = out_conv(r, o, hs, target, pad=(r == 1))
+            x = out_conv(r, o, hs, target, padded=(r == 1))
         t = 2 * sizes[0]
         y = empty(Fr, t, t, Fh // 2)
         ops.gemm_spatial(x.view(-1, Fh), self.cw[sc + "output_conv1"], self.b[sc + "output_conv1.bias"], Fr, t, t,
                          conv3x3=True, out1=y)
-        u = ops.upsample_bilinear(y, (Hh, Ww), add=self.pos_full, out_pad=True)
+        u = ops.upsample_bilinear(y, (Hh, Ww), add=self.pos_full, out_pad=True, out=pad("u", Hh, Ww, Fh // 2))
         act = 0 if self.activation == "exp" else 1
         ops.gemm_spatial(u.view(-1, Fh // 2), self.cw[sc + "output_conv2.0"], self.b[sc + "output_conv2.0.bias"],
                          Fr, Hh, Ww, conv3x3=True, head=(self.head_w, self.head_b, act, pred, conf))

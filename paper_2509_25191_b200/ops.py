@@ -57,7 +57,8 @@ class GaProblem(ctypes.Structure):
     ]
 
 
-EXPORTED_SYMBOLS = ("vx_gemm", "vx_attention", "vx_layernorm", "vx_patchify", "vx_special_tokens",
+EXPORTED_SYMBOLS = ("vx_gemm", "vx_attention", "vx_layernorm", "vx_layernorm_gather", "vx_patchify",
+                    "vx_special_tokens",
                     "vx_upsample_bilinear", "vx_gemm_spatial", "vx_epipolar_residuals",
                     "vx_epipolar_accumulate", "vx_ga_decode", "vx_ga_residuals", "vx_ga_loss_grad",
                     "vx_ga_adam", "vx_ga_adaptive_weights", "vx_matched_points", "vx_unproject_depth",
@@ -79,6 +80,8 @@ def load_library(path: os.PathLike | None = None) -> ctypes.CDLL:
     lib.vx_gemm.argtypes = [_i32, _vp, _i64, _vp, _i64, _i32, _i32, _i32, ctypes.POINTER(Epilogue), _vp]
     lib.vx_attention.argtypes = [_vp, _vp, _vp, _vp, _i64, _vp, _i32, _i32, _i32, _i32, _i32, _i64, _i64, _vp]
     lib.vx_layernorm.argtypes = [_vp, _i32, _i64, _vp, _i32, _i64, _vp, _vp, _i32, _i32, _f32, _vp]
+    lib.vx_layernorm_gather.argtypes = [_vp, _i32, _i64, _vp, _i32, _i64, _vp, _vp, _i32, _i32, _f32, _i32, _i32,
+                                        _i32, _vp]
     lib.vx_patchify.argtypes = [_vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp]
     lib.vx_special_tokens.argtypes = [_vp, _vp, _i32, _i32, _i32, _i32, _vp]
     lib.vx_upsample_bilinear.argtypes = [_vp, _i32, _i32, _i32, _i32, _vp, _i32, _i32, _vp, _i32, _vp]
@@ -232,6 +235,22 @@ def layernorm(x, w, b, eps, out=None, out_dtype=torch.bfloat16):
     code = {torch.float32: 0, torch.bfloat16: 1}
     _check(_lib.vx_layernorm(_ptr(x), code[x.dtype], ldx, _ptr(out), code[out.dtype], ldy, _ptr(w), _ptr(b),
                              rows, cols, eps, _stream()), "vx_layernorm")
+    return out
+
+
+def layernorm_tokens(x, start: int, w, b, eps, out=None, out_dtype=torch.bfloat16):
+    """LayerNorm of x[:, start:, :] for x [F, T, C] contiguous, written as [F*(T-start), C] (no gather copy)."""
+    load_library()
+    if not x.is_cuda or not x.is_contiguous() or x.dim() != 3:
+        raise RuntimeError("layernorm_tokens: contiguous CUDA [F, T, C] required")
+    F_, T, C = x.shape
+    rows = F_ * (T - start)
+    if out is None:
+        out = torch.empty(rows, C, device=x.device, dtype=out_dtype)
+    ldy = _rowmajor(out, "out")
+    code = {torch.float32: 0, torch.bfloat16: 1}
+    _check(_lib.vx_layernorm_gather(_ptr(x), code[x.dtype], C, _ptr(out), code[out.dtype], ldy, _ptr(w), _ptr(b),
+                                    rows, C, eps, T - start, T, start, _stream()), "vx_layernorm_gather")
     return out
 
 
