@@ -36,11 +36,12 @@ constexpr int GEMM_BK = 64;
 constexpr int GEMM_THREADS = 384;  // w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4..w11 epilogue
 constexpr int GEMM_EPI_WARPS = 8;  // two warps per TMEM lane quarter, each owning half of the tile columns
 
-template <int BN>
+template <int BN, bool CG2 = false>
 struct GemmCfg {
-  static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
+  // CG2 (CTA pair, cta_group::2): each CTA stages its 128 A rows and half of the B tile
+  static constexpr int STAGES = CG2 ? 6 : (BN == 256 ? 4 : (BN == 128 ? 6 : 8));
   static constexpr uint32_t A_BYTES = GEMM_BM * GEMM_BK * 2;
-  static constexpr uint32_t B_BYTES = BN * GEMM_BK * 2;
+  static constexpr uint32_t B_BYTES = (CG2 ? BN / 2 : BN) * GEMM_BK * 2;
   static constexpr uint32_t SMEM = STAGES * (A_BYTES + B_BYTES) + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr uint32_t TMEM_COLS = 2 * BN;
 };
@@ -344,11 +345,16 @@ VX_DEVICE void epi_headout(const GemmArgs& a, const PixInfo& pi, const uint32_t*
 // MC: clusters of 2 CTAs on adjacent M tiles (same N tile); each CTA TMA-loads half of the
 // B tile and multicasts it to both, halving the per-SM L2->SMEM traffic of the main loop
 // (a 128x256 tile needs ~94 B/clk/SM from L2 otherwise — above the chip's L2 throughput).
-template <int BN, int EPI, int HD, bool MC>
+// CG2: CTA pairs with cta_group::2 MMAs: a pair computes a 256 x BN tile; each CTA TMA-loads its
+// 128 A rows and half of the B tile into its own smem (completion on the leader's barrier), the
+// leader issues M = 256 MMAs reading both CTAs' smem, and each CTA's TMEM receives its 128 rows.
+// Per-SM smem operand traffic per MMA drops from (128 + BN) to (128 + BN/2) rows.
+template <int BN, int EPI, int HD, bool MC, bool CG2 = false>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const GemmArgs args) {
-  using Cfg = GemmCfg<BN>;
+  using Cfg = GemmCfg<BN, CG2>;
+  constexpr bool PAIRED = MC || CG2;
   constexpr int STAGES = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -367,14 +373,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int num_m = (M + GEMM_BM - 1) / GEMM_BM;
   const int kblocks = K / GEMM_BK;
   // work decomposition: MC clusters walk (M-tile pair, N tile) units; otherwise single tiles
-  const uint32_t crank = MC ? cluster_ctarank() : 0;
-  const int units = MC ? ((num_m + 1) / 2) * num_n : num_m * num_n;
-  const int unit0 = MC ? int(blockIdx.x >> 1) : int(blockIdx.x);
-  const int ustep = MC ? int(gridDim.x >> 1) : int(gridDim.x);
+  const uint32_t crank = PAIRED ? cluster_ctarank() : 0;
+  const int units = PAIRED ? ((num_m + 1) / 2) * num_n : num_m * num_n;
+  const int unit0 = PAIRED ? int(blockIdx.x >> 1) : int(blockIdx.x);
+  const int ustep = PAIRED ? int(gridDim.x >> 1) : int(gridDim.x);
   auto tile_mn = [&](int u, int& m_blk, int& n_blk) {
     const int mu = u / num_n;
     n_blk = u - mu * num_n;
-    m_blk = MC ? 2 * mu + int(crank) : mu;
+    m_blk = PAIRED ? 2 * mu + int(crank) : mu;
   };
 
   if (warp == 0 && elect_one()) {
@@ -386,14 +392,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], GEMM_EPI_WARPS);
+      // CG2: the leader's accumulator is released by both CTAs' epilogue warps
+      mbar_init(&tempty[s], CG2 ? 2 * GEMM_EPI_WARPS : GEMM_EPI_WARPS);
     }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  if (warp == 2) {
+    if constexpr (CG2) tmem_alloc_cg2(tmem_slot, Cfg::TMEM_COLS);
+    else tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  }
   tc_fence_before();
   __syncthreads();
-  if constexpr (MC) cluster_sync();  // peer barriers initialised before any multicast / remote arrive
+  if constexpr (PAIRED) cluster_sync();  // peer barriers initialised before any multicast / remote arrive
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -402,18 +412,28 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       const uint64_t pol_b = policy_evict_last();
       int stage = 0;
       uint32_t phase = 0;
+      [[maybe_unused]] const uint64_t pol_a = policy_evict_normal();
       for (int u = unit0; u < units; u += ustep) {
         int m_blk, n_blk;
         tile_mn(u, m_blk, n_blk);
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], Cfg::A_BYTES + Cfg::B_BYTES);
           int a_col = kb * GEMM_BK, a_row = m_blk * GEMM_BM;
           if (args.conv_cin_blocks > 0) {  // implicit 3x3 conv: tap t shifts the padded-grid row
             const int t = kb / args.conv_cin_blocks;
             a_col = (kb - t * args.conv_cin_blocks) * GEMM_BK;
             a_row += (t / 3) * args.conv_w2 + (t % 3);
           }
+          if constexpr (CG2) {  // both CTAs' halves complete on the leader's full barrier
+            if (crank == 0) mbar_expect_tx(&full[stage], 2 * (Cfg::A_BYTES + Cfg::B_BYTES));
+            const uint32_t full0 = mapa_shared(smem_u32(&full[stage]), 0);
+            tma_load_2d_cg2(sA + stage * Cfg::A_BYTES, &tmA, full0, a_col, a_row, pol_a);
+            tma_load_2d_cg2(sB + stage * Cfg::B_BYTES, &tmB, full0, kb * GEMM_BK, n_blk * BN + int(crank) * (BN / 2),
+                            pol_b);
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            continue;
+          }
+          mbar_expect_tx(&full[stage], Cfg::A_BYTES + Cfg::B_BYTES);
           tma_load_2d(sA + stage * Cfg::A_BYTES, &tmA, &full[stage], a_col, a_row);
           if constexpr (MC) {  // my half of the B tile, multicast to both CTAs of the pair
             tma_load_2d_mc(sB + stage * Cfg::B_BYTES + crank * (Cfg::B_BYTES / 2), &tmB, &full[stage], kb * GEMM_BK,
@@ -426,8 +446,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (elect_one()) {
-      constexpr uint32_t idesc = make_idesc_bf16(GEMM_BM, BN, 0, 0);
+    if (CG2 && crank != 0) {
+      // the pair leader issues every MMA of the pair
+    } else if (elect_one()) {
+      constexpr uint32_t idesc = make_idesc_bf16(CG2 ? 2 * GEMM_BM : GEMM_BM, BN, 0, 0);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -443,14 +465,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           const uint32_t b0 = smem_u32(sB + stage * Cfg::B_BYTES);
 #pragma unroll
           for (int k = 0; k < GEMM_BK / 16; ++k) {
-            mma_ss(d_tmem, make_sdesc(a0 + k * 32, 16, 1024, 2), make_sdesc(b0 + k * 32, 16, 1024, 2), idesc,
-                   (kb | k) != 0);
+            if constexpr (CG2)
+              mma_ss_cg2(d_tmem, make_sdesc(a0 + k * 32, 16, 1024, 2), make_sdesc(b0 + k * 32, 16, 1024, 2), idesc,
+                         (kb | k) != 0);
+            else
+              mma_ss(d_tmem, make_sdesc(a0 + k * 32, 16, 1024, 2), make_sdesc(b0 + k * 32, 16, 1024, 2), idesc,
+                     (kb | k) != 0);
           }
-          if constexpr (MC) mma_commit_mc(&empty[stage], 0x3);  // stage free in both CTAs' producers
+          if constexpr (CG2) mma_commit_cg2_mc(&empty[stage], 0x3);  // stage free in both CTAs
+          else if constexpr (MC) mma_commit_mc(&empty[stage], 0x3);  // stage free in both CTAs' producers
           else mma_commit(&empty[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        mma_commit(&tfull[acc]);
+        if constexpr (CG2) mma_commit_cg2_mc(&tfull[acc], 0x3);  // both CTAs' epilogues
+        else mma_commit(&tfull[acc]);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
@@ -507,23 +535,27 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if constexpr (CG2) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));  // the leader's barrier
+        else mbar_arrive(&tempty[acc]);
+      }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   }
   tc_fence_before();
   __syncthreads();
-  if constexpr (MC) cluster_sync();  // no CTA leaves while its peer may still multicast / arrive
+  if constexpr (PAIRED) cluster_sync();  // no CTA leaves while its peer may still multicast / arrive
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+    if constexpr (CG2) tmem_dealloc_cg2(tmem_base, Cfg::TMEM_COLS);
+    else tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
   }
 }
 
-template <int BN, int EPI, int HD, bool MC = false>
+template <int BN, int EPI, int HD, bool MC = false, bool CG2 = false>
 static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& args, cudaStream_t st) {
-  using Cfg = GemmCfg<BN>;
-  auto kern = gemm_kernel<BN, EPI, HD, MC>;
+  using Cfg = GemmCfg<BN, CG2>;
+  auto kern = gemm_kernel<BN, EPI, HD, MC, CG2>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
@@ -531,7 +563,7 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmA
     attr_set = true;
   }
   const int num_m = (args.M + GEMM_BM - 1) / GEMM_BM, num_n = (args.N + BN - 1) / BN;
-  if constexpr (MC) {
+  if constexpr (MC || CG2) {
     const int units = ((num_m + 1) / 2) * num_n;
     const int clusters = units < num_sms() / 2 ? units : num_sms() / 2;
     cudaLaunchConfig_t cfg = {};
@@ -557,19 +589,19 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmA
   return VX_OK;
 }
 
-template <int BN, bool MC = false>
+template <int BN, bool MC = false, bool CG2 = false>
 static int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, cudaStream_t st) {
   switch (epi) {
-    case VX_EPI_BF16: return launch_gemm<BN, VX_EPI_BF16, 0, MC>(ta, tb, a, st);
-    case VX_EPI_GELU: return launch_gemm<BN, VX_EPI_GELU, 0, MC>(ta, tb, a, st);
-    case VX_EPI_RESID: return launch_gemm<BN, VX_EPI_RESID, 0, MC>(ta, tb, a, st);
-    case VX_EPI_PATCH: return launch_gemm<BN, VX_EPI_PATCH, 0, MC>(ta, tb, a, st);
-    case VX_EPI_F32: return launch_gemm<BN, VX_EPI_F32, 0, MC>(ta, tb, a, st);
-    case VX_EPI_SPATIAL: return launch_gemm<BN, VX_EPI_SPATIAL, 0, MC>(ta, tb, a, st);
-    case VX_EPI_HEADOUT: return launch_gemm<BN, VX_EPI_HEADOUT, 0, MC>(ta, tb, a, st);
+    case VX_EPI_BF16: return launch_gemm<BN, VX_EPI_BF16, 0, MC, CG2>(ta, tb, a, st);
+    case VX_EPI_GELU: return launch_gemm<BN, VX_EPI_GELU, 0, MC, CG2>(ta, tb, a, st);
+    case VX_EPI_RESID: return launch_gemm<BN, VX_EPI_RESID, 0, MC, CG2>(ta, tb, a, st);
+    case VX_EPI_PATCH: return launch_gemm<BN, VX_EPI_PATCH, 0, MC, CG2>(ta, tb, a, st);
+    case VX_EPI_F32: return launch_gemm<BN, VX_EPI_F32, 0, MC, CG2>(ta, tb, a, st);
+    case VX_EPI_SPATIAL: return launch_gemm<BN, VX_EPI_SPATIAL, 0, MC, CG2>(ta, tb, a, st);
+    case VX_EPI_HEADOUT: return launch_gemm<BN, VX_EPI_HEADOUT, 0, MC, CG2>(ta, tb, a, st);
     case VX_EPI_QKV:
-      if (a.ep.head_dim == 64) return launch_gemm<BN, VX_EPI_QKV, 64, MC>(ta, tb, a, st);
-      if (a.ep.head_dim == 32) return launch_gemm<BN, VX_EPI_QKV, 32, MC>(ta, tb, a, st);
+      if (a.ep.head_dim == 64) return launch_gemm<BN, VX_EPI_QKV, 64, MC, CG2>(ta, tb, a, st);
+      if (a.ep.head_dim == 32) return launch_gemm<BN, VX_EPI_QKV, 32, MC, CG2>(ta, tb, a, st);
       set_error("vx_gemm: qkv epilogue needs head_dim 32 or 64 (got %d)", a.ep.head_dim);
       return VX_E_ARG;
   }
@@ -577,13 +609,14 @@ static int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, c
   return VX_E_ARG;
 }
 
-// B-multicast clusters for the large 256-wide-N GEMMs (enough M tiles to pair up)
-static bool use_multicast(int BN, int M) {
+// CTA pairs for the large 256-wide-N GEMMs (enough M tiles to pair up): 1 = B-tile multicast
+// with per-CTA M = 128 MMAs, 2 = cta_group::2 M = 256 MMAs
+static int pair_mode(int BN, int M) {
   static int env = [] {
-    const char* e = getenv("VX_GEMM_MC");  // diagnostic: 0 disables the B-tile multicast
-    return e ? atoi(e) : 1;
+    const char* e = getenv("VX_GEMM_PAIR");  // diagnostic: 0 single CTAs, 1 multicast pairs, 2 MMA pairs
+    return e ? atoi(e) : 2;
   }();
-  return env && BN == 256 && M >= 8 * GEMM_BM;
+  return (BN == 256 && M >= 8 * GEMM_BM) ? env : 0;
 }
 
 }  // namespace vx
@@ -610,12 +643,13 @@ extern "C" int vx_gemm(int epi, const void* A, int64_t lda, const void* B, int64
   args.K = K;
   args.ep = *ep;
   const int BN = (N % 256 == 0 || N > 512) ? 256 : 128;
-  const bool mc = use_multicast(BN, M);
+  const int pm = pair_mode(BN, M);
   CUtensorMap ta, tb;
   if (!make_tmap_2d_bf16(&ta, A, M, K, lda, GEMM_BM, GEMM_BK, 128)) return VX_E_ARG;
-  if (!make_tmap_2d_bf16(&tb, B, N, K, ldb, mc ? BN / 2 : BN, GEMM_BK, 128)) return VX_E_ARG;
+  if (!make_tmap_2d_bf16(&tb, B, N, K, ldb, pm ? BN / 2 : BN, GEMM_BK, 128)) return VX_E_ARG;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if (mc) return dispatch_epi<256, true>(epi, ta, tb, args, st);
+  if (pm == 2) return dispatch_epi<256, false, true>(epi, ta, tb, args, st);
+  if (pm) return dispatch_epi<256, true>(epi, ta, tb, args, st);
   return BN == 256 ? dispatch_epi<256>(epi, ta, tb, args, st) : dispatch_epi<128>(epi, ta, tb, args, st);
 }
 
@@ -651,13 +685,14 @@ extern "C" int vx_gemm_spatial(const void* A, const void* B, int N, int K, const
   args.M = int(rows);
   const int BN = sp->head_odim > 0 ? 32 : ((N % 256 == 0 || N > 512) ? 256 : 128);
   const int64_t lda = sp->conv3x3 ? K / 9 : K;
-  const bool mc = use_multicast(BN, int(rows));
+  const int pm = pair_mode(BN, int(rows));
   CUtensorMap ta, tb;
   if (!make_tmap_2d_bf16(&ta, A, rows, lda, lda, GEMM_BM, GEMM_BK, 128)) return VX_E_ARG;
-  if (!make_tmap_2d_bf16(&tb, B, N, K, K, mc ? BN / 2 : BN, GEMM_BK, 128)) return VX_E_ARG;
+  if (!make_tmap_2d_bf16(&tb, B, N, K, K, pm ? BN / 2 : BN, GEMM_BK, 128)) return VX_E_ARG;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int epi = sp->head_odim > 0 ? VX_EPI_HEADOUT : VX_EPI_SPATIAL;
   if (BN == 32) return launch_gemm<32, VX_EPI_HEADOUT, 0>(ta, tb, args, st);  // N == 32 output head
-  if (mc) return launch_gemm<256, VX_EPI_SPATIAL, 0, true>(ta, tb, args, st);
+  if (pm == 2) return launch_gemm<256, VX_EPI_SPATIAL, 0, false, true>(ta, tb, args, st);
+  if (pm) return launch_gemm<256, VX_EPI_SPATIAL, 0, true>(ta, tb, args, st);
   return BN == 256 ? dispatch_epi<256>(epi, ta, tb, args, st) : dispatch_epi<128>(epi, ta, tb, args, st);
 }

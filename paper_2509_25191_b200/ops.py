@@ -13,7 +13,8 @@ from pathlib import Path
 
 import torch
 
-_LIB_PATH = Path(__file__).resolve().parent / "libvx.so"
+# VX_LIB: diagnostic override (A/B-testing a second build of the same library)
+_LIB_PATH = Path(os.environ.get("VX_LIB", str(Path(__file__).resolve().parent / "libvx.so")))
 
 EPI_BF16, EPI_GELU, EPI_RESID, EPI_QKV, EPI_PATCH, EPI_F32 = range(6)
 
