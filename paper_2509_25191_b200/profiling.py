@@ -17,11 +17,13 @@ class PhaseTimer:
     def phase(self, name: str):
         s = torch.cuda.Event(enable_timing=True)
         e = torch.cuda.Event(enable_timing=True)
+        torch.cuda.nvtx.range_push(name)  # named ranges for nsys / ncu --nvtx
         s.record()
         try:
             yield
         finally:
             e.record()
+            torch.cuda.nvtx.range_pop()
             self.events[name].append((s, e))
 
     def summary(self):
