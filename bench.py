@@ -258,7 +258,6 @@ def main():
         outs = None
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
-        h2d = host.numel() * 4
         d2h = 0
         keys = ["pose_enc", "depth", "depth_conf", "world_points", "world_points_conf"]
         for it in range(args.steps + 1):
@@ -267,10 +266,11 @@ def main():
             torch.cuda.synchronize()
             if it == 1:
                 e0.record()
-            out = model(host)
+            out = model(host)  # each rank copies only its frames (VGGT._local slices the host batch)
             if outs is None:
                 outs = {k: torch.empty(out[k].shape, dtype=out[k].dtype, pin_memory=True) for k in keys}
                 d2h = sum(v.numel() * v.element_size() for v in outs.values())
+                h2d = out["images"].numel() * 4
             for k in keys:
                 outs[k].copy_(out[k], non_blocking=True)
             del out
@@ -281,8 +281,11 @@ def main():
             tt = torch.tensor([ems], device="cuda")
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             ems = tt.item()
-        e2e = {"value": S * args.steps / (ems / 1000.0), "unit": "views/s", "h2d_bytes_per_step": h2d // world
-               if world > 1 else h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ems / args.steps}
+            nb = torch.tensor([h2d, d2h], device="cuda", dtype=torch.float64)  # whole-job bytes
+            dist.all_reduce(nb, op=dist.ReduceOp.SUM)
+            h2d, d2h = int(nb[0].item()), int(nb[1].item())
+        e2e = {"value": S * args.steps / (ems / 1000.0), "unit": "views/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": ems / args.steps}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -81,7 +81,7 @@ class FrameShardedRing:
             raise ValueError(f"{S} views cannot be sharded over {self.world} ranks")
         self.split = frame_split(S, self.world)
         lo, hi = self.split[self.rank]
-        return images[lo:hi].contiguous(), lo, S
+        return images[lo:hi], lo, S  # a view: a host batch stays (pinned) host memory until the copy
 
     def tokens_of(self, r: int) -> int:
         lo, hi = self.split[r]

@@ -54,25 +54,26 @@ class VGGT:
             self.ring = FrameShardedRing(self.cfg, self.device)
 
     # -- helpers ------------------------------------------------------------
-    def _prep(self, images: torch.Tensor) -> torch.Tensor:
+    def _local(self, images: torch.Tensor, sharded_input: bool):
+        """(this rank's images on the device, global frame offset, global S).
+
+        Host inputs are sliced to the rank's frames BEFORE the host-to-device copy, so every rank
+        moves only its own views over PCIe."""
         if images.dim() == 5:
             if images.shape[0] != 1:
                 raise ValueError("batch size B must be 1 (frames are the batch dimension)")
             images = images[0]
         if images.dim() != 4 or images.shape[1] != 3:
             raise ValueError(f"images must be (S,3,H,W) or (1,S,3,H,W); got {tuple(images.shape)}")
-        return images.to(self.device, torch.float32, non_blocking=True).contiguous()
-
-    def _local(self, images, sharded_input: bool):
-        """(local images, global frame offset, global S) for this rank."""
         if self.ring is None:
-            return images, 0, images.shape[0]
-        return self.ring.local_frames(images, sharded_input)
+            local, f0, S = images, 0, images.shape[0]
+        else:
+            local, f0, S = self.ring.local_frames(images, sharded_input)
+        return local.to(self.device, torch.float32, non_blocking=True).contiguous(), f0, S
 
     # -- API ------------------------------------------------------------------
     @torch.no_grad()
     def aggregator(self, images: torch.Tensor, sharded_input: bool = False) -> Tuple[Dict[int, torch.Tensor], int]:
-        images = self._prep(images)
         local, f0, S = self._local(images, sharded_input)
         kept = self._aggregate(local, f0)
         return {i: t[None] for i, t in kept.items()}, self.cfg.patch_start_idx
@@ -87,7 +88,6 @@ class VGGT:
     @torch.no_grad()
     def forward(self, images: torch.Tensor, sharded_input: bool = False) -> Dict[str, torch.Tensor]:
         cfg = self.cfg
-        images = self._prep(images)
         local, f0, S = self._local(images, sharded_input)
         kept = self._aggregate(local, f0)
         Sl = local.shape[0]
