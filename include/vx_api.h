@@ -90,6 +90,14 @@ int vx_gemm(int epi, const void* A, int64_t lda, const void* B, int64_t ldb, int
  * D in {32, 64, 128} (128: camera-head trunk); scale = 1/sqrt(D). */
 int vx_attention(const void* q, const void* k, const void* v, void* out, int64_t ldo, float* lse,
                  int D, int H, int nseq, int Lq, int Lk, int64_t Tq, int64_t Tk, void* stream);
+/* One K/V-ring step of frame-sharded global attention with the log-sum-exp merge
+ * fused into the epilogue: mode 1 (first block) writes o_acc = O_blk (fp32 [Tq, ld_acc]) and
+ * lse_acc = lse_blk ([H, Tq]); mode 2 merges: o_acc = w_a o_acc + w_b O_blk, lse_acc =
+ * logaddexp(lse_acc, lse_blk); mode 3 merges and writes the final bf16 `out` (row stride ldo)
+ * instead of o_acc.  Same shapes and head layout as vx_attention. */
+int vx_attention_merge(const void* q, const void* k, const void* v, int mode, float* o_acc, int64_t ld_acc,
+                       float* lse_acc, void* out, int64_t ldo, int D, int H, int nseq, int Lq, int Lk,
+                       int64_t Tq, int64_t Tk, void* stream);
 
 /* LayerNorm over the last dim (cols): y = (x - mean) * rstd * w + b.
  * x_dtype / y_dtype: 0 = fp32, 1 = bf16.  w/b may be NULL (no affine). (norm1/norm2, a5) */

@@ -36,6 +36,11 @@ namespace vx {
 struct AttnArgs {
   int H, nseq, Lq, Lk;
   int64_t Tq, Tk;
+  // ring steps (vx_attention_merge): 0 plain; 1 first block -> o_acc / lse; 2 merge into o_acc / lse;
+  // 3 merge and write the final bf16 output
+  int merge;
+  float* o_acc;
+  int64_t ld_acc;
   int q_blocks, kv_tiles, units;
   float scale_log2;
   __nv_bfloat16* out;
@@ -464,15 +469,55 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
       if (q_local < a.Lq) {
         const float inv = 1.0f / l_run;
         const int64_t orow = (int64_t)s * a.Lq + q_local;
-        uint4* dst = reinterpret_cast<uint4*>(a.out + orow * a.ldo + h * D);
+        const float lse_new = (m_run + __log2f(l_run)) * 0.69314718055994531f;
+        if (a.merge == 0) {
+          uint4* dst = reinterpret_cast<uint4*>(a.out + orow * a.ldo + h * D);
 #pragma unroll
-        for (int c = 0; c < D / 8; ++c) {
+          for (int c = 0; c < D / 8; ++c) {
 #define VX_O(i) (__uint_as_float(orr[8 * c + i]) * inv)
-          dst[c] = make_uint4(pack_bf16(VX_O(0), VX_O(1)), pack_bf16(VX_O(2), VX_O(3)),
-                              pack_bf16(VX_O(4), VX_O(5)), pack_bf16(VX_O(6), VX_O(7)));
+            dst[c] = make_uint4(pack_bf16(VX_O(0), VX_O(1)), pack_bf16(VX_O(2), VX_O(3)),
+                                pack_bf16(VX_O(4), VX_O(5)), pack_bf16(VX_O(6), VX_O(7)));
 #undef VX_O
+          }
+          if (a.lse) a.lse[h * a.Tq + orow] = lse_new;
+        } else {
+          // ring step: log-sum-exp merge with the running (O, lse) of the blocks seen so far
+          float* acc = a.o_acc + orow * a.ld_acc + h * D;
+          float* lacc = a.lse + h * a.Tq + orow;
+          float wa = 0.f, wb = inv, lse_out = lse_new;
+          if (a.merge >= 2) {
+            const float lp = *lacc;
+            const float mx = fmaxf(lp, lse_new);
+            const float ea = __expf(lp - mx), eb = __expf(lse_new - mx);
+            const float rs = 1.0f / (ea + eb);
+            wa = ea * rs;
+            wb = eb * rs * inv;
+            lse_out = mx + __logf(ea + eb);
+          }
+          if (a.merge == 3) {
+            uint4* dst = reinterpret_cast<uint4*>(a.out + orow * a.ldo + h * D);
+            const float4* a4 = reinterpret_cast<const float4*>(acc);
+#pragma unroll
+            for (int c = 0; c < D / 8; ++c) {
+              const float4 p0 = a4[2 * c], p1 = a4[2 * c + 1];
+#define VX_M(i, pv) (wa * (pv) + wb * __uint_as_float(orr[8 * c + i]))
+              dst[c] = make_uint4(pack_bf16(VX_M(0, p0.x), VX_M(1, p0.y)), pack_bf16(VX_M(2, p0.z), VX_M(3, p0.w)),
+                                  pack_bf16(VX_M(4, p1.x), VX_M(5, p1.y)), pack_bf16(VX_M(6, p1.z), VX_M(7, p1.w)));
+#undef VX_M
+            }
+          } else {
+            float4* a4 = reinterpret_cast<float4*>(acc);
+#pragma unroll
+            for (int c = 0; c < D / 4; ++c) {
+              const float4 p = a.merge >= 2 ? a4[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+              a4[c] = make_float4(wa * p.x + wb * __uint_as_float(orr[4 * c + 0]),
+                                  wa * p.y + wb * __uint_as_float(orr[4 * c + 1]),
+                                  wa * p.z + wb * __uint_as_float(orr[4 * c + 2]),
+                                  wa * p.w + wb * __uint_as_float(orr[4 * c + 3]));
+            }
+          }
+          *lacc = lse_out;
         }
-        if (a.lse) a.lse[h * a.Tq + orow] = (m_run + __log2f(l_run)) * 0.69314718055994531f;
       }
     }
   }
@@ -508,18 +553,19 @@ static int launch_fmha(const void* q, const void* k, const void* v, AttnArgs arg
   return VX_OK;
 }
 
-}  // namespace vx
-
-extern "C" int vx_attention(const void* q, const void* k, const void* v, void* out, int64_t ldo, float* lse, int D,
-                            int H, int nseq, int Lq, int Lk, int64_t Tq, int64_t Tk, void* stream) {
-  using namespace vx;
-  VX_CHECK_ARG(q && k && v && out, "vx_attention: null pointer");
+static int attention_impl(const void* q, const void* k, const void* v, void* out, int64_t ldo, float* lse, int D,
+                          int H, int nseq, int Lq, int Lk, int64_t Tq, int64_t Tk, int merge, float* o_acc,
+                          int64_t ld_acc, void* stream) {
+  VX_CHECK_ARG(q && k && v, "vx_attention: null pointer");
+  VX_CHECK_ARG(merge == 1 || merge == 2 || out, "vx_attention: null out");
   VX_CHECK_ARG(D == 32 || D == 64 || D == 128, "vx_attention: head_dim %d unsupported (32, 64, 128)", D);
   VX_CHECK_ARG(H > 0 && nseq > 0 && Lq > 0 && Lk > 0, "vx_attention: empty problem");
   VX_CHECK_ARG((int64_t)nseq * Lq <= Tq && (int64_t)nseq * Lk <= Tk, "vx_attention: sequences exceed buffers");
   VX_CHECK_ARG((int64_t)H * Tq + 512 < (1ll << 31) && (int64_t)H * Tk + 512 < (1ll << 31),
                "vx_attention: too many rows for 32-bit TMA coordinates");
-  VX_CHECK_ARG(ldo >= (int64_t)H * D && ldo % 8 == 0, "vx_attention: bad ldo");
+  VX_CHECK_ARG(!out || (ldo >= (int64_t)H * D && ldo % 8 == 0), "vx_attention: bad ldo");
+  VX_CHECK_ARG(merge == 0 || (o_acc && lse && ld_acc >= (int64_t)H * D && ld_acc % 4 == 0),
+               "vx_attention: merge needs o_acc [Tq, >= H*D] fp32 and lse");
   AttnArgs a;
   a.H = H;
   a.nseq = nseq;
@@ -527,6 +573,9 @@ extern "C" int vx_attention(const void* q, const void* k, const void* v, void* o
   a.Lk = Lk;
   a.Tq = Tq;
   a.Tk = Tk;
+  a.merge = merge;
+  a.o_acc = o_acc;
+  a.ld_acc = ld_acc;
   // q_blocks / kv_tiles / units depend on the kernel configuration: set in launch_fmha
   a.scale_log2 = (1.0f / sqrtf(float(D))) * 1.4426950408889634f;
   a.out = reinterpret_cast<__nv_bfloat16*>(out);
@@ -560,4 +609,19 @@ extern "C" int vx_attention(const void* q, const void* k, const void* v, void* o
   }
   if (D == 128) return launch_fmha<128, 2>(q, k, v, a, st);
   return launch_fmha<32, 2>(q, k, v, a, st);
+}
+
+}  // namespace vx
+
+extern "C" int vx_attention(const void* q, const void* k, const void* v, void* out, int64_t ldo, float* lse, int D,
+                            int H, int nseq, int Lq, int Lk, int64_t Tq, int64_t Tk, void* stream) {
+  return vx::attention_impl(q, k, v, out, ldo, lse, D, H, nseq, Lq, Lk, Tq, Tk, 0, nullptr, 0, stream);
+}
+
+extern "C" int vx_attention_merge(const void* q, const void* k, const void* v, int mode, float* o_acc, int64_t ld_acc,
+                                  float* lse_acc, void* out, int64_t ldo, int D, int H, int nseq, int Lq, int Lk,
+                                  int64_t Tq, int64_t Tk, void* stream) {
+  VX_CHECK_ARG(mode >= 1 && mode <= 3, "vx_attention_merge: mode must be 1 (first), 2 (merge) or 3 (final)");
+  return vx::attention_impl(q, k, v, mode == 3 ? out : nullptr, ldo, lse_acc, D, H, nseq, Lq, Lk, Tq, Tk, mode, o_acc,
+                            ld_acc, stream);
 }

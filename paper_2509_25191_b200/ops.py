@@ -58,7 +58,7 @@ class GaProblem(ctypes.Structure):
     ]
 
 
-EXPORTED_SYMBOLS = ("vx_gemm", "vx_attention", "vx_layernorm", "vx_layernorm_gather", "vx_patchify",
+EXPORTED_SYMBOLS = ("vx_gemm", "vx_attention", "vx_attention_merge", "vx_layernorm", "vx_layernorm_gather", "vx_patchify",
                     "vx_special_tokens",
                     "vx_upsample_bilinear", "vx_gemm_spatial", "vx_epipolar_residuals",
                     "vx_epipolar_accumulate", "vx_ga_decode", "vx_ga_residuals", "vx_ga_loss_grad",
@@ -80,6 +80,8 @@ def load_library(path: os.PathLike | None = None) -> ctypes.CDLL:
     lib = ctypes.CDLL(str(p))
     lib.vx_gemm.argtypes = [_i32, _vp, _i64, _vp, _i64, _i32, _i32, _i32, ctypes.POINTER(Epilogue), _vp]
     lib.vx_attention.argtypes = [_vp, _vp, _vp, _vp, _i64, _vp, _i32, _i32, _i32, _i32, _i32, _i64, _i64, _vp]
+    lib.vx_attention_merge.argtypes = [_vp, _vp, _vp, _i32, _vp, _i64, _vp, _vp, _i64, _i32, _i32, _i32, _i32, _i32,
+                                       _i64, _i64, _vp]
     lib.vx_layernorm.argtypes = [_vp, _i32, _i64, _vp, _i32, _i64, _vp, _vp, _i32, _i32, _f32, _vp]
     lib.vx_layernorm_gather.argtypes = [_vp, _i32, _i64, _vp, _i32, _i64, _vp, _vp, _i32, _i32, _f32, _i32, _i32,
                                         _i32, _vp]
@@ -222,6 +224,27 @@ def attention(q, k, v, out, nseq: int, Lq: int, Lk: int, lse=None):
     _check(_lib.vx_attention(_ptr(q), _ptr(k), _ptr(v), _ptr(out), ldo, _ptr(lse), D, H, nseq, Lq, Lk,
                              Tq, Tk, _stream()), "vx_attention")
     return out
+
+
+def attention_merge(q, k, v, mode: int, o_acc, lse_acc, out=None, nseq: int = 1, Lq: int = 0, Lk: int = 0):
+    """One ring step with the fused LSE merge (vx_attention_merge): mode 1 first / 2 merge / 3 final (-> out)."""
+    load_library()
+    for t, nm in ((q, "q"), (k, "k"), (v, "v")):
+        _req(t, torch.bfloat16, nm)
+        if not t.is_contiguous():
+            raise ValueError(f"attention_merge: {nm} must be contiguous")
+    _req(o_acc, torch.float32, "o_acc")
+    _req(lse_acc, torch.float32, "lse_acc")
+    H, Tq, D = q.shape
+    Tk = k.shape[1]
+    ld_acc = _rowmajor(o_acc, "o_acc")
+    ldo = 0
+    if mode == 3:
+        _req(out, torch.bfloat16, "out")
+        ldo = _rowmajor(out, "out")
+    _check(_lib.vx_attention_merge(_ptr(q), _ptr(k), _ptr(v), mode, _ptr(o_acc), ld_acc, _ptr(lse_acc),
+                                   _ptr(out) if mode == 3 else None, ldo, D, H, nseq, Lq or Tq, Lk or Tk, Tq, Tk,
+                                   _stream()), "vx_attention_merge")
 
 
 def layernorm(x, w, b, eps, out=None, out_dtype=torch.bfloat16):

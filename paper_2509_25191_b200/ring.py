@@ -5,9 +5,10 @@ is per-frame locally (patch-embed, frame blocks, all GEMMs / norms of the global
 blocks, kept layers, DPT heads).  The only exchange on the data path is inside
 global attention: g-1 ring steps, each sending this rank's current K/V block
 (one packed [2, H, Tmax, d] bf16 buffer) to rank r+1 and receiving the next one
-from rank r-1 while the FMHA kernel works on the current block.  Each step
-yields (O_s, lse_s) for the local queries; they are merged in fp32 with the
-log-sum-exp rule.  Because RoPE positions are per frame and attention is
+from rank r-1 while the FMHA kernel works on the current block.  Each step's
+(O, lse) for the local queries is merged into a running fp32 (O, lse) with the
+log-sum-exp rule inside the FMHA epilogue (vx_attention_merge: no separate
+merge kernels; the last step writes the bf16 output).  Because RoPE positions are per frame and attention is
 non-causal, every step has identical work (no zig-zag needed).
 
 Every rank passes the full view batch (or its own slice); frame 0 carries the
@@ -61,6 +62,9 @@ class FrameShardedRing:
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+        # default: vx_attention_merge (LSE merge fused into the FMHA epilogue); injected functions are
+        # for the CPU (gloo) tests of the ring schedule
+        self.fused = partial_attention is None
         self.partial = partial_attention or _vx_partial
         self.merge = merge
         self.split: Optional[List[Tuple[int, int]]] = None
@@ -99,10 +103,14 @@ class FrameShardedRing:
         bufs = [torch.empty(2, H, Tmax, d, device=q.device, dtype=q.dtype) for _ in range(2)]
         bufs[0][0, :, :Tl].copy_(k)
         bufs[0][1, :, :Tl].copy_(v)
-        o_acc = torch.zeros(Tl, H * d, device=q.device, dtype=torch.float32)
-        lse_acc = torch.full((H, Tl), float("-inf"), device=q.device, dtype=torch.float32)
-        o_s = torch.empty(Tl, H * d, device=q.device, dtype=o.dtype)
-        lse_s = torch.empty(H, Tl, device=q.device, dtype=torch.float32)
+        if self.fused:
+            o_acc = torch.empty(Tl, H * d, device=q.device, dtype=torch.float32)
+            lse_acc = torch.empty(H, Tl, device=q.device, dtype=torch.float32)
+        else:
+            o_acc = torch.zeros(Tl, H * d, device=q.device, dtype=torch.float32)
+            lse_acc = torch.full((H, Tl), float("-inf"), device=q.device, dtype=torch.float32)
+            o_s = torch.empty(Tl, H * d, device=q.device, dtype=o.dtype)
+            lse_s = torch.empty(H, Tl, device=q.device, dtype=torch.float32)
         nxt, prv = (r + 1) % g, (r - 1) % g
         cur = 0
         for step in range(g):
@@ -115,12 +123,18 @@ class FrameShardedRing:
             Lk = self.tokens_of(src)
             kb = bufs[cur][0]
             vb = bufs[cur][1]
-            self.partial(q, kb, vb, o_s, lse_s, Tl, Lk)
-            self.merge(o_acc, lse_acc, o_s, lse_s)
+            if self.fused:  # one launch: partial attention + running log-sum-exp merge (+ final bf16 write)
+                from . import ops
+                mode = 1 if step == 0 else (3 if step == g - 1 else 2)
+                ops.attention_merge(q, kb, vb, mode, o_acc, lse_acc, out=o, Lq=Tl, Lk=Lk)
+            else:
+                self.partial(q, kb, vb, o_s, lse_s, Tl, Lk)
+                self.merge(o_acc, lse_acc, o_s, lse_s)
             for rq in reqs:
                 rq.wait()
             cur ^= 1
-        o.copy_(o_acc)
+        if not self.fused:
+            o.copy_(o_acc)
 
     # -- camera tokens -----------------------------------------------------
     def all_gather_frames(self, x: torch.Tensor) -> torch.Tensor:

@@ -332,3 +332,30 @@ def test_upsample_bilinear_matches_interpolate(ops):
         assert rel(out, ref) < 5e-3
         outp = ops.upsample_bilinear(x, (H, H), out_pad=True)
         assert rel(outp[:, 1:-1, 1:-1], ref - add.float()) < 5e-3
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shards", [[700], [300, 411], [513, 200, 333, 90]])
+def test_attention_ring_merge_matches_full(ops, shards):
+    # the ring's fused-merge steps (vx_attention_merge) over K/V shards == attention over all keys
+    H, Lq, D = 4, 600, 64
+    Lk = sum(shards)
+    q = _bf(H, Lq, D, seed=50)
+    k = _bf(H, Lk, D, seed=51)
+    v = _bf(H, Lk, D, seed=52)
+    ref, lse_ref = _sdpa_ref(q, k, v, 1, Lq, Lk)
+    o_acc = torch.empty(Lq, H * D, device="cuda")
+    lse = torch.empty(H, Lq, device="cuda")
+    out = torch.empty(Lq, H * D, device="cuda", dtype=torch.bfloat16)
+    off = 0
+    for i, n in enumerate(shards):
+        ks = k[:, off:off + n].contiguous()
+        vs = v[:, off:off + n].contiguous()
+        mode = 3 if i == len(shards) - 1 and i > 0 else (1 if i == 0 else 2)
+        if len(shards) == 1:
+            mode = 1
+        ops.attention_merge(q, ks, vs, mode, o_acc, lse, out=out, Lq=Lq, Lk=n)
+        off += n
+    got = o_acc if len(shards) == 1 else out
+    assert rel(got, ref) < 1e-2
+    assert (lse - lse_ref).abs().max().item() < 1e-2
