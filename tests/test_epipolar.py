@@ -44,6 +44,43 @@ def test_oracle_matches_reference_golden(mode):
         _check_pair(p, g, mode, e, nd, l, ws, G, sk, a, b)
 
 
+def _compiled_reference():
+    from oracle import build_ref
+    build_ref.build()  # no-op when the sources are absent or the binary is current
+    return build_ref.load()
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_oracle_matches_compiled_reference_kernel(mode):
+    """The restatement against the reference's own compiled Cython kernel (oracle/_ref, built from
+    pkg/src/epialign/_kernels_cy.pyx by oracle/build_ref.py): residuals bit-identical, sums to
+    rounding, on random workloads, degenerate lines and the dead zone."""
+    cy = _compiled_reference()
+    if cy is None:
+        pytest.skip("oracle/_ref not built (reference sources absent)")
+    assert cy.IMPL == "compiled"
+    rng = np.random.default_rng(11)
+    g = np.load(GOLD)
+    cases = [(F, xi, xj, w) for _, F, xi, xj, w, _ in _pairs(g)]
+    for _ in range(6):
+        F = rng.normal(size=(3, 3))
+        F /= np.linalg.norm(F)
+        k = int(rng.integers(1, 900))
+        cases.append((F, rng.uniform(0, 640, (k, 2)), rng.uniform(0, 480, (k, 2)), rng.uniform(0.1, 2, k)))
+    for F, xi, xj, w in cases:
+        F, xi, xj, w = (np.ascontiguousarray(x, dtype=np.float64) for x in (F, xi, xj, w))
+        e0, n0 = cy.pair_residuals(F, xi, xj, mode)
+        e1, n1 = R.pair_residuals(F, xi, xj, mode)
+        assert n0 == n1
+        assert np.array_equal(np.isnan(e0), np.isnan(e1))
+        assert np.array_equal(e0[~np.isnan(e0)], e1[~np.isnan(e1)])  # same formulas, same rounding
+        l0, ws0, G0, sk0 = cy.pair_accumulate(F, xi, xj, w, mode)
+        l1, ws1, G1, sk1 = R.pair_accumulate(F, xi, xj, w, mode)
+        assert sk0 == sk1
+        assert np.isclose(l0, l1, rtol=1e-12, atol=1e-300) and np.isclose(ws0, ws1, rtol=1e-12)
+        assert np.allclose(G0, G1, rtol=1e-9, atol=1e-12 * max(1.0, np.abs(G0).max()))
+
+
 @pytest.mark.skipif(not os.path.isdir(REF_SRC), reason="reference sources not mounted")
 @pytest.mark.parametrize("mode", [0, 1])
 def test_oracle_matches_reference_module_fresh(mode):
