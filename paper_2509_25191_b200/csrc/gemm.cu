@@ -44,6 +44,7 @@ struct GemmCfg {
   static constexpr uint32_t B_BYTES = (CG2 ? BN / 2 : BN) * GEMM_BK * 2;
   static constexpr uint32_t SMEM = STAGES * (A_BYTES + B_BYTES) + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr uint32_t TMEM_COLS = 2 * BN;
+  static_assert(SMEM <= 227 * 1024, "GEMM stage ring exceeds the 227 KB smem per CTA");
 };
 
 // ---------------------------------------------------------------------------
@@ -642,12 +643,24 @@ extern "C" int vx_gemm(int epi, const void* A, int64_t lda, const void* B, int64
   args.N = N;
   args.K = K;
   args.ep = *ep;
-  const int BN = (N % 256 == 0 || N > 512) ? 256 : 128;
+  // a single M tile (camera-head trunk, M = views) is bound by streaming the weights: 64-wide N
+  // tiles spread that over up to 4x more SMs than 256-wide ones
+  const bool small_m = M <= GEMM_BM && N % 64 == 0 && epi != VX_EPI_QKV && epi != VX_EPI_PATCH;
+  const int BN = small_m ? 64 : ((N % 256 == 0 || N > 512) ? 256 : 128);
   const int pm = pair_mode(BN, M);
   CUtensorMap ta, tb;
   if (!make_tmap_2d_bf16(&ta, A, M, K, lda, GEMM_BM, GEMM_BK, 128)) return VX_E_ARG;
   if (!make_tmap_2d_bf16(&tb, B, N, K, ldb, pm ? BN / 2 : BN, GEMM_BK, 128)) return VX_E_ARG;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (small_m) {
+    switch (epi) {
+      case VX_EPI_BF16: return launch_gemm<64, VX_EPI_BF16, 0>(ta, tb, args, st);
+      case VX_EPI_GELU: return launch_gemm<64, VX_EPI_GELU, 0>(ta, tb, args, st);
+      case VX_EPI_RESID: return launch_gemm<64, VX_EPI_RESID, 0>(ta, tb, args, st);
+      case VX_EPI_F32: return launch_gemm<64, VX_EPI_F32, 0>(ta, tb, args, st);
+      default: break;
+    }
+  }
   if (pm == 2) return dispatch_epi<256, false, true>(epi, ta, tb, args, st);
   if (pm) return dispatch_epi<256, true>(epi, ta, tb, args, st);
   return BN == 256 ? dispatch_epi<256>(epi, ta, tb, args, st) : dispatch_epi<128>(epi, ta, tb, args, st);
