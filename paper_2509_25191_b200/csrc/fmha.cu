@@ -102,6 +102,27 @@ VX_DEVICE void tmem_st_n(uint32_t taddr, const uint32_t* r) {
   if constexpr (N % 16 == 8) tmem_st8(taddr + N - 8, r + N - 8);
 }
 
+#ifdef VX_FMHA_TRACE
+// diagnostic build only (tools/trace_fmha.py): clock64 stamps of CTA 0's first unit
+__device__ unsigned long long* g_fmha_trace = nullptr;
+#define VX_TRACE(slot)                                                                    \
+  do {                                                                                    \
+    if (g_fmha_trace && blockIdx.x == 0 && (slot) >= 0) g_fmha_trace[(slot)] = clock64(); \
+  } while (0)
+#else
+#define VX_TRACE(slot) \
+  do {                 \
+  } while (0)
+#endif
+// trace slots: softmax tile t (lane 0 of its first warp), iteration j < 64, point k < 5:
+//   (t * 64 + j) * 8 + k; MMA thread: 4096 + (j * 4 + i) * 2 + {0: p_full seen, 1: S(j+1) committed}
+VX_DEVICE int trace_slot_sm(int unit_n, int wl, int lane, int tile, int j, int k) {
+  return (unit_n == 0 && wl == 0 && lane == 0 && j < 64) ? (tile * 64 + j) * 8 + k : -1;
+}
+VX_DEVICE int trace_slot_mma(int unit_n, int j, int i, int k) {
+  return (unit_n == 0 && j < 64) ? 4096 + (j * 4 + i) * 2 + k : -1;
+}
+
 template <bool B>
 struct BoolTag {
   static constexpr bool value = B;
@@ -277,11 +298,13 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
               for (int i = 0; i < NT; ++i) mbar_wait(&o_empty[i], (n & 1) ^ 1);
             for (int i = 0; i < NT; ++i) {
               mbar_wait(&p_full[i], pfull_ph);
+              VX_TRACE(trace_slot_mma(int(n), j, i, 0));
               tc_fence_after();
               issue_pv(i, vs, j > 0);
               if (has_next) {  // overwrites P_i(j): executes after PV_i(j) (tcgen05 issue order)
                 issue_qk(i, nks);
                 mma_commit(&s_full[i]);
+                VX_TRACE(trace_slot_mma(int(n), j, i, 1));
               } else {
                 mma_commit(&p_free[i]);  // last PV of the unit
               }
@@ -357,7 +380,8 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
     const float sl2 = a.scale_log2;
     const uint64_t SL2 = f2_pack(sl2, sl2);
     uint32_t sph = 0, pv_cnt = 0;
-    for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
+    [[maybe_unused]] int unit_n = 0;
+    for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++unit_n) {
       const int h = u / per_head;
       const int rem = u - h * per_head;
       const int s = rem / a.q_blocks;
@@ -366,7 +390,9 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
       float m_run = -INFINITY;
       float l_run = 0.f;
       for (int j = 0; j < nkv; ++j) {
+        VX_TRACE(trace_slot_sm(unit_n, wl, lane, tile, j, 0));
         mbar_wait(&s_full[tile], sph);
+        VX_TRACE(trace_slot_sm(unit_n, wl, lane, tile, j, 1));
         sph ^= 1;
         tc_fence_after();
         uint32_t sr[BKV];
@@ -400,6 +426,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
           const float alpha = need ? ex2(m_run - m_new) : 1.0f;
           if (need) m_run = m_new;
           const uint64_t NEGM = f2_pack(-m_run, -m_run);
+          VX_TRACE(trace_slot_sm(unit_n, wl, lane, tile, j, 2));
           uint64_t acc[4] = {0, 0, 0, 0};
           constexpr int NCHUNK = (BKV + 63) / 64;
 #pragma unroll
@@ -421,6 +448,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
               if constexpr (!SUMV) acc[c & 3] = f2_add(acc[c & 3], f2_pack(p0, p1));
               pk[c] = pack_bf16(p0, p1);
             }
+            VX_TRACE(trace_slot_sm(unit_n, wl, lane, tile, j, 3));
             if (!ALIAS && hf == 0 && j > 0) {  // P_i(j-1) consumed and O stable (waited after the first exps)
               mbar_wait(&p_free[tile], pv_cnt & 1);
               ++pv_cnt;
@@ -455,6 +483,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[tile]);
+        VX_TRACE(trace_slot_sm(unit_n, wl, lane, tile, j, 4));
       }
       mbar_wait(&p_free[tile], pv_cnt & 1);
       ++pv_cnt;
@@ -625,3 +654,10 @@ extern "C" int vx_attention_merge(const void* q, const void* k, const void* v, i
   return vx::attention_impl(q, k, v, mode == 3 ? out : nullptr, ldo, lse_acc, D, H, nseq, Lq, Lk, Tq, Tk, mode, o_acc,
                             ld_acc, stream);
 }
+
+#ifdef VX_FMHA_TRACE
+extern "C" int vx_fmha_set_trace(void* buf) {
+  cudaError_t e = cudaMemcpyToSymbol(vx::g_fmha_trace, &buf, sizeof(void*));
+  return e == cudaSuccess ? 0 : -2;
+}
+#endif
