@@ -243,7 +243,10 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    if (elect_one()) {
+    // the whole warp runs the (warp-uniform) issue loop and waits; one elected lane issues the
+    // tcgen05 ops, so descriptors and counters stay in uniform registers
+    const bool lead = elect_one();
+    {
       constexpr uint32_t idesc_qk = make_idesc_bf16(128, BKV, 0, 0);
       constexpr uint32_t idesc_pv = make_idesc_bf16(128, DO, 0, 1);
       const uint32_t q0 = smem_u32(sQ);
@@ -255,7 +258,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
           const uint32_t kstep = (k % KSTEPS_PER_PANEL) * 32;
           const uint32_t qoff = (k / KSTEPS_PER_PANEL) * Cfg::QPANEL_BYTES + kstep;
           const uint32_t koff = (k / KSTEPS_PER_PANEL) * Cfg::KVPANEL_BYTES + kstep;
-          mma_ss(tmem + Cfg::tS(i), make_sdesc(qs + qoff, 16, Cfg::SBO, Cfg::LAYOUT),
+          if (lead) mma_ss(tmem + Cfg::tS(i), make_sdesc(qs + qoff, 16, Cfg::SBO, Cfg::LAYOUT),
                  make_sdesc(ks + koff, 16, Cfg::SBO, Cfg::LAYOUT), idesc_qk, k > 0);
         }
       };
@@ -263,7 +266,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
       auto issue_pv = [&](int i, uint32_t vs, uint32_t acc) {
 #pragma unroll
         for (int kk = 0; kk < BKV / 16; ++kk)
-          mma_ts(tmem + Cfg::tO(i), tmem + Cfg::tP(i) + kk * 8,
+          if (lead) mma_ts(tmem + Cfg::tO(i), tmem + Cfg::tP(i) + kk * 8,
                  make_sdesc(vs + kk * 16 * Cfg::ROW_BYTES, Cfg::KVPANEL_BYTES, Cfg::SBO, Cfg::LAYOUT), idesc_pv,
                  (acc | kk) != 0);
       };
@@ -281,10 +284,10 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
             const uint32_t ks = smem_u32(sK + st * Cfg::KV_TILE_BYTES);
             for (int i = 0; i < NT; ++i) {
               issue_qk(i, ks);
-              mma_commit(&s_full[i]);
+              if (lead) mma_commit(&s_full[i]);
             }
-            mma_commit(&k_empty[st]);
-            if (nkv == 1) mma_commit(q_empty);
+            if (lead) mma_commit(&k_empty[st]);
+            if (nkv == 1 && lead) mma_commit(q_empty);
           }
           for (int j = 0; j < nkv; ++j, ++c) {
             const uint32_t st = c % KST, ph = (c / KST) & 1;
@@ -303,17 +306,17 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
               issue_pv(i, vs, j > 0);
               if (has_next) {  // overwrites P_i(j): executes after PV_i(j) (tcgen05 issue order)
                 issue_qk(i, nks);
-                mma_commit(&s_full[i]);
+                if (lead) mma_commit(&s_full[i]);
                 VX_TRACE(trace_slot_mma(int(n), j, i, 1));
               } else {
-                mma_commit(&p_free[i]);  // last PV of the unit
+                if (lead) mma_commit(&p_free[i]);  // last PV of the unit
               }
             }
             pfull_ph ^= 1;
-            mma_commit(&v_empty[st]);
+            if (lead) mma_commit(&v_empty[st]);
             if (has_next) {
-              mma_commit(&k_empty[nst]);
-              if (j + 2 == nkv) mma_commit(q_empty);
+              if (lead) mma_commit(&k_empty[nst]);
+              if (j + 2 == nkv && lead) mma_commit(q_empty);
             }
           }
         }
@@ -330,11 +333,11 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
               if (n > 0) mbar_wait(&s_free[i], sfree_ph);
               tc_fence_after();
               issue_qk(i, ks);
-              mma_commit(&s_full[i]);
+              if (lead) mma_commit(&s_full[i]);
             }
             if (n > 0) sfree_ph ^= 1;
-            mma_commit(&k_empty[st]);
-            if (nkv == 1) mma_commit(q_empty);
+            if (lead) mma_commit(&k_empty[st]);
+            if (nkv == 1 && lead) mma_commit(q_empty);
           }
           for (int j = 0; j < nkv; ++j, ++c) {
             const uint32_t st = c % KST, ph = (c / KST) & 1;
@@ -346,11 +349,11 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
                 mbar_wait(&s_free[i], sfree_ph);
                 tc_fence_after();
                 issue_qk(i, nks);
-                mma_commit(&s_full[i]);
+                if (lead) mma_commit(&s_full[i]);
               }
               sfree_ph ^= 1;
-              mma_commit(&k_empty[nst]);
-              if (j + 2 == nkv) mma_commit(q_empty);
+              if (lead) mma_commit(&k_empty[nst]);
+              if (j + 2 == nkv && lead) mma_commit(q_empty);
             }
             const uint32_t vs = smem_u32(sV + st * Cfg::V_STAGE_BYTES);
             mbar_wait(&v_full[st], ph);
@@ -360,10 +363,10 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
               mbar_wait(&p_full[i], pfull_ph);
               tc_fence_after();
               issue_pv(i, vs, j > 0);
-              mma_commit(&p_free[i]);
+              if (lead) mma_commit(&p_free[i]);
             }
             pfull_ph ^= 1;
-            mma_commit(&v_empty[st]);
+            if (lead) mma_commit(&v_empty[st]);
           }
         }
       }
