@@ -119,3 +119,16 @@ class VGGT:
         }
 
     __call__ = forward
+
+    @torch.no_grad()
+    def point_map_from_depth(self, preds: Dict[str, torch.Tensor]) -> torch.Tensor:
+        """Depth-based world points (1, S_local, H, W, 3) fp32 from a forward's depth and decoded cameras
+        (upstream `unproject_depth_map_to_point_map`; the point cloud VGGT-X uses to initialise 3DGS).
+        Runs vx_unproject_depth; with frame sharding the cameras of this rank's frames are used."""
+        from .scene import unproject_depth_maps
+        depth = preds["depth"][0]
+        S_local = depth.shape[0]
+        f0 = int(preds.get("frame_offset", 0))
+        enc = preds["pose_enc"][0, f0:f0 + S_local].float()
+        extri, intri = pose_encoding_to_extri_intri(enc, tuple(depth.shape[1:3]))
+        return unproject_depth_maps(depth, extri, intri)[None]

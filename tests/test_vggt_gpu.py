@@ -129,3 +129,22 @@ def test_prediction_set_export():
     for Rm in ps["rotations"].astype(np.float64):
         # the adapter's acceptance rule (export.py:111-128)
         assert np.linalg.norm(Rm.T @ Rm - np.eye(3)) <= 1e-3 and np.linalg.det(Rm) > 0
+
+
+@pytest.mark.gpu
+def test_point_map_from_depth_matches_oracle():
+    """VGGT.point_map_from_depth (vx_unproject_depth on the decoded cameras) vs the oracle's
+    per-pixel unprojection of the same depth and cameras."""
+    from oracle import scene_ref
+    from paper_2509_25191_b200.pose import pose_encoding_to_extri_intri
+    from paper_2509_25191_b200.vggt import VGGT
+    cfg = vggt_tiny()
+    model = VGGT(cfg)
+    out = model(synthetic_images(cfg, 3, 1).cuda())
+    pts = model.point_map_from_depth(out)
+    assert pts.shape == (1, 3, cfg.img_size, cfg.img_size, 3)
+    ext, K = pose_encoding_to_extri_intri(out["pose_enc"][0].float(), (cfg.img_size, cfg.img_size))
+    ref = scene_ref.unproject_depth_maps(out["depth"][0, ..., 0].cpu().double().numpy(), ext.cpu().double().numpy(),
+                                         K.cpu().double().numpy())
+    got = pts[0].cpu().double().numpy()
+    assert np.abs(got - ref).max() < 1e-4 * max(1.0, np.abs(ref).max())
