@@ -450,6 +450,10 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
               }
               if constexpr (!SUMV) acc[c & 3] = f2_add(acc[c & 3], f2_pack(p0, p1));
               pk[c] = pack_bf16(p0, p1);
+              // 48-wide tiles: store the first 16 P columns while the last 8 pairs are computed
+              if constexpr (PAIRS == 24) {
+                if (c == 15) tmem_st16(P_addr + 32 * hf, pk);
+              }
             }
             VX_TRACE(trace_slot_sm(unit_n, wl, lane, tile, j, 3));
             if (!ALIAS && hf == 0 && j > 0) {  // P_i(j-1) consumed and O stable (waited after the first exps)
@@ -457,7 +461,8 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
               ++pv_cnt;
               tc_fence_after();
             }
-            tmem_st_n<PAIRS>(P_addr + 32 * hf, pk);
+            if constexpr (PAIRS == 24) tmem_st8(P_addr + 32 * hf + 16, pk + 16);
+            else tmem_st_n<PAIRS>(P_addr + 32 * hf, pk);
           }
           if constexpr (!SUMV) {
             float a0, a1, b0, b1;
