@@ -38,7 +38,7 @@ class VGGTConfig:
     dpt_head_features_2: int = 32
     # memory discipline (VGGT-X "VGGT--")
     frame_chunk: int = 128             # frames per chunk for frame-wise MLP work
-    head_chunk: int = 8                # frames per DPT-head chunk
+    head_chunk: int = 16               # frames per DPT-head chunk (16: -9% head time vs 8 for +4 GB, tools/exp_dpt_chunk.py)
 
     def __post_init__(self):
         # native DPT convs use 64-channel K blocks and 32-channel output chunks
