@@ -15,6 +15,7 @@ frame slice while `pose_enc` is global.
 """
 from __future__ import annotations
 
+import os
 from typing import Dict, Optional, Tuple
 
 import torch
@@ -48,12 +49,19 @@ class VGGT:
         self.depth_head = DPTHeadDevice(self.W, "depth_head.", "exp")
         self.point_head = DPTHeadDevice(self.W, "point_head.", "inv_log")
         self.dist = dist
+        self.head_streams = os.environ.get("VX_HEAD_STREAMS", "1") != "0"  # diagnostic switch
+        self._streams = None
         self.ring = None
         if dist:
             from .ring import FrameShardedRing
             self.ring = FrameShardedRing(self.cfg, self.device)
 
     # -- helpers ------------------------------------------------------------
+    def _head_streams(self, dev):
+        if self._streams is None:
+            self._streams = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
+        return self._streams
+
     def _local(self, images: torch.Tensor, sharded_input: bool):
         """(this rank's images on the device, global frame offset, global S).
 
@@ -105,8 +113,25 @@ class VGGT:
         pts = torch.empty(Sl, H, W, 3, device=dev)
         pts_conf = torch.empty(Sl, H, W, device=dev)
         with phase("dpt_heads"):
-            self.depth_head(kept, depth, depth_conf, cfg.head_chunk)
-            self.point_head(kept, pts, pts_conf, cfg.head_chunk)
+            if self.head_streams:  # the two heads are independent: run them concurrently
+                cur = torch.cuda.current_stream(dev)
+                s_d, s_p = self._head_streams(dev)
+                s_d.wait_stream(cur)
+                s_p.wait_stream(cur)
+                with torch.cuda.stream(s_d):
+                    self.depth_head(kept, depth, depth_conf, cfg.head_chunk)
+                with torch.cuda.stream(s_p):
+                    self.point_head(kept, pts, pts_conf, cfg.head_chunk)
+                cur.wait_stream(s_d)
+                cur.wait_stream(s_p)
+                for t in (depth, depth_conf, pts, pts_conf):  # produced on the side streams
+                    t.record_stream(cur)
+                for t in kept.values():
+                    t.record_stream(s_d)
+                    t.record_stream(s_p)
+            else:
+                self.depth_head(kept, depth, depth_conf, cfg.head_chunk)
+                self.point_head(kept, pts, pts_conf, cfg.head_chunk)
         return {
             "pose_enc": pose_list[-1][None],
             "pose_enc_list": [p[None] for p in pose_list],
