@@ -104,16 +104,16 @@ class VGGT:
         cam = kept[cfg.kept_layers[-1]][:, 0]                      # (Sl, 2C) strided view
         if self.ring is not None:
             cam = self.ring.all_gather_frames(cam.contiguous())
-        with phase("camera_head"):
-            pose_list = camera_head(self.W, cam)
         H = W = cfg.img_size
         dev = self.device
         depth = torch.empty(Sl, H, W, 1, device=dev)
         depth_conf = torch.empty(Sl, H, W, device=dev)
         pts = torch.empty(Sl, H, W, 3, device=dev)
         pts_conf = torch.empty(Sl, H, W, device=dev)
-        with phase("dpt_heads"):
-            if self.head_streams:  # the two heads are independent: run them concurrently
+        if self.head_streams:
+            # the three heads are independent: depth and point heads on two side streams, the camera
+            # head concurrently on the current stream
+            with phase("heads"):
                 cur = torch.cuda.current_stream(dev)
                 s_d, s_p = self._head_streams(dev)
                 s_d.wait_stream(cur)
@@ -122,14 +122,20 @@ class VGGT:
                     self.depth_head(kept, depth, depth_conf, cfg.head_chunk)
                 with torch.cuda.stream(s_p):
                     self.point_head(kept, pts, pts_conf, cfg.head_chunk)
+                pose_list = camera_head(self.W, cam)
                 cur.wait_stream(s_d)
                 cur.wait_stream(s_p)
-                for t in (depth, depth_conf, pts, pts_conf):  # produced on the side streams
-                    t.record_stream(cur)
-                for t in kept.values():
+                for t in kept.values():  # read on the side streams
                     t.record_stream(s_d)
                     t.record_stream(s_p)
-            else:
+                depth.record_stream(s_d)
+                depth_conf.record_stream(s_d)
+                pts.record_stream(s_p)
+                pts_conf.record_stream(s_p)
+        else:
+            with phase("camera_head"):
+                pose_list = camera_head(self.W, cam)
+            with phase("dpt_heads"):
                 self.depth_head(kept, depth, depth_conf, cfg.head_chunk)
                 self.point_head(kept, pts, pts_conf, cfg.head_chunk)
         return {
