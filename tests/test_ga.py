@@ -231,3 +231,22 @@ def test_device_align_errors(ga):
         ga.align(rig, ms, ga.AlignerConfig(weight_mode="confidence"))
     with pytest.raises(ValueError):
         ga.align(rig, ms, ga.AlignerConfig(gauge_frame=99))
+
+
+@pytest.mark.gpu
+def test_device_align_dense_scene_matches_oracle(ga):
+    """A denser synthetic scene than the goldens (80 views, every frame in > 32 pairs, so the per-frame
+    CSR gather spans several warp strides) against the oracle restatement."""
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1] / "tools"))
+    import bench_ga
+    R, t, intr, pij, off, xi, xj = bench_ga.scene(80, 600, 80.0, 96, seed=3)
+    cfgv = np.array([30, 5e-4, 1e-3, 1e-2, 2.5, 7.5, 0.0, 0, 1.0, 0.5, 0, 0])
+    ref = ga_ref.align(R, t, intr, pij, off, xi, xj, cfgv)
+    o = ga.align_arrays(R, t, intr, pij, off, xi, xj, ga.AlignerConfig(iterations=30))
+    assert np.bincount(pij.reshape(-1)).max() > 32
+    tr = np.abs(o["loss_trace"] - ref["loss_trace"]) / np.abs(ref["loss_trace"])
+    assert tr.max() < 1e-8, tr.max()
+    assert np.abs(o["out_R"] - ref["out_R"]).max() < 1e-8
+    np.testing.assert_allclose(o["report"][:3], ref["report"][:3], rtol=1e-8)

@@ -163,3 +163,28 @@ def test_device_unproject_depth_maps(sc, S, H, W):
     ref = scene_ref.unproject_depth_maps(depth.double().numpy(), extri.double().numpy(), intri.double().numpy())
     scale = np.abs(ref).max()
     assert np.abs(out - ref).max() < 1e-5 * scale
+
+
+@pytest.mark.gpu
+def test_device_matched_points_mixed_map_sizes(sc):
+    """Per-frame depth maps of different sizes and dtypes (DepthMap-like objects): the kernel's map
+    table (offset, h, w per map) against the oracle."""
+    rng = np.random.default_rng(4)
+    dm = MP["depth_dense"]
+    maps = {}
+    for f in range(len(dm)):
+        h, w = dm.shape[1] - 7 * (f % 3), dm.shape[2] - 5 * (f % 2)
+        maps[f] = np.ascontiguousarray(dm[f, :h, :w])
+
+    class _DM:
+        def __init__(self, v):
+            self.values = v
+
+    objs = {f: _DM(v) for f, v in maps.items()}
+    w = rng.uniform(0, 1, MP["w"].shape[0])
+    ref_pts, ref_sc, ref_sk = scene_ref.select_matched_points(MP["pair_ij"], MP["offsets"], MP["xy_i"], MP["xy_j"], w,
+                                                              maps, MP["R"], MP["t"], MP["intr"], 0.3)
+    pts, cons, sk = sc.select_matched_points_arrays(MP["pair_ij"], MP["offsets"], MP["xy_i"], MP["xy_j"], w, objs,
+                                                    MP["R"], MP["t"], _kinv(MP["intr"]), 0.3)
+    assert sk == ref_sk and pts.shape == ref_pts.shape
+    np.testing.assert_allclose(pts, ref_pts, rtol=1e-12, atol=1e-12)
