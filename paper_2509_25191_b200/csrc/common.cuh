@@ -113,7 +113,9 @@ VX_DEVICE uint32_t mapa_shared(uint32_t saddr, uint32_t rank) {
 }
 // arrive on an mbarrier given by its shared::cluster address (possibly in the peer CTA)
 VX_DEVICE void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+  // relaxed: the accumulator hand-off is ordered by tcgen05.wait::ld + fence::before_thread_sync, and a
+  // release at cluster scope would drain every outstanding global store of the epilogue (MEMBAR.GPU)
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 // CTA-pair TMA load: data into this CTA's smem, completion signalled on `mbar_cluster` (the
 // pair leader's barrier, a shared::cluster address)
