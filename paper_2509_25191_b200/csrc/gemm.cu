@@ -50,19 +50,44 @@ struct GemmCfg {
 // ---------------------------------------------------------------------------
 // epilogues: one thread = one output row; columns processed 32 at a time
 // ---------------------------------------------------------------------------
+// the chunk's global operands (bias; the fp32 residual row segment for RESID), loaded before the
+// TMEM load so their latency overlaps it instead of serialising behind it
 template <int EPI>
-VX_DEVICE void epi_chunk32(const GemmArgs& a, int row, int col, const uint32_t* r) {
+struct EpiPre {
+  float4 b[8];
+  float4 x[EPI == VX_EPI_RESID ? 8 : 1];
+};
+
+template <int EPI>
+VX_DEVICE void epi_prefetch(const GemmArgs& a, int row, int col, EpiPre<EPI>& p) {
   const vx_epilogue& e = a.ep;
-  float v[32];
-#pragma unroll
-  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
   if (e.bias) {
     const float4* b4 = reinterpret_cast<const float4*>(e.bias + col);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      float4 b = __ldg(b4 + j);
-      v[4 * j] += b.x; v[4 * j + 1] += b.y; v[4 * j + 2] += b.z; v[4 * j + 3] += b.w;
+    for (int j = 0; j < 8; ++j) p.b[j] = __ldg(b4 + j);
+  } else {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) p.b[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  if constexpr (EPI == VX_EPI_RESID) {
+    if (row < a.M) {
+      const float4* x4 = reinterpret_cast<const float4*>(e.resid + (size_t)row * e.ldr + col);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) p.x[j] = x4[j];
     }
+  }
+}
+
+template <int EPI>
+VX_DEVICE void epi_chunk32(const GemmArgs& a, int row, int col, const uint32_t* r, const EpiPre<EPI>& pre) {
+  const vx_epilogue& e = a.ep;
+  float v[32];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    v[4 * j] = __uint_as_float(r[4 * j]) + pre.b[j].x;
+    v[4 * j + 1] = __uint_as_float(r[4 * j + 1]) + pre.b[j].y;
+    v[4 * j + 2] = __uint_as_float(r[4 * j + 2]) + pre.b[j].z;
+    v[4 * j + 3] = __uint_as_float(r[4 * j + 3]) + pre.b[j].w;
   }
   if (row >= a.M) return;
   if constexpr (EPI == VX_EPI_BF16 || EPI == VX_EPI_GELU) {
@@ -92,7 +117,7 @@ VX_DEVICE void epi_chunk32(const GemmArgs& a, int row, int col, const uint32_t* 
     const float4* g4 = reinterpret_cast<const float4*>(e.gamma + col);
     float4 xv[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) xv[j] = x4[j];
+    for (int j = 0; j < 8; ++j) xv[j] = pre.x[j];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       float4 g = __ldg(g4 + j);
@@ -528,10 +553,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         for (int c0 = c_beg; c0 < c_end; c0 += 32) {
           const int col = n_blk * BN + c0;
           if (col >= N) break;
+          EpiPre<EPI> pre;
+          epi_prefetch<EPI>(args, row, col, pre);
           uint32_t r[32];
           tmem_ld32(taddr + c0, r);
           tmem_wait_ld();
-          epi_chunk32<EPI>(args, row, col, r);
+          epi_chunk32<EPI>(args, row, col, r, pre);
         }
       }
       tc_fence_before();
