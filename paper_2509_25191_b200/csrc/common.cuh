@@ -56,6 +56,20 @@ VX_DEVICE void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
       "r"(bytes)
       : "memory");
 }
+// try_wait without a suspend-time hint (the default system time limit)
+VX_DEVICE void mbar_wait_nohint(uint64_t* bar, uint32_t phase) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "LAB_WAITN:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONEN;\n\t"
+      "bra LAB_WAITN;\n\t"
+      "DONEN:\n\t}" ::"r"(addr),
+      "r"(phase)
+      : "memory");
+}
+
 VX_DEVICE void mbar_wait(uint64_t* bar, uint32_t phase) {
   uint32_t addr = smem_u32(bar);
   asm volatile(
