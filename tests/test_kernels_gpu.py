@@ -147,7 +147,9 @@ def _sdpa_ref(q, k, v, nseq, Lq, Lk):
 @pytest.mark.parametrize("D,H,nseq,L", [(64, 16, 3, 1374), (64, 2, 1, 5000), (64, 4, 5, 69), (32, 4, 8, 69),
                                         (32, 4, 1, 552), (64, 1, 2, 128), (64, 3, 1, 300), (64, 2, 1, 17),
                                         (128, 16, 1, 200), (128, 4, 1, 1000), (128, 2, 3, 77), (128, 16, 1, 8),
-                                        (64, 2, 2, 4099), (64, 1, 1, 8192)])
+                                        (64, 2, 2, 4099), (64, 1, 1, 8192),
+                                        # > 148 work units: CTAs run several units (unit hand-offs)
+                                        (64, 16, 12, 1374), (64, 16, 1, 6000)])
 def test_attention_matches_sdpa(ops, D, H, nseq, L):
     T = nseq * L
     q = _bf(H, T, D, seed=20)
