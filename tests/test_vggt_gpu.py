@@ -148,3 +148,22 @@ def test_point_map_from_depth_matches_oracle():
                                          K.cpu().double().numpy())
     got = pts[0].cpu().double().numpy()
     assert np.abs(got - ref).max() < 1e-4 * max(1.0, np.abs(ref).max())
+
+
+@pytest.mark.gpu
+def test_sharded_embed_matches_global_slice():
+    """A frame shard that does not own global frame 0 (ranks > 0 under torchrun) embeds its views
+    exactly like the same views of the whole batch (camera/register tokens index 1)."""
+    from paper_2509_25191_b200.aggregator import DeviceWeights, alloc_workspace, embed
+    cfg = vggt_tiny()
+    W = DeviceWeights(make_state_dict(cfg, 0), cfg, torch.device("cuda"))
+    imgs = synthetic_images(cfg, 6, 1).cuda()
+    ws_all = alloc_workspace(cfg, 6)
+    embed(W, imgs, ws_all, frame0_is_first=True)
+    ws_shard = alloc_workspace(cfg, 3)
+    embed(W, imgs[2:5].contiguous(), ws_shard, frame0_is_first=False)
+    N = cfg.tokens_per_frame
+    assert torch.equal(ws_shard.x[: 3 * N], ws_all.x[2 * N:5 * N])
+    ws_head = alloc_workspace(cfg, 2)
+    embed(W, imgs[:2].contiguous(), ws_head, frame0_is_first=True)
+    assert torch.equal(ws_head.x[: 2 * N], ws_all.x[: 2 * N])
