@@ -361,3 +361,25 @@ def test_attention_ring_merge_matches_full(ops, shards):
     got = o_acc if len(shards) == 1 else out
     assert rel(got, ref) < 1e-2
     assert (lse - lse_ref).abs().max().item() < 1e-2
+
+
+@pytest.mark.gpu
+def test_c_abi_rejects_bad_shapes(ops):
+    """Every entry point validates its arguments and reports through vx_last_error (no CUDA fault)."""
+    bf = torch.bfloat16
+    with pytest.raises(RuntimeError, match="K=100"):
+        ops.gemm(torch.zeros(128, 100, device="cuda", dtype=bf), torch.zeros(256, 100, device="cuda", dtype=bf))
+    with pytest.raises(RuntimeError, match="head_dim 48"):
+        q = torch.zeros(2, 64, 48, device="cuda", dtype=bf)
+        ops.attention(q, q, q, torch.zeros(64, 96, device="cuda", dtype=bf), 1, 64, 64)
+    with pytest.raises(RuntimeError, match="cols=100"):
+        ops.layernorm(torch.zeros(4, 100, device="cuda"), None, None, 1e-5)
+    with pytest.raises(RuntimeError, match="multiple of 8"):
+        ops.upsample_bilinear(torch.zeros(1, 4, 4, 12, device="cuda", dtype=bf), (8, 8))
+    with pytest.raises(RuntimeError, match="mode must be"):
+        q = torch.zeros(2, 64, 64, device="cuda", dtype=bf)
+        ops.attention_merge(q, q, q, 7, torch.zeros(64, 128, device="cuda"), torch.zeros(2, 64, device="cuda"))
+    torch.cuda.synchronize()  # the context is still healthy
+    x = torch.randn(4, 128, device="cuda")
+    y = ops.layernorm(x, None, None, 1e-5)
+    assert torch.isfinite(y.float()).all()
