@@ -325,7 +325,7 @@ def test_spatial_fused_output_head(ops, act, odim):
 
 
 def test_upsample_bilinear_matches_interpolate(ops):
-    for (h, H, C) in ((19, 37, 256), (148, 296, 64), (296, 518, 128)):
+    for (h, H, C) in ((19, 37, 256), (148, 296, 64), (296, 518, 128), (5, 9, 24)):
         x = torch.randn(2, h, h, C, device="cuda").to(torch.bfloat16)
         add = torch.randn(H, H, C, device="cuda").to(torch.bfloat16)
         out = ops.upsample_bilinear(x, (H, H), add=add)
