@@ -640,9 +640,12 @@ static int attention_impl(const void* q, const void* k, const void* v, void* out
       case 3: return launch_fmha<64, 2, 3, 64>(q, k, v, a, st);
       case 4: return launch_fmha<64, 2, 4, 64, true>(q, k, v, a, st);
       case 14: return launch_fmha<64, 2, 4, 48, true, true, false>(q, k, v, a, st);  // suspend-hint waits
+      case 15: return launch_fmha<64, 2, 4, 48, true, false, true>(q, k, v, a, st);  // FADD row sums
+      case 16: return launch_fmha<64, 1, 4, 48, true, false, true>(q, k, v, a, st);
       default: break;
     }
     switch (emu) {  // S-ready / P-ready waits without a suspend-time hint: +0.4% (tools/exp_nohint.sh)
+      case 0: return launch_fmha<64, 0, 4, 48, true, true, true>(q, k, v, a, st);
       case 1: return launch_fmha<64, 1, 4, 48, true, true, true>(q, k, v, a, st);
       case 3: return launch_fmha<64, 3, 4, 48, true, true, true>(q, k, v, a, st);
       default: return launch_fmha<64, 2, 4, 48, true, true, true>(q, k, v, a, st);
