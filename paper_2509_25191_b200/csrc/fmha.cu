@@ -27,6 +27,10 @@
 #include <math.h>
 #include <stdlib.h>
 
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "../../include/vx_api.h"
 #include "common.cuh"
 #include "host_util.h"
@@ -46,7 +50,26 @@ struct AttnArgs {
   __nv_bfloat16* out;
   int64_t ldo;
   float* lse;
+  // KV-split tail (plain attention only): units >= split_from run as `parts` work items, each over
+  // a contiguous range of KV tiles, writing normalised fp32 partial O + lse to part_o / part_lse
+  // (item-major, ROWS rows each); fmha_split_merge combines them. work = total work items.
+  int split_from, parts, work;
+  float* part_o;
+  float* part_lse;
 };
+
+// work item w -> unit, first KV tile, KV tile count, part (-1: whole unit), tail index
+struct WorkItem {
+  int u, j0, cnt, part, t;
+};
+VX_DEVICE WorkItem work_item(const AttnArgs& a, int w) {
+  if (w < a.split_from) return {w, 0, a.kv_tiles, -1, 0};
+  const int x = w - a.split_from;
+  const int t = x / a.parts, p = x - t * a.parts;
+  const int j0 = p * a.kv_tiles / a.parts;  // host guarantees parts * kv_tiles < 2^31
+  const int j1 = (p + 1) * a.kv_tiles / a.parts;
+  return {a.split_from + t, j0, j1 - j0, p, t};
+}
 
 template <int D, int NT_ = (D == 128 ? 1 : 2), int BKV_ = 128, bool ALIAS_ = false, bool SUMV_ = false>
 struct AttnCfg {
@@ -204,7 +227,6 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
   const uint32_t tmem = *tmem_slot;
 
   const int per_head = a.nseq * a.q_blocks;
-  const int nkv = a.kv_tiles;
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -213,7 +235,9 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
       const uint64_t pol_q = policy_evict_first();
       uint32_t c = 0;  // global K/V tile counter
       uint32_t n = 0;  // local unit counter
-      for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++n) {
+      for (int w = blockIdx.x; w < a.work; w += gridDim.x, ++n) {
+        const WorkItem wi = work_item(a, w);
+        const int u = wi.u;
         const int h = u / per_head;
         const int rem = u - h * per_head;
         const int s = rem / a.q_blocks;
@@ -226,7 +250,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
           for (int pn = 0; pn < Cfg::PANELS; ++pn)
             tma_load_2d_hint(sQ + i * Cfg::Q_TILE_BYTES + pn * Cfg::QPANEL_BYTES, &tmQ, q_full,
                              pn * Cfg::PANEL_COLS, q_row + 128 * i, pol_q);
-        for (int j = 0; j < nkv; ++j, ++c) {
+        for (int j = wi.j0; j < wi.j0 + wi.cnt; ++j, ++c) {
           const uint32_t st = c % KST, ph = (c / KST) & 1;
           mbar_wait(&k_empty[st], ph ^ 1);
           mbar_expect_tx(&k_full[st], Cfg::KV_TILE_BYTES);
@@ -274,7 +298,8 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
       uint32_t n = 0;  // local unit counter
       uint32_t sfree_ph = 0, pfull_ph = 0;
       if constexpr (ALIAS) {
-        for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++n) {
+        for (int w = blockIdx.x; w < a.work; w += gridDim.x, ++n) {
+          const int nkv = work_item(a, w).cnt;
           mbar_wait(q_full, n & 1);
           tc_fence_after();
           {  // S(0): the previous unit's P / S columns were consumed by its last PVs (in order)
@@ -322,7 +347,8 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
           }
         }
       } else {
-        for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++n) {
+        for (int w = blockIdx.x; w < a.work; w += gridDim.x, ++n) {
+          const int nkv = work_item(a, w).cnt;
           mbar_wait(q_full, n & 1);
           tc_fence_after();
           {  // S(0) of both tiles; the S buffers were released by the previous unit's last s_free
@@ -385,7 +411,10 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
     const uint64_t SL2 = f2_pack(sl2, sl2);
     uint32_t sph = 0, pv_cnt = 0;
     [[maybe_unused]] int unit_n = 0;
-    for (int u = blockIdx.x; u < a.units; u += gridDim.x, ++unit_n) {
+    for (int w = blockIdx.x; w < a.work; w += gridDim.x, ++unit_n) {
+      const WorkItem wi = work_item(a, w);
+      const int nkv = wi.cnt;
+      const int u = wi.u;
       const int h = u / per_head;
       const int rem = u - h * per_head;
       const int s = rem / a.q_blocks;
@@ -408,7 +437,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
           __syncwarp();
           if (lane == 0) mbar_arrive(&s_free[tile]);
         }
-        const int valid = a.Lk - BKV * j;
+        const int valid = a.Lk - BKV * (wi.j0 + j);
         auto step = [&](auto mask_tag) {
           if constexpr (decltype(mask_tag)::value) {
 #pragma unroll
@@ -509,7 +538,16 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
         const float inv = 1.0f / l_run;
         const int64_t orow = (int64_t)s * a.Lq + q_local;
         const float lse_new = (m_run + __log2f(l_run)) * 0.69314718055994531f;
-        if (a.merge == 0) {
+        if (wi.part >= 0) {  // KV-split tail item: normalised fp32 partial + lse, merged by fmha_split_merge
+          const int64_t item = (int64_t)wi.t * a.parts + wi.part;
+          const int lr = tile * 128 + r;
+          float4* dst = reinterpret_cast<float4*>(a.part_o + (item * Cfg::ROWS + lr) * D);
+#pragma unroll
+          for (int c = 0; c < D / 4; ++c)
+            dst[c] = make_float4(__uint_as_float(orr[4 * c]) * inv, __uint_as_float(orr[4 * c + 1]) * inv,
+                                 __uint_as_float(orr[4 * c + 2]) * inv, __uint_as_float(orr[4 * c + 3]) * inv);
+          a.part_lse[item * Cfg::ROWS + lr] = lse_new;
+        } else if (a.merge == 0) {
           uint4* dst = reinterpret_cast<uint4*>(a.out + orow * a.ldo + h * D);
 #pragma unroll
           for (int c = 0; c < D / 8; ++c) {
@@ -568,6 +606,69 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
   }
 }
 
+// Combines the KV-split tail items: one thread per (tail row, 4 output columns).
+template <int D, int ROWS>
+__global__ void __launch_bounds__(256) fmha_split_merge(const AttnArgs a) {
+  constexpr int G4 = D / 4;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t total = (int64_t)(a.units - a.split_from) * ROWS * G4;
+  if (idx >= total) return;
+  const int g = int(idx % G4);
+  const int64_t rr = idx / G4;
+  const int lr = int(rr % ROWS);
+  const int t = int(rr / ROWS);
+  const int u = a.split_from + t;
+  const int per_head = a.nseq * a.q_blocks;
+  const int h = u / per_head;
+  const int rem = u - h * per_head;
+  const int s = rem / a.q_blocks;
+  const int qb = rem - s * a.q_blocks;
+  const int q_local = qb * ROWS + lr;
+  if (q_local >= a.Lq) return;
+  const int64_t item0 = (int64_t)t * a.parts;
+  float mx = -INFINITY;
+  for (int p = 0; p < a.parts; ++p) mx = fmaxf(mx, a.part_lse[(item0 + p) * ROWS + lr]);
+  float wsum = 0.f;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int p = 0; p < a.parts; ++p) {
+    const float wgt = __expf(a.part_lse[(item0 + p) * ROWS + lr] - mx);
+    const float4 o = reinterpret_cast<const float4*>(a.part_o + ((item0 + p) * ROWS + lr) * D)[g];
+    wsum += wgt;
+    acc.x += wgt * o.x;
+    acc.y += wgt * o.y;
+    acc.z += wgt * o.z;
+    acc.w += wgt * o.w;
+  }
+  const float inv = 1.0f / wsum;
+  const int64_t orow = (int64_t)s * a.Lq + q_local;
+  *reinterpret_cast<uint2*>(a.out + orow * a.ldo + h * D + 4 * g) =
+      make_uint2(pack_bf16(acc.x * inv, acc.y * inv), pack_bf16(acc.z * inv, acc.w * inv));
+  if (g == 0 && a.lse) a.lse[h * a.Tq + orow] = mx + __logf(wsum);
+}
+
+// Per-stream scratch for the KV-split tail (at most one wave of items: num_sms x ROWS x (D + 1)
+// fp32). Allocated once per stream and kept; not allocated while the stream is being captured.
+static float* split_scratch(cudaStream_t st, size_t floats) {
+  static std::mutex mu;
+  static std::map<cudaStream_t, std::pair<float*, size_t>> bufs;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = bufs.find(st);
+  if (it != bufs.end() && it->second.second >= floats) return it->second.first;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
+  float* p = nullptr;
+  if (cudaMalloc(&p, floats * sizeof(float)) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  if (it != bufs.end()) {  // grow: the old buffer may still be read by queued work on this stream
+    cudaStreamSynchronize(st);
+    cudaFree(it->second.first);
+  }
+  bufs[st] = {p, floats};
+  return p;
+}
+
 template <int D, int EMU, int NT = (D == 128 ? 1 : 2), int BKV = 128, bool ALIAS = false, bool SUMV = false,
           bool NOHINT = false>
 static int launch_fmha(const void* q, const void* k, const void* v, AttnArgs args, cudaStream_t st) {
@@ -580,6 +681,30 @@ static int launch_fmha(const void* q, const void* k, const void* v, AttnArgs arg
   args.q_blocks = (args.Lq + Cfg::ROWS - 1) / Cfg::ROWS;
   args.kv_tiles = (args.Lk + BKV - 1) / BKV;
   args.units = args.H * args.nseq * args.q_blocks;
+  // KV-split tail: when the last wave of units would leave more than half the SMs idle, split each
+  // of its units over `parts` CTAs (contiguous KV ranges) and merge the partials afterwards
+  const int sms = num_sms();
+  const int tail = args.units % sms;
+  args.split_from = args.units;
+  args.parts = 1;
+  static const bool split_on = [] {
+    const char* e = getenv("VX_FMHA_SPLIT");  // diagnostic: 0 disables the KV-split tail
+    return !(e && atoi(e) == 0);
+  }();
+  if (split_on && args.merge == 0 && tail > 0 && 2 * tail <= sms) {
+    int parts = sms / tail;
+    if (parts > args.kv_tiles / 2) parts = args.kv_tiles / 2;  // >= 2 KV tiles per item
+    if (parts >= 2 && (int64_t)parts * args.kv_tiles < (1ll << 31)) {
+      float* scratch = split_scratch(st, (size_t)sms * Cfg::ROWS * (D + 1));
+      if (scratch) {
+        args.split_from = args.units - tail;
+        args.parts = parts;
+        args.part_o = scratch;
+        args.part_lse = scratch + (size_t)sms * Cfg::ROWS * D;
+      }
+    }
+  }
+  args.work = args.split_from + (args.units - args.split_from) * args.parts;
   auto kern = fmha_kernel<D, EMU, NT, BKV, ALIAS, SUMV, NOHINT>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -587,9 +712,14 @@ static int launch_fmha(const void* q, const void* k, const void* v, AttnArgs arg
     if (e != cudaSuccess) return fail_cuda(e, "fmha: cudaFuncSetAttribute");
     attr_set = true;
   }
-  const int grid = args.units < num_sms() ? args.units : num_sms();
+  const int grid = args.work < sms ? args.work : sms;
   kern<<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(tq, tk, tv, args);
   VX_CHECK_LAUNCH("fmha launch");
+  if (args.split_from < args.units) {
+    const int64_t threads = (int64_t)(args.units - args.split_from) * Cfg::ROWS * (D / 4);
+    fmha_split_merge<D, Cfg::ROWS><<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(args);
+    VX_CHECK_LAUNCH("fmha split merge");
+  }
   return VX_OK;
 }
 
@@ -606,7 +736,7 @@ static int attention_impl(const void* q, const void* k, const void* v, void* out
   VX_CHECK_ARG(!out || (ldo >= (int64_t)H * D && ldo % 8 == 0), "vx_attention: bad ldo");
   VX_CHECK_ARG(merge == 0 || (o_acc && lse && ld_acc >= (int64_t)H * D && ld_acc % 4 == 0),
                "vx_attention: merge needs o_acc [Tq, >= H*D] fp32 and lse");
-  AttnArgs a;
+  AttnArgs a{};
   a.H = H;
   a.nseq = nseq;
   a.Lq = Lq;

@@ -176,7 +176,9 @@ def test_attention_large_logits_rescale(ops, L):
     assert rel(out, ref) < 1e-2
 
 
-@pytest.mark.parametrize("Lq,Lk", [(700, 1900), (333, 6000), (4200, 257)])
+@pytest.mark.parametrize("Lq,Lk", [(700, 1900), (333, 6000), (4200, 257),
+                                   # 600 units = 4 full waves + 8: the 8 tail units run KV-split (18 parts)
+                                   (512 * 149 + 100, 3000)])
 def test_attention_cross_lengths(ops, Lq, Lk):
     # ring-step shape: local queries against a remote K/V shard of another length
     H, D = 4, 64
