@@ -87,7 +87,12 @@ int vx_gemm(int epi, const void* A, int64_t lda, const void* B, int64_t ldb, int
  *   h*Tq + s*Lq .. +Lq (q) and h*Tk + s*Lk .. +Lk (k, v).
  *   out: bf16, row (s*Lq + i), columns h*D .. h*D+D-1, row stride ldo.
  *   lse: optional fp32 [H, Tq] natural-log log-sum-exp of the scaled scores.
- * D in {32, 64, 128} (128: camera-head trunk); scale = 1/sqrt(D). */
+ * D in {32, 64, 128} (128: camera-head trunk); scale = 1/sqrt(D).
+ * When the last wave of 512-row work units would leave more than half the SMs idle, those units
+ * are split over KV ranges and merged by a second kernel on the same stream; the fp32 partials
+ * live in a per-stream scratch buffer (num_SMs x 512 x (D+1) floats, ~19 MB at D=64) allocated on
+ * first use and kept. While the stream is being captured into a graph nothing is allocated and
+ * the split is skipped unless the buffer already exists. */
 int vx_attention(const void* q, const void* k, const void* v, void* out, int64_t ldo, float* lse,
                  int D, int H, int nseq, int Lq, int Lk, int64_t Tq, int64_t Tk, void* stream);
 /* One K/V-ring step of frame-sharded global attention with the log-sum-exp merge
