@@ -50,7 +50,7 @@ struct AttnArgs {
   __nv_bfloat16* out;
   int64_t ldo;
   float* lse;
-  // KV-split tail (plain attention only): units >= split_from run as `parts` work items, each over
+  // KV-split tail (plain and ring-merge modes): units >= split_from run as `parts` work items, each over
   // a contiguous range of KV tiles, writing normalised fp32 partial O + lse to part_o / part_lse
   // (item-major, ROWS rows each); fmha_split_merge combines them. work = total work items.
   int split_from, parts, work;
@@ -606,13 +606,15 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
   }
 }
 
-// Combines the KV-split tail items: one thread per (tail row, 4 output columns).
+// Combines the KV-split tail items: one thread per (tail row, 4 output columns); the threads of a
+// row are consecutive lanes of one warp (G4 divides 32). merge 0 writes out (+ lse); ring modes
+// 1-3 fold the combined block into (o_acc, lse_acc) exactly like the FMHA epilogue does.
 template <int D, int ROWS>
 __global__ void __launch_bounds__(256) fmha_split_merge(const AttnArgs a) {
   constexpr int G4 = D / 4;
+  static_assert(32 % G4 == 0, "row threads within one warp");
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t total = (int64_t)(a.units - a.split_from) * ROWS * G4;
-  if (idx >= total) return;
   const int g = int(idx % G4);
   const int64_t rr = idx / G4;
   const int lr = int(rr % ROWS);
@@ -624,26 +626,57 @@ __global__ void __launch_bounds__(256) fmha_split_merge(const AttnArgs a) {
   const int s = rem / a.q_blocks;
   const int qb = rem - s * a.q_blocks;
   const int q_local = qb * ROWS + lr;
-  if (q_local >= a.Lq) return;
-  const int64_t item0 = (int64_t)t * a.parts;
-  float mx = -INFINITY;
-  for (int p = 0; p < a.parts; ++p) mx = fmaxf(mx, a.part_lse[(item0 + p) * ROWS + lr]);
-  float wsum = 0.f;
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int p = 0; p < a.parts; ++p) {
-    const float wgt = __expf(a.part_lse[(item0 + p) * ROWS + lr] - mx);
-    const float4 o = reinterpret_cast<const float4*>(a.part_o + ((item0 + p) * ROWS + lr) * D)[g];
-    wsum += wgt;
-    acc.x += wgt * o.x;
-    acc.y += wgt * o.y;
-    acc.z += wgt * o.z;
-    acc.w += wgt * o.w;
-  }
-  const float inv = 1.0f / wsum;
+  // no early return: every lane reaches the __syncwarp below
+  const bool live = idx < total && q_local < a.Lq;
   const int64_t orow = (int64_t)s * a.Lq + q_local;
-  *reinterpret_cast<uint2*>(a.out + orow * a.ldo + h * D + 4 * g) =
-      make_uint2(pack_bf16(acc.x * inv, acc.y * inv), pack_bf16(acc.z * inv, acc.w * inv));
-  if (g == 0 && a.lse) a.lse[h * a.Tq + orow] = mx + __logf(wsum);
+  float4 ob = make_float4(0.f, 0.f, 0.f, 0.f);
+  float lse_b = 0.f, lp = -INFINITY;
+  if (live) {
+    const int64_t item0 = (int64_t)t * a.parts;
+    float mx = -INFINITY;
+    for (int p = 0; p < a.parts; ++p) mx = fmaxf(mx, a.part_lse[(item0 + p) * ROWS + lr]);
+    float wsum = 0.f;
+    for (int p = 0; p < a.parts; ++p) {
+      const float wgt = __expf(a.part_lse[(item0 + p) * ROWS + lr] - mx);
+      const float4 o = reinterpret_cast<const float4*>(a.part_o + ((item0 + p) * ROWS + lr) * D)[g];
+      wsum += wgt;
+      ob.x += wgt * o.x;
+      ob.y += wgt * o.y;
+      ob.z += wgt * o.z;
+      ob.w += wgt * o.w;
+    }
+    const float inv = 1.0f / wsum;
+    ob = make_float4(ob.x * inv, ob.y * inv, ob.z * inv, ob.w * inv);
+    lse_b = mx + __logf(wsum);
+    if (a.merge >= 2) lp = a.lse[h * a.Tq + orow];
+  }
+  __syncwarp();  // every lane of the row has read lse_acc before lane g == 0 overwrites it
+  if (!live) return;
+  if (a.merge == 0) {
+    *reinterpret_cast<uint2*>(a.out + orow * a.ldo + h * D + 4 * g) =
+        make_uint2(pack_bf16(ob.x, ob.y), pack_bf16(ob.z, ob.w));
+    if (g == 0 && a.lse) a.lse[h * a.Tq + orow] = lse_b;
+    return;
+  }
+  float wa = 0.f, wb = 1.f, lse_out = lse_b;
+  if (a.merge >= 2) {
+    const float mx = fmaxf(lp, lse_b);
+    const float ea = __expf(lp - mx), eb = __expf(lse_b - mx);
+    const float rs = 1.0f / (ea + eb);
+    wa = ea * rs;
+    wb = eb * rs;
+    lse_out = mx + __logf(ea + eb);
+  }
+  float4* acc = reinterpret_cast<float4*>(a.o_acc + orow * a.ld_acc + h * D) + g;
+  const float4 pa = a.merge >= 2 ? *acc : make_float4(0.f, 0.f, 0.f, 0.f);
+  const float4 m = make_float4(wa * pa.x + wb * ob.x, wa * pa.y + wb * ob.y, wa * pa.z + wb * ob.z,
+                               wa * pa.w + wb * ob.w);
+  if (a.merge == 3)
+    *reinterpret_cast<uint2*>(a.out + orow * a.ldo + h * D + 4 * g) =
+        make_uint2(pack_bf16(m.x, m.y), pack_bf16(m.z, m.w));
+  else
+    *acc = m;
+  if (g == 0) a.lse[h * a.Tq + orow] = lse_out;
 }
 
 // Per-stream scratch for the KV-split tail (at most one wave of items: num_sms x ROWS x (D + 1)
@@ -691,7 +724,7 @@ static int launch_fmha(const void* q, const void* k, const void* v, AttnArgs arg
     const char* e = getenv("VX_FMHA_SPLIT");  // diagnostic: 0 disables the KV-split tail
     return !(e && atoi(e) == 0);
   }();
-  if (split_on && args.merge == 0 && tail > 0 && 2 * tail <= sms) {
+  if (split_on && tail > 0 && 2 * tail <= sms) {
     int parts = sms / tail;
     if (parts > args.kv_tiles / 2) parts = args.kv_tiles / 2;  // >= 2 KV tiles per item
     if (parts >= 2 && (int64_t)parts * args.kv_tiles < (1ll << 31)) {

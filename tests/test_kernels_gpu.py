@@ -339,10 +339,12 @@ def test_upsample_bilinear_matches_interpolate(ops):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("shards", [[700], [300, 411], [513, 200, 333, 90]])
-def test_attention_ring_merge_matches_full(ops, shards):
+@pytest.mark.parametrize("shards,Lq", [([700], 600), ([300, 411], 600), ([513, 200, 333, 90], 600),
+                                       # 600 units = 4 waves + 8: KV-split tail in every merge mode
+                                       ([3000], 512 * 149 + 100), ([2000, 1500, 2500], 512 * 149 + 100)])
+def test_attention_ring_merge_matches_full(ops, shards, Lq):
     # the ring's fused-merge steps (vx_attention_merge) over K/V shards == attention over all keys
-    H, Lq, D = 4, 600, 64
+    H, D = 4, 64
     Lk = sum(shards)
     q = _bf(H, Lq, D, seed=50)
     k = _bf(H, Lk, D, seed=51)
