@@ -203,7 +203,7 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    launches0 = ops.launch_count
+    launches0 = ops.kernel_launches()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record()
@@ -215,7 +215,7 @@ def main():
         dist.barrier()
     clk = clocks.stop()
     profiling.set_timer(None)
-    launches = (ops.launch_count - launches0) // args.steps
+    launches = (ops.kernel_launches() - launches0) // args.steps
     ms = t0.elapsed_time(t1)
     if world > 1:
         tt = torch.tensor([ms], device="cuda")

@@ -266,6 +266,8 @@ int vx_pairwise_errors(const double* Rp, const double* tp, const double* Rg, con
                        uint8_t* zero_baseline, void* stream);
 
 int vx_num_sms(void);
+/* Kernels this library has launched in this process (a CUDA-graph replay counts its kernel nodes). */
+uint64_t vx_launch_count(void);
 const char* vx_last_error(void);
 const char* vx_version(void);
 

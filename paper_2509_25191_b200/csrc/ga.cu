@@ -595,6 +595,8 @@ static int frame_blocks(int n) { return (n + GA_FRAME_THREADS - 1) / GA_FRAME_TH
 static int frame_warp_blocks(int n) { return (32 * n + GA_FRAME_THREADS - 1) / GA_FRAME_THREADS; }
 static int chain_blocks(int p) { return std::max(1, (p + GA_CHAIN_THREADS - 1) / GA_CHAIN_THREADS); }
 
+static uint64_t iteration_kernels(const vx_ga_problem& pb) { return pb.n_pairs > 0 ? 4 : 2; }
+
 static void launch_iteration(const vx_ga_problem& pb, int t, double lr, const double* bc1, const double* bc2,
                              double* trace, double* skipped_total, cudaStream_t st) {
   if (pb.n_pairs > 0) {
@@ -639,7 +641,7 @@ extern "C" int vx_ga_loss_grad(const vx_ga_problem* pb, double* grad, void* stre
   }
   ga_chain_kernel<<<chain_blocks(pb->n_pairs), GA_CHAIN_THREADS, 0, st>>>(*pb, nullptr, 0, nullptr);
   ga_frame_kernel<<<frame_warp_blocks(pb->n_frames), GA_FRAME_THREADS, 0, st>>>(*pb, grad, 0.0, nullptr, nullptr, 0);
-  VX_CHECK_LAUNCH("ga loss/grad launch");
+  VX_CHECK_LAUNCH_N("ga loss/grad launch", iteration_kernels(*pb));
   return VX_OK;
 }
 
@@ -653,7 +655,7 @@ extern "C" int vx_ga_adam(const vx_ga_problem* pb, int t0, int iters, double lr,
   if (iters == 0) return VX_OK;
   if (!use_graph) {
     for (int k = 0; k < iters; ++k) launch_iteration(*pb, t0 + k, lr, bc1, bc2, trace, skipped_total, st);
-    VX_CHECK_LAUNCH("ga adam launch");
+    VX_CHECK_LAUNCH_N("ga adam launch", (uint64_t)iters * iteration_kernels(*pb));
     return VX_OK;
   }
   // capture on a private stream (the caller's may be the legacy default stream), replay on the caller's
@@ -673,6 +675,7 @@ extern "C" int vx_ga_adam(const vx_ga_problem* pb, int t0, int iters, double lr,
   if (graph) cudaGraphDestroy(graph);
   cudaStreamDestroy(cap);
   if (err != cudaSuccess) return fail_cuda(err, "ga adam graph");
+  count_launches((uint64_t)iters * iteration_kernels(*pb));
   return VX_OK;
 }
 
@@ -688,6 +691,6 @@ extern "C" int vx_ga_adaptive_weights(const double* e, int64_t K, const double* 
   ga_hist_kernel<<<blocks, 256, 0, st>>>(e, K, edges, n_bins, counts);
   ga_density_kernel<<<1, GA_W_THREADS, 0, st>>>(e, K, edges, n_bins, counts, out_stats);
   ga_weight_kernel<<<blocks, 256, 0, st>>>(e, K, edges, n_bins, out_stats, alpha, w);
-  VX_CHECK_LAUNCH("ga adaptive weights launch");
+  VX_CHECK_LAUNCH_N("ga adaptive weights launch", 3);
   return VX_OK;
 }

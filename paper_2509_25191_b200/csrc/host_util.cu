@@ -1,5 +1,6 @@
 #include <cudaTypedefs.h>
 
+#include <atomic>
 #include <cstdarg>
 #include <mutex>
 
@@ -21,6 +22,9 @@ int fail_cuda(cudaError_t e, const char* where) {
   set_error("%s: %s", where, cudaGetErrorString(e));
   return VX_E_CUDA;
 }
+
+static std::atomic<uint64_t> g_launches{0};
+void count_launches(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 int num_sms() {
   static int n = 0;
@@ -80,3 +84,5 @@ const char* vx_last_error(void) { return vx::g_err; }
 int vx_num_sms(void) { return vx::num_sms(); }
 const char* vx_version(void) { return "vx 0.1 sm_100a"; }
 }
+
+extern "C" uint64_t vx_launch_count(void) { return vx::g_launches.load(std::memory_order_relaxed); }

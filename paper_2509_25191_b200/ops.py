@@ -63,7 +63,7 @@ EXPORTED_SYMBOLS = ("vx_gemm", "vx_attention", "vx_attention_merge", "vx_layerno
                     "vx_upsample_bilinear", "vx_gemm_spatial", "vx_epipolar_residuals",
                     "vx_epipolar_accumulate", "vx_ga_decode", "vx_ga_residuals", "vx_ga_loss_grad",
                     "vx_ga_adam", "vx_ga_adaptive_weights", "vx_matched_points", "vx_unproject_depth",
-                    "vx_select_pairs", "vx_pairwise_errors", "vx_num_sms", "vx_last_error", "vx_version")
+                    "vx_select_pairs", "vx_pairwise_errors", "vx_num_sms", "vx_launch_count", "vx_last_error", "vx_version")
 
 _lib = None
 
@@ -105,8 +105,9 @@ def load_library(path: os.PathLike | None = None) -> ctypes.CDLL:
     lib.vx_pairwise_errors.argtypes = [_vp, _vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp]
     lib.vx_last_error.restype = ctypes.c_char_p
     lib.vx_version.restype = ctypes.c_char_p
+    lib.vx_launch_count.restype = ctypes.c_uint64
     for name in EXPORTED_SYMBOLS:
-        if name in ("vx_last_error", "vx_version"):
+        if name in ("vx_last_error", "vx_version", "vx_launch_count"):
             continue
         getattr(lib, name).restype = _i32
     if path is None:
@@ -114,8 +115,14 @@ def load_library(path: os.PathLike | None = None) -> ctypes.CDLL:
     return lib
 
 
-# number of vx kernel launches issued by this process (bench.py's gpu_launches)
+# number of vx C-ABI calls issued by this process
 launch_count = 0
+
+
+def kernel_launches() -> int:
+    """Kernels libvx has launched in this process (bench.py's gpu_launches; vx_launch_count)."""
+    load_library()
+    return int(_lib.vx_launch_count())
 
 
 def _check(status: int, what: str):

@@ -10,7 +10,7 @@ ROOT = Path(__file__).resolve().parent.parent
 
 def declared_symbols():
     text = (ROOT / "include" / "vx_api.h").read_text()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*|void)\s+(vx_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|uint64_t|const char\*|void)\s+(vx_\w+)\s*\(", text, re.M)))
 
 
 def test_header_declares_entry_points():
@@ -56,3 +56,14 @@ def test_sass_contains_tcgen05_and_tma():
     assert "LDTM" in sass
     assert "UTMALDG" in sass
     assert "HMMA" not in sass.replace("UTCHMMA", "")
+
+
+def test_launch_counter_ignores_rejected_calls():
+    """vx_launch_count (bench.py's gpu_launches) counts kernels, not calls: a call rejected by
+    argument validation launches nothing."""
+    from paper_2509_25191_b200 import ops
+    lib = ops.load_library()
+    before = ops.kernel_launches()
+    rc = lib.vx_layernorm(None, 0, 0, None, 0, 0, None, None, 0, 0, 1e-5, None)
+    assert rc != 0
+    assert ops.kernel_launches() == before == lib.vx_launch_count()
