@@ -167,3 +167,12 @@ def test_sharded_embed_matches_global_slice():
     ws_head = alloc_workspace(cfg, 2)
     embed(W, imgs[:2].contiguous(), ws_head, frame0_is_first=True)
     assert torch.equal(ws_head.x[: 2 * N], ws_all.x[: 2 * N])
+
+
+def test_vggt1b_eight_views():
+    """VGGT-1B-shaped, S = 8: global attention has 16 x 22 = 352 work units (2 waves + 56), so its
+    last wave runs KV-split, inside a full forward against the oracle."""
+    cfg = vggt_1b()
+    sd = make_state_dict(cfg, 0)
+    images = synthetic_images(cfg, 8, 3)
+    _check(cfg, sd, images, _oracle(cfg, sd, images), "1b-s8")
