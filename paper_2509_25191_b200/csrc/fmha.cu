@@ -20,10 +20,12 @@
 //   w2      TMEM allocator
 //   w4..    softmax + epilogue: one warpgroup per Q tile; thread = one query row = one TMEM
 //           lane owning all score columns of the KV tile (row max / sum thread-local).
-// Softmax arithmetic: x = s*scale*log2e - m with FFMA2 (packed fp32x2), 2 of every 8 exp pairs
-// on the FMA pipe (packed degree-3 polynomial), the rest on MUFU ex2; FMNMX3 max tree; lazy
-// rescaling of O only when the running max grows by > 2^8.  The column mask of the last KV tile
-// lives on a separate code path (BoolTag) so the common path carries none.
+// Softmax arithmetic: x = s*scale*log2e - m with FFMA2 (packed fp32x2), 1 of every 8 exp pairs
+// on the FMA pipe (packed degree-2 polynomial), the rest on MUFU ex2; FMNMX3 max tree; lazy
+// rescaling of O only when the running max grows by > 2^8.  Because m only moves past that
+// threshold, the exps of a tile start with the running max and the tile max is computed alongside
+// them (speculative; a warp with a row over the threshold redoes the tile).  The column mask of
+// the last KV tile lives on a separate code path (BoolTag) so the common path carries none.
 #include <math.h>
 #include <stdlib.h>
 
@@ -155,12 +157,15 @@ constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
 
 
 // EMU_PAIRS_OF_8: of every 8 exp pairs, this many use the FMA-pipe polynomial
-template <int D, int EMU_PAIRS_OF_8, int NT_, int BKV_, bool ALIAS_, bool SUMV_, bool NOHINT = false>
+template <int D, int EMU_PAIRS_OF_8, int NT_, int BKV_, bool ALIAS_, bool SUMV_, bool NOHINT = false,
+          bool SPEC_ = false>
 __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS, 1)
     fmha_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                 const __grid_constant__ CUtensorMap tmV, const AttnArgs a) {
   using Cfg = AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>;
   constexpr bool ALIAS = ALIAS_;
+  // speculative exps (step_spec) need P writes that can be repeated before p_full: aliased kernels only
+  constexpr bool SPEC = SPEC_ && ALIAS_;
   constexpr bool SUMV = SUMV_;
   constexpr int DO = Cfg::DO;
   constexpr int BKV = Cfg::BKV;
@@ -438,12 +443,8 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
           if (lane == 0) mbar_arrive(&s_free[tile]);
         }
         const int valid = a.Lk - BKV * (wi.j0 + j);
-        auto step = [&](auto mask_tag) {
-          if constexpr (decltype(mask_tag)::value) {
-#pragma unroll
-            for (int c = 0; c < BKV; ++c)
-              if (c >= valid) sr[c] = 0xff800000u;
-          }
+        // row max of the tile (FMNMX3 chains), in log2 units
+        auto tile_max = [&]() -> float {
           constexpr int CH = BKV / 16;  // independent FMNMX3 chains
           float mq[CH];
 #pragma unroll
@@ -455,13 +456,12 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
           float mx = mq[0];
 #pragma unroll
           for (int q = 1; q < CH; ++q) mx = fmaxf(mx, mq[q]);
-          const float m_new = mx * sl2;
-          const bool need = m_new > m_run + RESCALE_THRESHOLD;
-          const float alpha = need ? ex2(m_run - m_new) : 1.0f;
-          if (need) m_run = m_new;
-          const uint64_t NEGM = f2_pack(-m_run, -m_run);
-          VX_TRACE(trace_slot_sm(unit_n, wl, lane, tile, j, 2));
-          uint64_t acc[4] = {0, 0, 0, 0};
+          return mx * sl2;
+        };
+        // P = 2^(s * scale * log2e - m) for the whole tile, packed to bf16 and stored over S
+        uint64_t acc[4];
+        auto exps = [&](const uint64_t NEGM) {
+          acc[0] = acc[1] = acc[2] = acc[3] = 0;
           constexpr int NCHUNK = (BKV + 63) / 64;
 #pragma unroll
           for (int hf = 0; hf < NCHUNK; ++hf) {
@@ -495,28 +495,65 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
             if constexpr (PAIRS == 24) tmem_st8(P_addr + 32 * hf + 16, pk + 16);
             else tmem_st_n<PAIRS>(P_addr + 32 * hf, pk);
           }
+        };
+        auto rescale_o = [&](const float alpha) {
+          uint32_t orr[32];
+#pragma unroll
+          for (int c0 = 0; c0 < DO; c0 += 32) {
+            const int w = DO - c0 >= 32 ? 32 : 16;
+            if (w == 32) tmem_ld32(O_addr + c0, orr);
+            else tmem_ld16(O_addr + c0, orr);
+            tmem_wait_ld();
+#pragma unroll
+            for (int c = 0; c < 32; ++c) orr[c] = __float_as_uint(__uint_as_float(orr[c]) * alpha);
+            if (w == 32) tmem_st32(O_addr + c0, orr);
+            else tmem_st16(O_addr + c0, orr);
+          }
+        };
+        auto row_sums = [&](const float alpha) {
           if constexpr (!SUMV) {
             float a0, a1, b0, b1;
             f2_unpack(f2_add(acc[0], acc[1]), a0, a1);
             f2_unpack(f2_add(acc[2], acc[3]), b0, b1);
             l_run = l_run * alpha + ((a0 + a1) + (b0 + b1));
           }
-          if (__any_sync(0xffffffff, need) && j > 0) {
-            uint32_t orr[32];
+        };
+        // exact: max first, then exps with the (possibly raised) running max
+        auto step = [&](auto mask_tag) {
+          if constexpr (decltype(mask_tag)::value) {
 #pragma unroll
-            for (int c0 = 0; c0 < DO; c0 += 32) {
-              const int w = DO - c0 >= 32 ? 32 : 16;
-              if (w == 32) tmem_ld32(O_addr + c0, orr);
-              else tmem_ld16(O_addr + c0, orr);
-              tmem_wait_ld();
-#pragma unroll
-              for (int c = 0; c < 32; ++c) orr[c] = __float_as_uint(__uint_as_float(orr[c]) * alpha);
-              if (w == 32) tmem_st32(O_addr + c0, orr);
-              else tmem_st16(O_addr + c0, orr);
-            }
+            for (int c = 0; c < BKV; ++c)
+              if (c >= valid) sr[c] = 0xff800000u;
+          }
+          const float m_new = tile_max();
+          const bool need = m_new > m_run + RESCALE_THRESHOLD;
+          const float alpha = need ? ex2(m_run - m_new) : 1.0f;
+          if (need) m_run = m_new;
+          VX_TRACE(trace_slot_sm(unit_n, wl, lane, tile, j, 2));
+          exps(f2_pack(-m_run, -m_run));
+          row_sums(alpha);
+          if (__any_sync(0xffffffff, need) && j > 0) rescale_o(alpha);
+        };
+        // speculative (unmasked tiles after the first): the running max almost never moves by more
+        // than the threshold, so the exps start with it right away and the tile max is computed
+        // alongside (off the critical path); a warp with a row that does need the new max redoes
+        // the tile (rare)
+        auto step_spec = [&]() {
+          exps(f2_pack(-m_run, -m_run));
+          const float m_new = tile_max();
+          const bool need = m_new > m_run + RESCALE_THRESHOLD;
+          if (__any_sync(0xffffffff, need)) {
+            const float alpha = need ? ex2(m_run - m_new) : 1.0f;
+            if (need) m_run = m_new;
+            exps(f2_pack(-m_run, -m_run));
+            row_sums(alpha);
+            rescale_o(alpha);
+          } else {
+            row_sums(1.0f);
           }
         };
         if (valid < BKV) step(BoolTag<true>{});
+        else if (SPEC && j > 0) step_spec();
         else step(BoolTag<false>{});
         tmem_wait_st();
         tc_fence_before();
@@ -703,7 +740,7 @@ static float* split_scratch(cudaStream_t st, size_t floats) {
 }
 
 template <int D, int EMU, int NT = (D == 128 ? 1 : 2), int BKV = 128, bool ALIAS = false, bool SUMV = false,
-          bool NOHINT = false>
+          bool NOHINT = false, bool SPEC = false>
 static int launch_fmha(const void* q, const void* k, const void* v, AttnArgs args, cudaStream_t st) {
   using Cfg = AttnCfg<D, NT, BKV, ALIAS, SUMV>;
   CUtensorMap tq, tk, tv;
@@ -724,7 +761,9 @@ static int launch_fmha(const void* q, const void* k, const void* v, AttnArgs arg
     const char* e = getenv("VX_FMHA_SPLIT");  // diagnostic: 0 disables the KV-split tail
     return !(e && atoi(e) == 0);
   }();
-  if (split_on && tail > 0 && 2 * tail <= sms) {
+  // only for long units: each split costs a merge launch and fp32 partial round trips, which a
+  // frame-attention unit (29 KV tiles) does not earn back (S=20 frame layer 0.215 -> 0.228 ms)
+  if (split_on && tail > 0 && 2 * tail <= sms && args.kv_tiles >= 128) {
     int parts = sms / tail;
     if (parts > args.kv_tiles / 2) parts = args.kv_tiles / 2;  // >= 2 KV tiles per item
     if (parts >= 2 && (int64_t)parts * args.kv_tiles < (1ll << 31)) {
@@ -738,7 +777,7 @@ static int launch_fmha(const void* q, const void* k, const void* v, AttnArgs arg
     }
   }
   args.work = args.split_from + (args.units - args.split_from) * args.parts;
-  auto kern = fmha_kernel<D, EMU, NT, BKV, ALIAS, SUMV, NOHINT>;
+  auto kern = fmha_kernel<D, EMU, NT, BKV, ALIAS, SUMV, NOHINT, SPEC>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
@@ -787,31 +826,32 @@ static int attention_impl(const void* q, const void* k, const void* v, void* out
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   static int emu = [] {
     const char* e = getenv("VX_FMHA_EMU");  // diagnostic: exp pairs (of 8) on the FMA pipe
-    return e ? atoi(e) : 2;
+    return e ? atoi(e) : 1;
   }();
   static int cfg = [] {
-    const char* e = getenv("VX_FMHA_CFG");  // diagnostic: 0 default (4x48 + ones panel), 1 = 2x128, 3 = 3x64,
-                                            // 4 = 4x64 aliased
+    const char* e = getenv("VX_FMHA_CFG");  // diagnostic kernel variants, see below
     return e ? atoi(e) : 0;
   }();
   if (D == 64) {
     // default (frame and global layers): 4 Q tiles x 48-wide KV tiles, P aliased onto S, row sums
-    // from a ones panel appended to V (tools/sweep_sumv.sh: global 1013 / frame 740 TFLOP/s at 20
-    // views vs 991 / 719 for 4x64-aliased and 971 / 733 for 3x64 run-ahead)
+    // from a ones panel appended to V, S-ready / P-ready waits without a suspend-time hint, exps
+    // started with the running max (speculative; the tile max is checked afterwards) and 1 of 8
+    // exp pairs on the FMA pipe. Sustained S=200 global layer (tools/sustain_attn.sh): 920 TFLOP/s
+    // vs 910 for the exact-max kernel with 2 of 8 pairs (VX_FMHA_CFG=13).
     switch (cfg) {
-      case 1: return launch_fmha<64, 2, 2, 128>(q, k, v, a, st);
-      case 3: return launch_fmha<64, 2, 3, 64>(q, k, v, a, st);
-      case 4: return launch_fmha<64, 2, 4, 64, true>(q, k, v, a, st);
-      case 14: return launch_fmha<64, 2, 4, 48, true, true, false>(q, k, v, a, st);  // suspend-hint waits
-      case 15: return launch_fmha<64, 2, 4, 48, true, false, true>(q, k, v, a, st);  // FADD row sums
+      case 1: return launch_fmha<64, 2, 2, 128>(q, k, v, a, st);                       // 2 x 128 run-ahead
+      case 3: return launch_fmha<64, 2, 3, 64>(q, k, v, a, st);                        // 3 x 64 run-ahead
+      case 4: return launch_fmha<64, 2, 4, 64, true>(q, k, v, a, st);                  // 4 x 64 aliased
+      case 13: return launch_fmha<64, 2, 4, 48, true, true, true>(q, k, v, a, st);     // exact max
+      case 14: return launch_fmha<64, 2, 4, 48, true, true, false>(q, k, v, a, st);    // + suspend-hint waits
+      case 15: return launch_fmha<64, 2, 4, 48, true, false, true>(q, k, v, a, st);    // FADD row sums
       case 16: return launch_fmha<64, 1, 4, 48, true, false, true>(q, k, v, a, st);
       default: break;
     }
-    switch (emu) {  // S-ready / P-ready waits without a suspend-time hint: +0.4% (tools/exp_nohint.sh)
-      case 0: return launch_fmha<64, 0, 4, 48, true, true, true>(q, k, v, a, st);
-      case 1: return launch_fmha<64, 1, 4, 48, true, true, true>(q, k, v, a, st);
-      case 3: return launch_fmha<64, 3, 4, 48, true, true, true>(q, k, v, a, st);
-      default: return launch_fmha<64, 2, 4, 48, true, true, true>(q, k, v, a, st);
+    switch (emu) {
+      case 0: return launch_fmha<64, 0, 4, 48, true, true, true, true>(q, k, v, a, st);
+      case 2: return launch_fmha<64, 2, 4, 48, true, true, true, true>(q, k, v, a, st);
+      default: return launch_fmha<64, 1, 4, 48, true, true, true, true>(q, k, v, a, st);
     }
   }
   if (D == 128) return launch_fmha<128, 2>(q, k, v, a, st);

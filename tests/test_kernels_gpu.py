@@ -177,8 +177,9 @@ def test_attention_large_logits_rescale(ops, L):
 
 
 @pytest.mark.parametrize("Lq,Lk", [(700, 1900), (333, 6000), (4200, 257),
-                                   # 600 units = 4 full waves + 8: the 8 tail units run KV-split (18 parts)
-                                   (512 * 149 + 100, 3000)])
+                                   # 4 heads x 38 Q blocks = 152 units = 1 wave + 4: the 4 tail units run
+                                   # KV-split (37 parts; split needs >= 128 KV tiles per unit)
+                                   (512 * 37 + 100, 6200)])
 def test_attention_cross_lengths(ops, Lq, Lk):
     # ring-step shape: local queries against a remote K/V shard of another length
     H, D = 4, 64
@@ -340,8 +341,8 @@ def test_upsample_bilinear_matches_interpolate(ops):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("shards,Lq", [([700], 600), ([300, 411], 600), ([513, 200, 333, 90], 600),
-                                       # 600 units = 4 waves + 8: KV-split tail in every merge mode
-                                       ([3000], 512 * 149 + 100), ([2000, 1500, 2500], 512 * 149 + 100)])
+                                       # 152 units = 1 wave + 4: KV-split tail in every merge mode
+                                       ([6200], 512 * 37 + 100), ([6200, 6300, 6150], 512 * 37 + 100)])
 def test_attention_ring_merge_matches_full(ops, shards, Lq):
     # the ring's fused-merge steps (vx_attention_merge) over K/V shards == attention over all keys
     H, D = 4, 64
