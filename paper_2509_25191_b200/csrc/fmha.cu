@@ -158,7 +158,7 @@ constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
 
 // EMU_PAIRS_OF_8: of every 8 exp pairs, this many use the FMA-pipe polynomial
 template <int D, int EMU_PAIRS_OF_8, int NT_, int BKV_, bool ALIAS_, bool SUMV_, bool NOHINT = false,
-          bool SPEC_ = false>
+          bool SPEC_ = false, bool LDSPLIT = false>
 __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS, 1)
     fmha_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                 const __grid_constant__ CUtensorMap tmV, const AttnArgs a) {
@@ -435,14 +435,24 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
         sph ^= 1;
         tc_fence_after();
         uint32_t sr[BKV];
-        tmem_ld_n<BKV>(S_addr, sr);
-        tmem_wait_ld();
+        const int valid = a.Lk - BKV * (wi.j0 + j);
+        // speculative tiles (48 wide) leave the last 16 S columns in flight: the first 16 exp pairs
+        // only need columns 0-31, and the wait for the rest sits just before pair 16
+        constexpr bool SPLIT_LD = SPEC && LDSPLIT && BKV == 48;
+        const bool spec_now = SPEC && j > 0 && valid >= BKV;
+        if (SPLIT_LD && spec_now) {
+          tmem_ld32(S_addr, sr);
+          tmem_wait_ld();
+          tmem_ld16(S_addr + 32, sr + 32);
+        } else {
+          tmem_ld_n<BKV>(S_addr, sr);
+          tmem_wait_ld();
+        }
         if constexpr (!ALIAS) {
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&s_free[tile]);
         }
-        const int valid = a.Lk - BKV * (wi.j0 + j);
         // row max of the tile (FMNMX3 chains), in log2 units
         auto tile_max = [&]() -> float {
           constexpr int CH = BKV / 16;  // independent FMNMX3 chains
@@ -460,7 +470,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
         };
         // P = 2^(s * scale * log2e - m) for the whole tile, packed to bf16 and stored over S
         uint64_t acc[4];
-        auto exps = [&](const uint64_t NEGM) {
+        auto exps = [&](const uint64_t NEGM, auto mid_wait) {
           acc[0] = acc[1] = acc[2] = acc[3] = 0;
           constexpr int NCHUNK = (BKV + 63) / 64;
 #pragma unroll
@@ -469,6 +479,9 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
             uint32_t pk[PAIRS];
 #pragma unroll
             for (int c = 0; c < PAIRS; ++c) {
+              if constexpr (decltype(mid_wait)::value && PAIRS == 24) {
+                if (c == 16) tmem_wait_ld_dep16(sr + 32);
+              }
               const int e = 64 * hf + 2 * c;
               const uint64_t x = f2_fma(f2_pack(__uint_as_float(sr[e]), __uint_as_float(sr[e + 1])), SL2, NEGM);
               float x0, x1, p0, p1;
@@ -530,7 +543,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
           const float alpha = need ? ex2(m_run - m_new) : 1.0f;
           if (need) m_run = m_new;
           VX_TRACE(trace_slot_sm(unit_n, wl, lane, tile, j, 2));
-          exps(f2_pack(-m_run, -m_run));
+          exps(f2_pack(-m_run, -m_run), BoolTag<false>{});
           row_sums(alpha);
           if (__any_sync(0xffffffff, need) && j > 0) rescale_o(alpha);
         };
@@ -539,13 +552,13 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
         // alongside (off the critical path); a warp with a row that does need the new max redoes
         // the tile (rare)
         auto step_spec = [&]() {
-          exps(f2_pack(-m_run, -m_run));
+          exps(f2_pack(-m_run, -m_run), BoolTag<SPLIT_LD>{});
           const float m_new = tile_max();
           const bool need = m_new > m_run + RESCALE_THRESHOLD;
           if (__any_sync(0xffffffff, need)) {
             const float alpha = need ? ex2(m_run - m_new) : 1.0f;
             if (need) m_run = m_new;
-            exps(f2_pack(-m_run, -m_run));
+            exps(f2_pack(-m_run, -m_run), BoolTag<false>{});
             row_sums(alpha);
             rescale_o(alpha);
           } else {
@@ -553,7 +566,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
           }
         };
         if (valid < BKV) step(BoolTag<true>{});
-        else if (SPEC && j > 0) step_spec();
+        else if (spec_now) step_spec();
         else step(BoolTag<false>{});
         tmem_wait_st();
         tc_fence_before();
@@ -740,7 +753,7 @@ static float* split_scratch(cudaStream_t st, size_t floats) {
 }
 
 template <int D, int EMU, int NT = (D == 128 ? 1 : 2), int BKV = 128, bool ALIAS = false, bool SUMV = false,
-          bool NOHINT = false, bool SPEC = false>
+          bool NOHINT = false, bool SPEC = false, bool LDSPLIT = false>
 static int launch_fmha(const void* q, const void* k, const void* v, AttnArgs args, cudaStream_t st) {
   using Cfg = AttnCfg<D, NT, BKV, ALIAS, SUMV>;
   CUtensorMap tq, tk, tv;
@@ -777,7 +790,7 @@ static int launch_fmha(const void* q, const void* k, const void* v, AttnArgs arg
     }
   }
   args.work = args.split_from + (args.units - args.split_from) * args.parts;
-  auto kern = fmha_kernel<D, EMU, NT, BKV, ALIAS, SUMV, NOHINT, SPEC>;
+  auto kern = fmha_kernel<D, EMU, NT, BKV, ALIAS, SUMV, NOHINT, SPEC, LDSPLIT>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
@@ -836,8 +849,9 @@ static int attention_impl(const void* q, const void* k, const void* v, void* out
     // default (frame and global layers): 4 Q tiles x 48-wide KV tiles, P aliased onto S, row sums
     // from a ones panel appended to V, S-ready / P-ready waits without a suspend-time hint, exps
     // started with the running max (speculative; the tile max is checked afterwards) and 1 of 8
-    // exp pairs on the FMA pipe. Sustained S=200 global layer (tools/sustain_attn.sh): 920 TFLOP/s
-    // vs 910 for the exact-max kernel with 2 of 8 pairs (VX_FMHA_CFG=13).
+    // exp pairs on the FMA pipe, the last 16 S columns loaded behind the first 16 exp pairs.
+    // Sustained S=200 global layer (tools/sustain_attn.sh): 914 TFLOP/s vs 905 for the exact-max
+    // kernel with 2 of 8 pairs (VX_FMHA_CFG=13); the split S load adds +0.6% (VX_FMHA_CFG=20 without).
     switch (cfg) {
       case 1: return launch_fmha<64, 2, 2, 128>(q, k, v, a, st);                       // 2 x 128 run-ahead
       case 3: return launch_fmha<64, 2, 3, 64>(q, k, v, a, st);                        // 3 x 64 run-ahead
@@ -846,12 +860,13 @@ static int attention_impl(const void* q, const void* k, const void* v, void* out
       case 14: return launch_fmha<64, 2, 4, 48, true, true, false>(q, k, v, a, st);    // + suspend-hint waits
       case 15: return launch_fmha<64, 2, 4, 48, true, false, true>(q, k, v, a, st);    // FADD row sums
       case 16: return launch_fmha<64, 1, 4, 48, true, false, true>(q, k, v, a, st);
+      case 20: return launch_fmha<64, 1, 4, 48, true, true, true, true, false>(q, k, v, a, st);  // one S load
       default: break;
     }
     switch (emu) {
-      case 0: return launch_fmha<64, 0, 4, 48, true, true, true, true>(q, k, v, a, st);
-      case 2: return launch_fmha<64, 2, 4, 48, true, true, true, true>(q, k, v, a, st);
-      default: return launch_fmha<64, 1, 4, 48, true, true, true, true>(q, k, v, a, st);
+      case 0: return launch_fmha<64, 0, 4, 48, true, true, true, true, true>(q, k, v, a, st);
+      case 2: return launch_fmha<64, 2, 4, 48, true, true, true, true, true>(q, k, v, a, st);
+      default: return launch_fmha<64, 1, 4, 48, true, true, true, true, true>(q, k, v, a, st);
     }
   }
   if (D == 128) return launch_fmha<128, 2>(q, k, v, a, st);
