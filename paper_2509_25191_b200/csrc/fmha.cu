@@ -280,24 +280,26 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
       constexpr uint32_t idesc_pv = make_idesc_bf16(128, DO, 0, 1);
       const uint32_t q0 = smem_u32(sQ);
       constexpr int KSTEPS_PER_PANEL = Cfg::PANEL_COLS / 16;
+      // descriptors: one base per operand, offsets added in 16-byte units (smem addresses < 256 KB
+      // keep the 14-bit start-address field from carrying into the next field)
+      const uint64_t qdesc0 = make_sdesc(q0, 16, Cfg::SBO, Cfg::LAYOUT);
       auto issue_qk = [&](int i, uint32_t ks) {
-        const uint32_t qs = q0 + i * Cfg::Q_TILE_BYTES;
+        const uint64_t kd = make_sdesc(ks, 16, Cfg::SBO, Cfg::LAYOUT);
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const uint32_t kstep = (k % KSTEPS_PER_PANEL) * 32;
-          const uint32_t qoff = (k / KSTEPS_PER_PANEL) * Cfg::QPANEL_BYTES + kstep;
+          const uint32_t qoff = i * Cfg::Q_TILE_BYTES + (k / KSTEPS_PER_PANEL) * Cfg::QPANEL_BYTES + kstep;
           const uint32_t koff = (k / KSTEPS_PER_PANEL) * Cfg::KVPANEL_BYTES + kstep;
-          if (lead) mma_ss(tmem + Cfg::tS(i), make_sdesc(qs + qoff, 16, Cfg::SBO, Cfg::LAYOUT),
-                 make_sdesc(ks + koff, 16, Cfg::SBO, Cfg::LAYOUT), idesc_qk, k > 0);
+          mma_ss_if(lead, tmem + Cfg::tS(i), qdesc0 + (qoff >> 4), kd + (koff >> 4), idesc_qk, k > 0);
         }
       };
       // V is the MN-major B operand: for D = 128 its two 64-column panels are the two MN atoms (LBO)
       auto issue_pv = [&](int i, uint32_t vs, uint32_t acc) {
+        const uint64_t vd = make_sdesc(vs, Cfg::KVPANEL_BYTES, Cfg::SBO, Cfg::LAYOUT);
 #pragma unroll
         for (int kk = 0; kk < BKV / 16; ++kk)
-          if (lead) mma_ts(tmem + Cfg::tO(i), tmem + Cfg::tP(i) + kk * 8,
-                 make_sdesc(vs + kk * 16 * Cfg::ROW_BYTES, Cfg::KVPANEL_BYTES, Cfg::SBO, Cfg::LAYOUT), idesc_pv,
-                 (acc | kk) != 0);
+          mma_ts_if(lead, tmem + Cfg::tO(i), tmem + Cfg::tP(i) + kk * 8, vd + ((kk * 16 * Cfg::ROW_BYTES) >> 4),
+                    idesc_pv, (acc | kk) != 0);
       };
       uint32_t c = 0;  // global K/V tile counter
       uint32_t n = 0;  // local unit counter
@@ -314,10 +316,10 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
             const uint32_t ks = smem_u32(sK + st * Cfg::KV_TILE_BYTES);
             for (int i = 0; i < NT; ++i) {
               issue_qk(i, ks);
-              if (lead) mma_commit(&s_full[i]);
+              mma_commit_if(lead, &s_full[i]);
             }
-            if (lead) mma_commit(&k_empty[st]);
-            if (nkv == 1 && lead) mma_commit(q_empty);
+            mma_commit_if(lead, &k_empty[st]);
+            mma_commit_if(lead && nkv == 1, q_empty);
           }
           for (int j = 0; j < nkv; ++j, ++c) {
             const uint32_t st = c % KST, ph = (c / KST) & 1;
@@ -337,17 +339,17 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
               issue_pv(i, vs, j > 0);
               if (has_next) {  // overwrites P_i(j): executes after PV_i(j) (tcgen05 issue order)
                 issue_qk(i, nks);
-                if (lead) mma_commit(&s_full[i]);
+                mma_commit_if(lead, &s_full[i]);
                 VX_TRACE(trace_slot_mma(int(n), j, i, 1));
               } else {
-                if (lead) mma_commit(&p_free[i]);  // last PV of the unit
+                mma_commit_if(lead, &p_free[i]);  // last PV of the unit
               }
             }
             pfull_ph ^= 1;
-            if (lead) mma_commit(&v_empty[st]);
+            mma_commit_if(lead, &v_empty[st]);
             if (has_next) {
-              if (lead) mma_commit(&k_empty[nst]);
-              if (j + 2 == nkv && lead) mma_commit(q_empty);
+              mma_commit_if(lead, &k_empty[nst]);
+              mma_commit_if(lead && j + 2 == nkv, q_empty);
             }
           }
         }
@@ -365,11 +367,11 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
               if (n > 0) mbar_wait(&s_free[i], sfree_ph);
               tc_fence_after();
               issue_qk(i, ks);
-              if (lead) mma_commit(&s_full[i]);
+              mma_commit_if(lead, &s_full[i]);
             }
             if (n > 0) sfree_ph ^= 1;
-            if (lead) mma_commit(&k_empty[st]);
-            if (nkv == 1 && lead) mma_commit(q_empty);
+            mma_commit_if(lead, &k_empty[st]);
+            mma_commit_if(lead && nkv == 1, q_empty);
           }
           for (int j = 0; j < nkv; ++j, ++c) {
             const uint32_t st = c % KST, ph = (c / KST) & 1;
@@ -381,11 +383,11 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
                 mbar_wait(&s_free[i], sfree_ph);
                 tc_fence_after();
                 issue_qk(i, nks);
-                if (lead) mma_commit(&s_full[i]);
+                mma_commit_if(lead, &s_full[i]);
               }
               sfree_ph ^= 1;
-              if (lead) mma_commit(&k_empty[nst]);
-              if (j + 2 == nkv && lead) mma_commit(q_empty);
+              mma_commit_if(lead, &k_empty[nst]);
+              mma_commit_if(lead && j + 2 == nkv, q_empty);
             }
             const uint32_t vs = smem_u32(sV + st * Cfg::V_STAGE_BYTES);
             mbar_wait(&v_full[st], ph);
@@ -395,10 +397,10 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
               mbar_wait(&p_full[i], pfull_ph);
               tc_fence_after();
               issue_pv(i, vs, j > 0);
-              if (lead) mma_commit(&p_free[i]);
+              mma_commit_if(lead, &p_free[i]);
             }
             pfull_ph ^= 1;
-            if (lead) mma_commit(&v_empty[st]);
+            mma_commit_if(lead, &v_empty[st]);
           }
         }
       }
