@@ -20,7 +20,7 @@
 //   w2      TMEM allocator
 //   w4..    softmax + epilogue: one warpgroup per Q tile; thread = one query row = one TMEM
 //           lane owning all score columns of the KV tile (row max / sum thread-local).
-// Softmax arithmetic: x = s*scale*log2e - m with FFMA2 (packed fp32x2), 1 of every 8 exp pairs
+// Softmax arithmetic: x = s*scale*log2e - m with FFMA2 (packed fp32x2), 2 of every 8 exp pairs
 // on the FMA pipe (packed degree-2 polynomial), the rest on MUFU ex2; FMNMX3 max tree; lazy
 // rescaling of O only when the running max grows by > 2^8.  Because m only moves past that
 // threshold, the exps of a tile start with the running max and the tile max is computed alongside
@@ -841,7 +841,7 @@ static int attention_impl(const void* q, const void* k, const void* v, void* out
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   static int emu = [] {
     const char* e = getenv("VX_FMHA_EMU");  // diagnostic: exp pairs (of 8) on the FMA pipe
-    return e ? atoi(e) : 1;
+    return e ? atoi(e) : 2;
   }();
   static int cfg = [] {
     const char* e = getenv("VX_FMHA_CFG");  // diagnostic kernel variants, see below
@@ -850,10 +850,10 @@ static int attention_impl(const void* q, const void* k, const void* v, void* out
   if (D == 64) {
     // default (frame and global layers): 4 Q tiles x 48-wide KV tiles, P aliased onto S, row sums
     // from a ones panel appended to V, S-ready / P-ready waits without a suspend-time hint, exps
-    // started with the running max (speculative; the tile max is checked afterwards) and 1 of 8
-    // exp pairs on the FMA pipe, the last 16 S columns loaded behind the first 16 exp pairs.
-    // Sustained S=200 global layer (tools/sustain_attn.sh): 914 TFLOP/s vs 905 for the exact-max
-    // kernel with 2 of 8 pairs (VX_FMHA_CFG=13); the split S load adds +0.6% (VX_FMHA_CFG=20 without).
+    // started with the running max (speculative; the tile max is checked afterwards) and 2 of 8
+    // exp pairs on the FMA pipe, the last 16 S columns loaded behind the first 16 exp pairs, and a
+    // branch-free MMA issue path. Sustained S=200 global layer (tools/sustain_attn.sh): 954
+    // TFLOP/s (EMU 1: 923, 3: 922, 4: 887); isolated S=20: 1089.
     switch (cfg) {
       case 1: return launch_fmha<64, 2, 2, 128>(q, k, v, a, st);                       // 2 x 128 run-ahead
       case 3: return launch_fmha<64, 2, 3, 64>(q, k, v, a, st);                        // 3 x 64 run-ahead
@@ -862,13 +862,14 @@ static int attention_impl(const void* q, const void* k, const void* v, void* out
       case 14: return launch_fmha<64, 2, 4, 48, true, true, false>(q, k, v, a, st);    // + suspend-hint waits
       case 15: return launch_fmha<64, 2, 4, 48, true, false, true>(q, k, v, a, st);    // FADD row sums
       case 16: return launch_fmha<64, 1, 4, 48, true, false, true>(q, k, v, a, st);
-      case 20: return launch_fmha<64, 1, 4, 48, true, true, true, true, false>(q, k, v, a, st);  // one S load
+      case 20: return launch_fmha<64, 2, 4, 48, true, true, true, true, false>(q, k, v, a, st);  // one S load
       default: break;
     }
     switch (emu) {
       case 0: return launch_fmha<64, 0, 4, 48, true, true, true, true, true>(q, k, v, a, st);
-      case 2: return launch_fmha<64, 2, 4, 48, true, true, true, true, true>(q, k, v, a, st);
-      default: return launch_fmha<64, 1, 4, 48, true, true, true, true, true>(q, k, v, a, st);
+      case 1: return launch_fmha<64, 1, 4, 48, true, true, true, true, true>(q, k, v, a, st);
+      case 3: return launch_fmha<64, 3, 4, 48, true, true, true, true, true>(q, k, v, a, st);
+      default: return launch_fmha<64, 2, 4, 48, true, true, true, true, true>(q, k, v, a, st);
     }
   }
   if (D == 128) return launch_fmha<128, 2>(q, k, v, a, st);
