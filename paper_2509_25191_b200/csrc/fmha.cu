@@ -283,14 +283,14 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
       // descriptors: one base per operand, offsets added in 16-byte units (smem addresses < 256 KB
       // keep the 14-bit start-address field from carrying into the next field)
       const uint64_t qdesc0 = make_sdesc(q0, 16, Cfg::SBO, Cfg::LAYOUT);
-      auto issue_qk = [&](int i, uint32_t ks) {
+      auto issue_qk = [&](int i, uint32_t ks, bool issue = true) {
         const uint64_t kd = make_sdesc(ks, 16, Cfg::SBO, Cfg::LAYOUT);
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const uint32_t kstep = (k % KSTEPS_PER_PANEL) * 32;
           const uint32_t qoff = i * Cfg::Q_TILE_BYTES + (k / KSTEPS_PER_PANEL) * Cfg::QPANEL_BYTES + kstep;
           const uint32_t koff = (k / KSTEPS_PER_PANEL) * Cfg::KVPANEL_BYTES + kstep;
-          mma_ss_if(lead, tmem + Cfg::tS(i), qdesc0 + (qoff >> 4), kd + (koff >> 4), idesc_qk, k > 0);
+          mma_ss_if(lead && issue, tmem + Cfg::tS(i), qdesc0 + (qoff >> 4), kd + (koff >> 4), idesc_qk, k > 0);
         }
       };
       // V is the MN-major B operand: for D = 128 its two 64-column panels are the two MN atoms (LBO)
@@ -337,13 +337,12 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
               VX_TRACE(trace_slot_mma(int(n), j, i, 0));
               tc_fence_after();
               issue_pv(i, vs, j > 0);
-              if (has_next) {  // overwrites P_i(j): executes after PV_i(j) (tcgen05 issue order)
-                issue_qk(i, nks);
-                mma_commit_if(lead, &s_full[i]);
-                VX_TRACE(trace_slot_mma(int(n), j, i, 1));
-              } else {
-                mma_commit_if(lead, &p_free[i]);  // last PV of the unit
-              }
+              // S_i(j+1) overwrites P_i(j): executes after PV_i(j) (tcgen05 issue order). Predicated
+              // rather than branched, so the issue path has no branch.
+              issue_qk(i, nks, has_next);
+              mma_commit_if(lead && has_next, &s_full[i]);
+              mma_commit_if(lead && !has_next, &p_free[i]);  // last PV of the unit
+              VX_TRACE(trace_slot_mma(int(n), j, i, 1));
             }
             pfull_ph ^= 1;
             mma_commit_if(lead, &v_empty[st]);
