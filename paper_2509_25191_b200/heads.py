@@ -233,11 +233,16 @@ class DPTHeadDevice:
             L.append((l, lr))
 
         def out_conv(r, o, hs, target, padded):
-            up = ops.upsample_bilinear(o, (target, target))
-            x = pad(f"oc{r}", target, target, Fh) if padded else empty(Fr, target, target, Fh)
-            ops.gemm_spatial(up.view(-1, Fh), self.cw[f"{sc}refinenet{r}.out_conv"],
-                             self.b[f"{sc}refinenet{r}.out_conv.bias"], Fr, target, target, out1=x, out1_pad=padded)
-            return x
+            # upstream: out_conv(interpolate(o)). A 1x1 conv commutes with bilinear resizing (both
+            # linear; the resize weights sum to 1, so the bias passes through), so the conv runs at
+            # the source resolution (~4x fewer pixels) and the resize writes the result, straight
+            # into the zero-bordered buffer the next 3x3 conv reads when `padded`
+            y = empty(Fr, hs, hs, Fh)
+            ops.gemm_spatial(o.view(-1, Fh), self.cw[f"{sc}refinenet{r}.out_conv"],
+                             self.b[f"{sc}refinenet{r}.out_conv.bias"], Fr, hs, hs, out1=y)
+            if padded:
+                return ops.upsample_bilinear(y, (target, target), out=pad(f"oc{r}", target, target, Fh), out_pad=True)
+            return ops.upsample_bilinear(y, (target, target))
 
         # refinenet4: RCU2(l4) -> upsample to layer3 size -> out_conv
         o, _ = self._rcu(f"{sc}refinenet4.resConfUnit2", L[3][0], L[3][1], Fr, sizes[3], dense_out=True)
