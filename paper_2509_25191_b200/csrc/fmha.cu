@@ -8,9 +8,9 @@
 // units, head-major so concurrently running CTAs share K/V through L2.
 //
 // d = 64 (default): NT = 4 tiles x 48-wide KV tiles.  TMEM (512 columns) per Q tile i:
-//   S_i [48 fp32, P_i bf16 written over it] | O_i [64 + 16 fp32].
+//   S_i [48 fp32, P_i bf16 written over it] | O_i [64 + 8 fp32].
 // V is extended by a constant panel of ones, so the PV MMA also accumulates the row sums of P
-// into O_i[:, 64] (same lazy rescaling as O; no FADD row sums).  With P aliased onto S the MMA
+// into O_i[:, 64] (same lazy rescaling as O; no FADD row sums); the PV MMA runs with N = 72.  With P aliased onto S the MMA
 // issuer runs PV_i(j) then S_i(j+1) into the same columns (tcgen05 executes in issue order).
 // Other shapes (d = 32 / 128, diagnostics): separate P columns, S(j+1) issued ahead of the softmax.
 //
@@ -81,7 +81,7 @@ struct AttnCfg {
   // SUMV: the row sums come out of the PV MMA: V is extended by a panel of ones (N = D + 16), so
   // O_i[:, D] accumulates sum_k P_ik with the same lazy rescaling as O — no FADD row sums
   static constexpr bool SUMV = SUMV_;
-  static constexpr int DO = D + (SUMV ? 16 : 0);           // O accumulator columns
+  static constexpr int DO = D + (SUMV ? 8 : 0);            // O accumulator columns (N of the PV MMA)
   static constexpr int NT = NT_;                           // 128-row Q tiles per CTA (TMEM budget)
   static constexpr int BKV = BKV_;                         // KV rows per tile (score columns)
   static constexpr int KST = D == 128 ? 2 : (BKV <= 64 ? 4 : 3);
@@ -514,14 +514,15 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
           uint32_t orr[32];
 #pragma unroll
           for (int c0 = 0; c0 < DO; c0 += 32) {
-            const int w = DO - c0 >= 32 ? 32 : 16;
+            const int w = DO - c0 >= 32 ? 32 : DO - c0;  // 32, 16 or 8 (never past this tile's O)
             if (w == 32) tmem_ld32(O_addr + c0, orr);
-            else tmem_ld16(O_addr + c0, orr);
+            else tmem_ld16(O_addr + c0, orr);  // an 8-wide tail reads 8 extra columns, unused
             tmem_wait_ld();
 #pragma unroll
             for (int c = 0; c < 32; ++c) orr[c] = __float_as_uint(__uint_as_float(orr[c]) * alpha);
             if (w == 32) tmem_st32(O_addr + c0, orr);
-            else tmem_st16(O_addr + c0, orr);
+            else if (w == 16) tmem_st16(O_addr + c0, orr);
+            else tmem_st8(O_addr + c0, orr);
           }
         };
         auto row_sums = [&](const float alpha) {
@@ -578,8 +579,9 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
       mbar_wait(&p_free[tile], pv_cnt & 1);
       ++pv_cnt;
       tc_fence_after();
-      uint32_t orr[DO];
-      tmem_ld_n<DO>(O_addr, orr);
+      constexpr int DL = (DO + 15) / 16 * 16;  // load width (a 72-column O reads 8 unused columns)
+      uint32_t orr[DL];
+      tmem_ld_n<DL>(O_addr, orr);
       tmem_wait_ld();
       if constexpr (SUMV) l_run = __uint_as_float(orr[D]);  // sum_k P_ik from the ones panel
       tc_fence_before();
