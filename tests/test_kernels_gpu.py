@@ -149,7 +149,9 @@ def _sdpa_ref(q, k, v, nseq, Lq, Lk):
                                         (128, 16, 1, 200), (128, 4, 1, 1000), (128, 2, 3, 77), (128, 16, 1, 8),
                                         (64, 2, 2, 4099), (64, 1, 1, 8192),
                                         # > 148 work units: CTAs run several units (unit hand-offs)
-                                        (64, 16, 12, 1374), (64, 16, 1, 6000)])
+                                        (64, 16, 12, 1374), (64, 16, 1, 6000),
+                                        # KV-split tail across sequences: 26 units of 130 KV tiles
+                                        (64, 1, 2, 6200), (64, 3, 3, 6200)])
 def test_attention_matches_sdpa(ops, D, H, nseq, L):
     T = nseq * L
     q = _bf(H, T, D, seed=20)
