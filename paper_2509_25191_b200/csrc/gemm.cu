@@ -42,20 +42,30 @@ struct GemmCfg {
   static constexpr int STAGES = CG2 ? 6 : (BN == 256 ? 4 : (BN == 128 ? 6 : 8));
   static constexpr uint32_t A_BYTES = GEMM_BM * GEMM_BK * 2;
   static constexpr uint32_t B_BYTES = (CG2 ? BN / 2 : BN) * GEMM_BK * 2;
-  static constexpr uint32_t SMEM = STAGES * (A_BYTES + B_BYTES) + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr uint32_t RING = STAGES * (A_BYTES + B_BYTES);
+  static constexpr uint32_t SMEM = RING + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr uint32_t TMEM_COLS = 2 * BN;
   static_assert(SMEM <= 227 * 1024, "GEMM stage ring exceeds the 227 KB smem per CTA");
 };
 
+// RESID epilogue transpose buffer: each epilogue warp stages its 32 x 32 fp32 accumulator block
+// (stride 33: conflict-free row writes and column reads) so that the fp32 residual read-modify-
+// write walks row segments with the 32 lanes on consecutive columns (one 128 B sector run per
+// row) instead of 32 rows per instruction (32 half-used sectors)
+constexpr uint32_t RESID_TILE_FLOATS = 32 * 33;
+template <int EPI>
+constexpr uint32_t epi_smem_bytes() {
+  return EPI == VX_EPI_RESID ? GEMM_EPI_WARPS * RESID_TILE_FLOATS * 4 : 0;
+}
+
 // ---------------------------------------------------------------------------
 // epilogues: one thread = one output row; columns processed 32 at a time
 // ---------------------------------------------------------------------------
-// the chunk's global operands (bias; the fp32 residual row segment for RESID), loaded before the
-// TMEM load so their latency overlaps it instead of serialising behind it
+// the chunk's bias, loaded before the TMEM load so its latency overlaps it instead of
+// serialising behind it (RESID has its own warp-transposed epilogue in gemm_kernel)
 template <int EPI>
 struct EpiPre {
   float4 b[8];
-  float4 x[EPI == VX_EPI_RESID ? 8 : 1];
 };
 
 template <int EPI>
@@ -68,13 +78,6 @@ VX_DEVICE void epi_prefetch(const GemmArgs& a, int row, int col, EpiPre<EPI>& p)
   } else {
 #pragma unroll
     for (int j = 0; j < 8; ++j) p.b[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-  }
-  if constexpr (EPI == VX_EPI_RESID) {
-    if (row < a.M) {
-      const float4* x4 = reinterpret_cast<const float4*>(e.resid + (size_t)row * e.ldr + col);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) p.x[j] = x4[j];
-    }
   }
 }
 
@@ -112,29 +115,6 @@ VX_DEVICE void epi_chunk32(const GemmArgs& a, int row, int col, const uint32_t* 
     float4* dst = reinterpret_cast<float4*>(e.resid + ((size_t)f * e.tokens_per_frame + e.patch_start + p) * e.ldr + col);
 #pragma unroll
     for (int j = 0; j < 8; ++j) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-  } else if constexpr (EPI == VX_EPI_RESID) {
-    float4* x4 = reinterpret_cast<float4*>(e.resid + (size_t)row * e.ldr + col);
-    const float4* g4 = reinterpret_cast<const float4*>(e.gamma + col);
-    float4 xv[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) xv[j] = pre.x[j];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      float4 g = __ldg(g4 + j);
-      xv[j].x += g.x * v[4 * j];
-      xv[j].y += g.y * v[4 * j + 1];
-      xv[j].z += g.z * v[4 * j + 2];
-      xv[j].w += g.w * v[4 * j + 3];
-      x4[j] = xv[j];
-    }
-    if (e.kept) {
-      uint4* kd = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(e.kept) + (size_t)row * e.ldk + col);
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        kd[j] = make_uint4(pack_bf16(xv[2 * j].x, xv[2 * j].y), pack_bf16(xv[2 * j].z, xv[2 * j].w),
-                           pack_bf16(xv[2 * j + 1].x, xv[2 * j + 1].y),
-                           pack_bf16(xv[2 * j + 1].z, xv[2 * j + 1].w));
-    }
   }
 }
 
@@ -391,6 +371,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  [[maybe_unused]] float* epi_buf = reinterpret_cast<float*>(smem + Cfg::RING + 256);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -548,6 +529,39 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           if constexpr (EPI == VX_EPI_SPATIAL) epi_spatial32(args, pi, col, r);
           else epi_headout(args, pi, r);
         }
+      } else if constexpr (EPI == VX_EPI_RESID) {
+        float* tb = epi_buf + (warp - 4) * RESID_TILE_FLOATS;
+        const vx_epilogue& e = args.ep;
+        const int row0 = m_blk * GEMM_BM + ew * 32;
+        const int nrows = M - row0 < 32 ? M - row0 : 32;
+#pragma unroll 1
+        for (int c0 = c_beg; c0 < c_end; c0 += 32) {
+          const int col = n_blk * BN + c0;
+          if (col >= N) break;
+          const int cc = col + int(lane);
+          float* xcol = e.resid + (size_t)row0 * e.ldr + cc;
+          float x[32];
+#pragma unroll
+          for (int rr = 0; rr < 32; ++rr) x[rr] = rr < nrows ? xcol[(size_t)rr * e.ldr] : 0.f;
+          const float b = e.bias ? __ldg(e.bias + cc) : 0.f;
+          const float g = __ldg(e.gamma + cc);
+          uint32_t r[32];
+          tmem_ld32(taddr + c0, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) tb[lane * 33 + j] = __uint_as_float(r[j]);
+          __syncwarp();
+          __nv_bfloat16* kcol = e.kept ? reinterpret_cast<__nv_bfloat16*>(e.kept) + (size_t)row0 * e.ldk + cc : nullptr;
+#pragma unroll
+          for (int rr = 0; rr < 32; ++rr) {
+            if (rr < nrows) {
+              const float xv = x[rr] + g * (tb[rr * 33 + lane] + b);
+              xcol[(size_t)rr * e.ldr] = xv;
+              if (kcol) kcol[(size_t)rr * e.ldk] = __float2bfloat16_rn(xv);
+            }
+          }
+          __syncwarp();
+        }
       } else {
 #pragma unroll 1
         for (int c0 = c_beg; c0 < c_end; c0 += 32) {
@@ -583,10 +597,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 template <int BN, int EPI, int HD, bool MC = false, bool CG2 = false>
 static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& args, cudaStream_t st) {
   using Cfg = GemmCfg<BN, CG2>;
+  constexpr uint32_t SMEM = Cfg::SMEM + epi_smem_bytes<EPI>();
+  static_assert(SMEM <= 227 * 1024, "GEMM stage ring + epilogue buffer exceed the 227 KB smem per CTA");
   auto kern = gemm_kernel<BN, EPI, HD, MC, CG2>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     if (e != cudaSuccess) return fail_cuda(e, "gemm: cudaFuncSetAttribute");
     attr_set = true;
   }
@@ -597,7 +613,7 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmA
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * clusters);
     cfg.blockDim = dim3(GEMM_THREADS);
-    cfg.dynamicSmemBytes = Cfg::SMEM;
+    cfg.dynamicSmemBytes = SMEM;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -611,7 +627,7 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmA
   } else {
     const int tiles = num_m * num_n;
     const int grid = tiles < num_sms() ? tiles : num_sms();
-    kern<<<grid, GEMM_THREADS, Cfg::SMEM, st>>>(ta, tb, args);
+    kern<<<grid, GEMM_THREADS, SMEM, st>>>(ta, tb, args);
   }
   VX_CHECK_LAUNCH("gemm launch");
   return VX_OK;

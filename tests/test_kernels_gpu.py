@@ -64,8 +64,9 @@ def test_gemm_strided_a(ops):
 
 
 @pytest.mark.parametrize("with_kept", [False, True])
-def test_gemm_residual_layerscale(ops, with_kept):
-    M, N, K = 2000, 1024, 4096
+@pytest.mark.parametrize("M", [2000, 2748, 100])  # ragged last M tile; CTA-pair path; single-M-tile path
+def test_gemm_residual_layerscale(ops, with_kept, M):
+    N, K = 1024, 4096
     a = _bf(M, K, seed=7)
     w = _bf(N, K, scale=0.02, seed=8)
     bias = torch.randn(N, device="cuda") * 0.1
