@@ -371,7 +371,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  [[maybe_unused]] float* epi_buf = reinterpret_cast<float*>(smem + Cfg::RING + 256);
+  // offset from smem_raw (not the integer-aligned pointer) so the compiler keeps the shared state
+  // space and emits LDS / STS for the transpose tile rather than generic LD / ST
+  [[maybe_unused]] float* epi_buf = reinterpret_cast<float*>(smem_raw + (smem - smem_raw) + Cfg::RING + 256);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
