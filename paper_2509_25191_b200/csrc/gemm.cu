@@ -501,6 +501,19 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     for (int u = unit0; u < units; u += ustep) {
       int m_blk, n_blk;
       tile_mn(u, m_blk, n_blk);
+      // RESID: the first residual chunk of this tile is loaded before the accumulator wait, so its
+      // latency overlaps the tile's main loop; later chunks are loaded one chunk ahead (below)
+      [[maybe_unused]] float xpre[EPI == VX_EPI_RESID ? 32 : 1];
+      [[maybe_unused]] const int rrow0 = m_blk * GEMM_BM + ew * 32;
+      [[maybe_unused]] const int nrows = M - rrow0 < 32 ? M - rrow0 : 32;
+      [[maybe_unused]] auto load_resid = [&](int col) {
+        const float* xc = args.ep.resid + (size_t)rrow0 * args.ep.ldr + col + int(lane);
+#pragma unroll
+        for (int rr = 0; rr < 32; ++rr) xpre[rr] = rr < nrows ? xc[(size_t)rr * args.ep.ldr] : 0.f;
+      };
+      if constexpr (EPI == VX_EPI_RESID) {
+        if (n_blk * BN + c_beg < N) load_resid(n_blk * BN + c_beg);
+      }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int row = m_blk * GEMM_BM + ew * 32 + lane;
@@ -534,8 +547,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       } else if constexpr (EPI == VX_EPI_RESID) {
         float* tb = epi_buf + (warp - 4) * RESID_TILE_FLOATS;
         const vx_epilogue& e = args.ep;
-        const int row0 = m_blk * GEMM_BM + ew * 32;
-        const int nrows = M - row0 < 32 ? M - row0 : 32;
+        const int row0 = rrow0;
 #pragma unroll 1
         for (int c0 = c_beg; c0 < c_end; c0 += 32) {
           const int col = n_blk * BN + c0;
@@ -544,7 +556,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           float* xcol = e.resid + (size_t)row0 * e.ldr + cc;
           float x[32];
 #pragma unroll
-          for (int rr = 0; rr < 32; ++rr) x[rr] = rr < nrows ? xcol[(size_t)rr * e.ldr] : 0.f;
+          for (int rr = 0; rr < 32; ++rr) x[rr] = xpre[rr];
+          if (c0 + 32 < c_end && col + 32 < N) load_resid(col + 32);
           const float b = e.bias ? __ldg(e.bias + cc) : 0.f;
           const float g = __ldg(e.gamma + cc);
           uint32_t r[32];
