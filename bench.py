@@ -103,7 +103,10 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * statistics.median(secs),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (torch.rand views seed 1, random-init weights seed 0)",
-        "config": {"workload": f"vggt1b_518_S{args.views}", "views": args.views, "img": 518},
+        "config": {"workload": f"vggt1b_518_S{args.views}", "views": args.views, "img": 518,
+                   "tokens_per_view": cfg.tokens_per_frame, "model": "VGGT-1B-shaped (24x2 blocks, C=1024)",
+                   "parallelism": "CPU host cores (rank 0 only)",
+                   "l2": "n/a (CPU oracle, bounded 2-view sample per step)"},
         "cpu_baseline": {"value": v, "unit": "views/s", "cores": threads, "kind": "port",
                          "sample": r["sample"]},
         "e2e": {"value": v, "unit": "views/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
