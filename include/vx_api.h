@@ -44,7 +44,8 @@ enum {
                                                                               + residual, a9/a10/a11) */
   VX_EPI_QKV = 3,    /* qkv Linear + q/k LayerNorm(head_dim) + 2D RoPE, scattered
                         to q/k/v bf16 [H, T, head_dim]                       (Attention.qkv/q_norm/
-                                                                              k_norm/rope, a4/a6)  */
+                                                                              k_norm/rope, a4/a6);
+                        without qk-norm and RoPE any head_dim % 32 == 0 (camera-head trunk, d = 128) */
   VX_EPI_PATCH = 4,  /* patch-embed: resid fp32 row (f*tpf + ps + p) = D + bias (PatchEmbed, a2)    */
   VX_EPI_F32 = 5     /* out fp32 [M, ldo]   = D + bias                                              */
 };
@@ -103,6 +104,25 @@ int vx_attention(const void* q, const void* k, const void* v, void* out, int64_t
 int vx_attention_merge(const void* q, const void* k, const void* v, int mode, float* o_acc, int64_t ld_acc,
                        float* lse_acc, void* out, int64_t ldo, int D, int H, int nseq, int Lq, int Lk,
                        int64_t Tq, int64_t Tk, void* stream);
+
+/* Camera head, fp32 parts ("bf16 except MLP in heads").
+ * vx_linear_f32: out[M, N] = epi(X[M, K] . W[N, K]^T + bias), fp32 SIMT (X row stride ldx; ldx = 0
+ * broadcasts one row, e.g. the (1, 1, 9) `empty_pose_tokens`).  Replaces CameraHead.embed_pose
+ * (+ the SiLU of poseLN_modulation), pose_branch.fc1 + GELU and pose_branch.fc2 + the iterative
+ * `pred_pose_enc + delta` update + activate_pose. */
+enum {
+  VX_LF_F32 = 0,        /* out fp32 = acc + bias                                   */
+  VX_LF_GELU = 1,       /* out fp32 = gelu_erf(acc + bias)                         */
+  VX_LF_SILU_BF16 = 2,  /* out bf16 = silu(acc + bias)                             */
+  VX_LF_POSE = 3        /* N == 9: out fp32 pred = (prev ? prev : 0) + acc + bias;
+                           act_out = activate_pose(pred) (T, quat linear; FoV relu) */
+};
+int vx_linear_f32(int epi, const float* X, int64_t ldx, const float* W, int64_t ldw, const float* bias, int M, int N,
+                  int K, void* out, int64_t ldo, const float* prev, float* act_out, void* stream);
+/* AdaLN modulation of the camera tokens (CameraHead.trunk_fn input): mod fp32 [S, 3D] = [shift | scale |
+ * gate] (output of poseLN_modulation), out fp32 [S, D] = gate * (LN(tok) * (1 + scale) + shift) + tok
+ * with the no-affine `adaln_norm` LayerNorm (eps).  D in {256, 512, 1024, 2048}. */
+int vx_adaln_modulate(const float* tok, const float* mod, float* out, int S, int D, float eps, void* stream);
 
 /* LayerNorm over the last dim (cols): y = (x - mean) * rstd * w + b.
  * x_dtype / y_dtype: 0 = fp32, 1 = bf16.  w/b may be NULL (no affine). (norm1/norm2, a5) */

@@ -184,7 +184,8 @@ def camera_head(tokens_last, sd, cfg: VGGTConfig) -> List[torch.Tensor]:
     pred = None
     outs = []
     for _ in range(cfg.cam_iters):
-        inp = torch.zeros(S, 9) if pred is None else pred
+        # iteration 0 embeds the learnable (1, 1, 9) empty_pose_tokens (upstream CameraHead.forward)
+        inp = sd[ch + "empty_pose_tokens"].reshape(1, 9).expand(S, 9) if pred is None else pred
         emb = linear(inp, sd, ch + "embed_pose")
         mod = linear(F.silu(emb), sd, ch + "poseLN_modulation.1")
         shift, scale, gate = mod.chunk(3, dim=-1)

@@ -79,6 +79,30 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     return LIB
 
 
+def build_diag(out: Path = ROOT / "exp" / "libvx_diag.so", defines=("VX_DIAG",)) -> Path:
+    """The diagnostic library for tools/ (`-DVX_DIAG`: the run-time kernel-variant switches
+    VX_FMHA_CFG / VX_FMHA_EMU / VX_FMHA_SPLIT / VX_GEMM_PAIR of DESIGN.md's A/B measurements).
+    Never loaded by the product path; tools bind it with ops.use_library(path)."""
+    out.parent.mkdir(parents=True, exist_ok=True)
+    objdir = out.parent / (out.stem + "_obj")
+    objdir.mkdir(exist_ok=True)
+    dflags = [f"-D{d}" for d in defines]
+    objs = []
+    with open(objdir / "nvcc.log", "w") as log:
+        for src in sources():
+            obj = objdir / (src.stem + ".o")
+            cmd = [NVCC, *ARCH, *FLAGS, *dflags, *EXTRA.get(src.name, []), "-c", str(src), "-o", str(obj)]
+            r = subprocess.run(cmd, capture_output=True, text=True)
+            log.write(f"$ {' '.join(cmd)}\n{r.stdout}{r.stderr}\n")
+            if r.returncode != 0:
+                raise RuntimeError(f"nvcc failed for {src.name}:\n{r.stderr[-4000:]}")
+            objs.append(obj)
+    r = subprocess.run([NVCC, *ARCH, "-shared", "-o", str(out), *map(str, objs)], capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"nvcc link failed:\n{r.stderr[-4000:]}")
+    return out
+
+
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose="-v" in sys.argv)
     print(LIB)

@@ -773,10 +773,14 @@ static int launch_fmha(const void* q, const void* k, const void* v, AttnArgs arg
   const int tail = args.units % sms;
   args.split_from = args.units;
   args.parts = 1;
+#ifdef VX_DIAG
   static const bool split_on = [] {
-    const char* e = getenv("VX_FMHA_SPLIT");  // diagnostic: 0 disables the KV-split tail
+    const char* e = getenv("VX_FMHA_SPLIT");  // diagnostic build only: 0 disables the KV-split tail
     return !(e && atoi(e) == 0);
   }();
+#else
+  constexpr bool split_on = true;
+#endif
   // only for long units: each split costs a merge launch and fp32 partial round trips, which a
   // frame-attention unit (29 KV tiles) does not earn back (S=20 frame layer 0.215 -> 0.228 ms)
   if (split_on && tail > 0 && 2 * tail <= sms && args.kv_tiles >= 128) {
@@ -840,21 +844,23 @@ static int attention_impl(const void* q, const void* k, const void* v, void* out
   a.ldo = ldo;
   a.lse = lse;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  static int emu = [] {
-    const char* e = getenv("VX_FMHA_EMU");  // diagnostic: exp pairs (of 8) on the FMA pipe
-    return e ? atoi(e) : 2;
-  }();
-  static int cfg = [] {
-    const char* e = getenv("VX_FMHA_CFG");  // diagnostic kernel variants, see below
-    return e ? atoi(e) : 0;
-  }();
   if (D == 64) {
-    // default (frame and global layers): 4 Q tiles x 48-wide KV tiles, P aliased onto S, row sums
-    // from a ones panel appended to V, S-ready / P-ready waits without a suspend-time hint, exps
-    // started with the running max (speculative; the tile max is checked afterwards) and 2 of 8
-    // exp pairs on the FMA pipe, the last 16 S columns loaded behind the first 16 exp pairs, and a
-    // branch-free MMA issue path. Sustained S=200 global layer (tools/sustain_attn.sh): 954
-    // TFLOP/s (EMU 1: 923, 3: 922, 4: 887); isolated S=20: 1089.
+    // frame and global layers: 4 Q tiles x 48-wide KV tiles, P aliased onto S, row sums from a
+    // ones panel appended to V, S-ready / P-ready waits without a suspend-time hint, exps started
+    // with the running max (speculative; the tile max is checked afterwards) and 2 of 8 exp pairs on
+    // the FMA pipe, the last 16 S columns loaded behind the first 16 exp pairs, and a branch-free
+    // MMA issue path. Sustained S=200 global layer (tools/sustain_attn.sh): 954 TFLOP/s (EMU 1: 923,
+    // 3: 922, 4: 887); isolated S=20: 1089.
+#ifdef VX_DIAG
+    // diagnostic build only (tools/, -DVX_DIAG): the measured alternatives of DESIGN.md §3.1
+    static int emu = [] {
+      const char* e = getenv("VX_FMHA_EMU");  // exp pairs (of 8) on the FMA pipe
+      return e ? atoi(e) : 2;
+    }();
+    static int cfg = [] {
+      const char* e = getenv("VX_FMHA_CFG");
+      return e ? atoi(e) : 0;
+    }();
     switch (cfg) {
       case 1: return launch_fmha<64, 2, 2, 128>(q, k, v, a, st);                       // 2 x 128 run-ahead
       case 3: return launch_fmha<64, 2, 3, 64>(q, k, v, a, st);                        // 3 x 64 run-ahead
@@ -870,8 +876,10 @@ static int attention_impl(const void* q, const void* k, const void* v, void* out
       case 0: return launch_fmha<64, 0, 4, 48, true, true, true, true, true>(q, k, v, a, st);
       case 1: return launch_fmha<64, 1, 4, 48, true, true, true, true, true>(q, k, v, a, st);
       case 3: return launch_fmha<64, 3, 4, 48, true, true, true, true, true>(q, k, v, a, st);
-      default: return launch_fmha<64, 2, 4, 48, true, true, true, true, true>(q, k, v, a, st);
+      default: break;
     }
+#endif
+    return launch_fmha<64, 2, 4, 48, true, true, true, true, true>(q, k, v, a, st);
   }
   if (D == 128) return launch_fmha<128, 2>(q, k, v, a, st);
   return launch_fmha<32, 2>(q, k, v, a, st);

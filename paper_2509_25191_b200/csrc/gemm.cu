@@ -198,6 +198,27 @@ VX_DEVICE void epi_qkv_head(const GemmArgs& a, int row, int col, float* v) {
                         pack_bf16(v[8 * j + 4], v[8 * j + 5]), pack_bf16(v[8 * j + 6], v[8 * j + 7]));
 }
 
+// q/k/v scatter without qk-norm / RoPE (camera-head trunk, head_dim = e.head_dim, any multiple of
+// 32): a 32-column chunk never straddles a head, so it goes straight to [H, T, head_dim]
+VX_DEVICE void epi_qkv_scatter32(const GemmArgs& a, int row, int col, const uint32_t* r, const EpiPre<VX_EPI_QKV>& pre) {
+  const vx_epilogue& e = a.ep;
+  if (row >= a.M) return;
+  const int C = e.embed_dim;
+  const int which = col / C;
+  const int hc = col - which * C;
+  const int h = hc / e.head_dim, off = hc - h * e.head_dim;
+  __nv_bfloat16* base = reinterpret_cast<__nv_bfloat16*>(which == 0 ? e.q : (which == 1 ? e.k : e.v));
+  uint4* dst = reinterpret_cast<uint4*>(base + ((size_t)h * e.tokens_total + row) * e.head_dim + off);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float4 b0 = pre.b[2 * j], b1 = pre.b[2 * j + 1];
+    dst[j] = make_uint4(pack_bf16(__uint_as_float(r[8 * j + 0]) + b0.x, __uint_as_float(r[8 * j + 1]) + b0.y),
+                        pack_bf16(__uint_as_float(r[8 * j + 2]) + b0.z, __uint_as_float(r[8 * j + 3]) + b0.w),
+                        pack_bf16(__uint_as_float(r[8 * j + 4]) + b1.x, __uint_as_float(r[8 * j + 5]) + b1.y),
+                        pack_bf16(__uint_as_float(r[8 * j + 6]) + b1.z, __uint_as_float(r[8 * j + 7]) + b1.w));
+  }
+}
+
 // ---------------------------------------------------------------------------
 // spatial (DPT) epilogues
 // ---------------------------------------------------------------------------
@@ -518,7 +539,19 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       tc_fence_after();
       const int row = m_blk * GEMM_BM + ew * 32 + lane;
       const uint32_t taddr = tmem_base + (uint32_t(ew * 32) << 16) + acc * BN;
-      if constexpr (EPI == VX_EPI_QKV) {
+      if constexpr (EPI == VX_EPI_QKV && HD == 0) {
+#pragma unroll 1
+        for (int c0 = c_beg; c0 < c_end; c0 += 32) {
+          const int col = n_blk * BN + c0;
+          if (col >= N) break;
+          EpiPre<EPI> pre;
+          epi_prefetch<EPI>(args, row, col, pre);
+          uint32_t r[32];
+          tmem_ld32(taddr + c0, r);
+          tmem_wait_ld();
+          epi_qkv_scatter32(args, row, col, r, pre);
+        }
+      } else if constexpr (EPI == VX_EPI_QKV) {
 #pragma unroll 1
         for (int c0 = c_beg; c0 < c_end; c0 += HD) {
           const int col = n_blk * BN + c0;
@@ -659,6 +692,7 @@ static int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, c
     case VX_EPI_SPATIAL: return launch_gemm<BN, VX_EPI_SPATIAL, 0, MC, CG2>(ta, tb, a, st);
     case VX_EPI_HEADOUT: return launch_gemm<BN, VX_EPI_HEADOUT, 0, MC, CG2>(ta, tb, a, st);
     case VX_EPI_QKV:
+      if (!a.ep.qn_w && !a.ep.rope_cos) return launch_gemm<BN, VX_EPI_QKV, 0, MC, CG2>(ta, tb, a, st);
       if (a.ep.head_dim == 64) return launch_gemm<BN, VX_EPI_QKV, 64, MC, CG2>(ta, tb, a, st);
       if (a.ep.head_dim == 32) return launch_gemm<BN, VX_EPI_QKV, 32, MC, CG2>(ta, tb, a, st);
       set_error("vx_gemm: qkv epilogue needs head_dim 32 or 64 (got %d)", a.ep.head_dim);
@@ -671,10 +705,14 @@ static int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, c
 // CTA pairs for the large 256-wide-N GEMMs (enough M tiles to pair up): 1 = B-tile multicast
 // with per-CTA M = 128 MMAs, 2 = cta_group::2 M = 256 MMAs
 static int pair_mode(int BN, int M) {
+#ifdef VX_DIAG
   static int env = [] {
-    const char* e = getenv("VX_GEMM_PAIR");  // diagnostic: 0 single CTAs, 1 multicast pairs, 2 MMA pairs
+    const char* e = getenv("VX_GEMM_PAIR");  // diagnostic build only: 0 single CTAs, 1 multicast pairs, 2 MMA pairs
     return e ? atoi(e) : 2;
   }();
+#else
+  constexpr int env = 2;
+#endif
   return (BN == 256 && M >= 8 * GEMM_BM) ? env : 0;
 }
 
@@ -691,7 +729,9 @@ extern "C" int vx_gemm(int epi, const void* A, int64_t lda, const void* B, int64
   if (epi == VX_EPI_RESID) VX_CHECK_ARG(ep->resid && ep->gamma, "vx_gemm: resid epilogue needs resid+gamma");
   if (epi == VX_EPI_QKV) {
     VX_CHECK_ARG(ep->q && ep->k && ep->v, "vx_gemm: qkv epilogue needs q/k/v");
-    VX_CHECK_ARG(N == 3 * ep->embed_dim && ep->embed_dim % ep->head_dim == 0, "vx_gemm: qkv N != 3C");
+    VX_CHECK_ARG(ep->head_dim > 0 && N == 3 * ep->embed_dim && ep->embed_dim % ep->head_dim == 0,
+                 "vx_gemm: qkv N != 3C");
+    VX_CHECK_ARG(ep->head_dim % 32 == 0 || ep->qn_w || ep->rope_cos, "vx_gemm: qkv scatter needs head_dim %% 32 == 0");
     VX_CHECK_ARG(ep->tokens_total >= M, "vx_gemm: tokens_total < M");
   }
   if (epi == VX_EPI_PATCH) VX_CHECK_ARG(ep->resid && ep->tokens_per_frame > ep->patch_start, "vx_gemm: patch args");
@@ -703,7 +743,8 @@ extern "C" int vx_gemm(int epi, const void* A, int64_t lda, const void* B, int64
   args.ep = *ep;
   // a single M tile (camera-head trunk, M = views) is bound by streaming the weights: 64-wide N
   // tiles spread that over up to 4x more SMs than 256-wide ones
-  const bool small_m = M <= GEMM_BM && N % 64 == 0 && epi != VX_EPI_QKV && epi != VX_EPI_PATCH;
+  const bool plain_qkv = epi == VX_EPI_QKV && !ep->qn_w && !ep->rope_cos;
+  const bool small_m = M <= GEMM_BM && N % 64 == 0 && (epi != VX_EPI_QKV || plain_qkv) && epi != VX_EPI_PATCH;
   const int BN = small_m ? 64 : ((N % 256 == 0 || N > 512) ? 256 : 128);
   const int pm = pair_mode(BN, M);
   CUtensorMap ta, tb;
@@ -716,11 +757,14 @@ extern "C" int vx_gemm(int epi, const void* A, int64_t lda, const void* B, int64
       case VX_EPI_GELU: return launch_gemm<64, VX_EPI_GELU, 0>(ta, tb, args, st);
       case VX_EPI_RESID: return launch_gemm<64, VX_EPI_RESID, 0>(ta, tb, args, st);
       case VX_EPI_F32: return launch_gemm<64, VX_EPI_F32, 0>(ta, tb, args, st);
+      case VX_EPI_QKV: return launch_gemm<64, VX_EPI_QKV, 0>(ta, tb, args, st);
       default: break;
     }
   }
   if (pm == 2) return dispatch_epi<256, false, true>(epi, ta, tb, args, st);
-  if (pm) return dispatch_epi<256, true>(epi, ta, tb, args, st);
+#ifdef VX_DIAG
+  if (pm) return dispatch_epi<256, true>(epi, ta, tb, args, st);  // B-tile multicast pairs (measured slower)
+#endif
   return BN == 256 ? dispatch_epi<256>(epi, ta, tb, args, st) : dispatch_epi<128>(epi, ta, tb, args, st);
 }
 
@@ -764,6 +808,8 @@ extern "C" int vx_gemm_spatial(const void* A, const void* B, int N, int K, const
   const int epi = sp->head_odim > 0 ? VX_EPI_HEADOUT : VX_EPI_SPATIAL;
   if (BN == 32) return launch_gemm<32, VX_EPI_HEADOUT, 0>(ta, tb, args, st);  // N == 32 output head
   if (pm == 2) return launch_gemm<256, VX_EPI_SPATIAL, 0, false, true>(ta, tb, args, st);
+#ifdef VX_DIAG
   if (pm) return launch_gemm<256, VX_EPI_SPATIAL, 0, true>(ta, tb, args, st);
+#endif
   return BN == 256 ? dispatch_epi<256>(epi, ta, tb, args, st) : dispatch_epi<128>(epi, ta, tb, args, st);
 }

@@ -257,6 +257,7 @@ class DeviceProblem:
     # -- state ---------------------------------------------------------------------------------
     def set_params(self, params):
         self.t_["params"].copy_(torch.as_tensor(np.asarray(params, dtype=np.float64).reshape(self.n, self.dim)))
+        self._clear_status()
         ops.ga_decode(self.pb)
         self._check_status()
 
@@ -269,6 +270,11 @@ class DeviceProblem:
             raise ValueError("weight table size does not match the match set")
         if self.K:
             self.t_["w"][: self.K].copy_(w.reshape(-1))
+
+    def _clear_status(self):
+        # the device only ever sets status bits (atomicOr): clear them before each call that can
+        # raise, so one failure does not stick to every later call on valid inputs
+        self.t_["status"][0].zero_()
 
     def _check_status(self):
         st = int(self.t_["status"][0].item())
@@ -291,6 +297,7 @@ class DeviceProblem:
 
     def loss_and_gradient(self) -> LossGradient:
         grad = torch.empty(self.n, self.dim, device=self.device, dtype=torch.float64)
+        self._clear_status()
         ops.ga_loss_grad(self.pb, grad)
         self._check_status()
         num, den, sk, _ = self.t_["scalars"][:4].tolist()
@@ -391,6 +398,7 @@ def align_arrays(R, t, intr, pair_ij, offsets, xy_i, xy_j, cfg: AlignerConfig | 
     skipped = torch.zeros(1, device=prob.device, dtype=torch.float64)
     seg = cfg.reweight_every if cfg.reweight_every > 0 else T
     t0 = 0
+    prob._clear_status()  # bits accumulate over the segments below and are checked once after them
     while t0 < T:
         if t0 > 0:  # aligner.py:405-407: re-weight at t = 1 + k * reweight_every
             e_now, _, _ = prob.residuals_device()
@@ -445,8 +453,12 @@ def _match_arrays(matches):
     xy_j = np.concatenate([np.asarray(p.xy_j, dtype=np.float64).reshape(-1, 2) for p in pairs]) if pairs else \
         np.zeros((0, 2))
     conf = None
-    if pairs and all(getattr(p, "confidence", None) is not None for p in pairs):
-        conf = np.concatenate([np.asarray(p.confidence, dtype=np.float64).reshape(-1) for p in pairs])
+    # the reference checks confidences only on the live (non-empty) pairs align() keeps
+    # (aligner.py:358-360, weighting.py:108-111): an empty pair without confidences is fine
+    live = [p for p, c in zip(pairs, cnt) if c > 0]
+    if live and all(getattr(p, "confidence", None) is not None for p in live):
+        conf = np.concatenate([np.asarray(p.confidence, dtype=np.float64).reshape(-1) if c > 0 else np.zeros(0)
+                               for p, c in zip(pairs, cnt)])
     return pair_ij, offsets, xy_i, xy_j, conf
 
 

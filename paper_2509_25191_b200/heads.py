@@ -14,7 +14,6 @@ Precision policy ("bf16 except MLP in heads", `PAPER.md:81`):
 """
 from __future__ import annotations
 
-import math
 from typing import Dict, List
 
 import torch
@@ -28,14 +27,18 @@ from .aggregator import DeviceWeights
 # camera head
 # ---------------------------------------------------------------------------
 def _trunk_block(W: DeviceWeights, name: str, x: torch.Tensor, num_heads: int, eps: float):
-    """Camera-trunk Block (no RoPE, no qk-norm) on fp32 residual x (S, D)."""
+    """Camera-trunk Block (no RoPE, no qk-norm) on fp32 residual x (S, D), in place.
+
+    The qkv GEMM epilogue scatters q/k/v head-major ([H, S, d], d = 128) for the vx FMHA, which
+    attends across the S camera tokens (attention across frames)."""
     S, D = x.shape
     d = D // num_heads
+    dev = x.device
     xn = ops.layernorm(x, W[name + ".norm1.weight"], W[name + ".norm1.bias"], eps)
-    qkv = ops.gemm(xn, W[name + ".attn.qkv.weight"], ops.EPI_BF16, bias=W[name + ".attn.qkv.bias"])
-    q, k, v = (t.contiguous() for t in qkv.view(S, 3, num_heads, d).permute(1, 2, 0, 3).unbind(0))
-    # attention across the S camera tokens (head_dim 128) on the vx FMHA
-    o = torch.empty(S, D, device=x.device, dtype=torch.bfloat16)
+    q, k, v = (torch.empty(num_heads, S, d, device=dev, dtype=torch.bfloat16) for _ in range(3))
+    ops.gemm(xn, W[name + ".attn.qkv.weight"], ops.EPI_QKV, bias=W[name + ".attn.qkv.bias"], qkv=(q, k, v),
+             head_dim=d, tokens_total=S)
+    o = torch.empty(S, D, device=dev, dtype=torch.bfloat16)
     ops.attention(q, k, v, o, nseq=1, Lq=S, Lk=S)
     ops.gemm(o, W[name + ".attn.proj.weight"], ops.EPI_RESID, bias=W[name + ".attn.proj.bias"], resid=x,
              gamma=W[name + ".ls1.gamma"])
@@ -47,36 +50,45 @@ def _trunk_block(W: DeviceWeights, name: str, x: torch.Tensor, num_heads: int, e
 
 
 def activate_pose(enc: torch.Tensor) -> torch.Tensor:
-    """absT_quaR_FoV: translation linear, quaternion linear, fov relu."""
+    """absT_quaR_FoV: translation linear, quaternion linear, fov relu (host reference of the
+    VX_LF_POSE epilogue; used by the pose tools, not on the forward path)."""
     return torch.cat([enc[..., :7], F.relu(enc[..., 7:])], dim=-1)
 
 
 def camera_head(W: DeviceWeights, cam_tokens: torch.Tensor) -> List[torch.Tensor]:
-    """cam_tokens: (S, 2C) bf16/fp32 camera tokens of the last kept layer -> 4 x (S, 9) fp32."""
+    """cam_tokens: (S, 2C) bf16/fp32 camera tokens of the last kept layer -> 4 x (S, 9) fp32.
+
+    Upstream CameraHead.forward / trunk_fn: every iteration embeds the previous
+    pose encoding (iteration 0: the learnable `empty_pose_tokens`), modulates the normalised camera
+    tokens (AdaLN: shift / scale / gate), runs the 4-block trunk with attention across the S views,
+    and adds the pose-branch delta.  All on libvx: fp32 SIMT linears for the pose embedding and the
+    pose-branch MLP (kept fp32), the bf16 tcgen05 GEMM for the modulation and the trunk.
+    """
     cfg = W.cfg
     ch = "camera_head."
     eps = cfg.ln_eps
     S, D = cam_tokens.shape
+    dev = cam_tokens.device
     tok = ops.layernorm(cam_tokens, W[ch + "token_norm.weight"], W[ch + "token_norm.bias"], eps,
                         out_dtype=torch.float32)
+    empty = W[ch + "empty_pose_tokens"].reshape(1, 9).expand(S, 9)
     pred = None
     outs = []
     for _ in range(cfg.cam_iters):
-        inp = torch.zeros(S, 9, device=tok.device) if pred is None else pred
-        emb = F.linear(inp, W[ch + "embed_pose.weight"], W[ch + "embed_pose.bias"])
-        mod = ops.gemm(F.silu(emb).to(torch.bfloat16), W[ch + "poseLN_modulation.1.weight"], ops.EPI_F32,
-                       bias=W[ch + "poseLN_modulation.1.bias"])
-        shift, scale, gate = mod.chunk(3, dim=-1)
-        hn = ops.layernorm(tok, None, None, 1e-6, out_dtype=torch.float32)
-        x = gate * (hn * (1 + scale) + shift) + tok
-        x = x.contiguous()
+        emb = ops.linear_f32(empty if pred is None else pred, W[ch + "embed_pose.weight"], W[ch + "embed_pose.bias"],
+                             ops.LF_SILU_BF16)
+        mod = ops.gemm(emb, W[ch + "poseLN_modulation.1.weight"], ops.EPI_F32, bias=W[ch + "poseLN_modulation.1.bias"])
+        x = ops.adaln_modulate(tok, mod, 1e-6)
         for j in range(cfg.cam_trunk_depth):
             _trunk_block(W, f"{ch}trunk.{j}", x, cfg.cam_num_heads, eps)
         xn = ops.layernorm(x, W[ch + "trunk_norm.weight"], W[ch + "trunk_norm.bias"], eps, out_dtype=torch.float32)
-        hid = F.gelu(F.linear(xn, W[ch + "pose_branch.fc1.weight"], W[ch + "pose_branch.fc1.bias"]))
-        delta = F.linear(hid, W[ch + "pose_branch.fc2.weight"], W[ch + "pose_branch.fc2.bias"])
-        pred = delta if pred is None else pred + delta
-        outs.append(activate_pose(pred))
+        hid = ops.linear_f32(xn, W[ch + "pose_branch.fc1.weight"], W[ch + "pose_branch.fc1.bias"], ops.LF_GELU)
+        new = torch.empty(S, 9, device=dev, dtype=torch.float32)
+        act = torch.empty(S, 9, device=dev, dtype=torch.float32)
+        ops.linear_f32(hid, W[ch + "pose_branch.fc2.weight"], W[ch + "pose_branch.fc2.bias"], ops.LF_POSE, out=new,
+                       prev=pred, act_out=act)
+        pred = new
+        outs.append(act)
     return outs
 
 

@@ -13,10 +13,10 @@ from pathlib import Path
 
 import torch
 
-# VX_LIB: diagnostic override (A/B-testing a second build of the same library)
-_LIB_PATH = Path(os.environ.get("VX_LIB", str(Path(__file__).resolve().parent / "libvx.so")))
+_LIB_PATH = Path(__file__).resolve().parent / "libvx.so"
 
 EPI_BF16, EPI_GELU, EPI_RESID, EPI_QKV, EPI_PATCH, EPI_F32 = range(6)
+LF_F32, LF_GELU, LF_SILU_BF16, LF_POSE = range(4)  # vx_linear_f32 epilogues
 
 _vp = ctypes.c_void_p
 _i64 = ctypes.c_int64
@@ -59,7 +59,7 @@ class GaProblem(ctypes.Structure):
 
 
 EXPORTED_SYMBOLS = ("vx_gemm", "vx_attention", "vx_attention_merge", "vx_layernorm", "vx_layernorm_gather", "vx_patchify",
-                    "vx_special_tokens",
+                    "vx_special_tokens", "vx_linear_f32", "vx_adaln_modulate",
                     "vx_upsample_bilinear", "vx_gemm_spatial", "vx_epipolar_residuals",
                     "vx_epipolar_accumulate", "vx_ga_decode", "vx_ga_residuals", "vx_ga_loss_grad",
                     "vx_ga_adam", "vx_ga_adaptive_weights", "vx_matched_points", "vx_unproject_depth",
@@ -86,6 +86,8 @@ def load_library(path: os.PathLike | None = None) -> ctypes.CDLL:
     lib.vx_layernorm_gather.argtypes = [_vp, _i32, _i64, _vp, _i32, _i64, _vp, _vp, _i32, _i32, _f32, _i32, _i32,
                                         _i32, _vp]
     lib.vx_patchify.argtypes = [_vp, _vp, _i32, _i32, _i32, _i32, _i32, _vp]
+    lib.vx_linear_f32.argtypes = [_i32, _vp, _i64, _vp, _i64, _vp, _i32, _i32, _i32, _vp, _i64, _vp, _vp, _vp]
+    lib.vx_adaln_modulate.argtypes = [_vp, _vp, _vp, _i32, _i32, _f32, _vp]
     lib.vx_special_tokens.argtypes = [_vp, _vp, _i32, _i32, _i32, _i32, _vp]
     lib.vx_upsample_bilinear.argtypes = [_vp, _i32, _i32, _i32, _i32, _vp, _i32, _i32, _vp, _i32, _vp]
     lib.vx_gemm_spatial.argtypes = [_vp, _vp, _i32, _i32, _vp, ctypes.POINTER(Spatial), _vp]
@@ -113,6 +115,14 @@ def load_library(path: os.PathLike | None = None) -> ctypes.CDLL:
     if path is None:
         _lib = lib
     return lib
+
+
+def use_library(path: os.PathLike) -> ctypes.CDLL:
+    """Bind every op of this module to another build of the library (tools/: A/B runs against a
+    `-DVX_DIAG` build from build.build_diag); the product path never calls this."""
+    global _lib
+    _lib = load_library(path)
+    return _lib
 
 
 # number of vx C-ABI calls issued by this process
@@ -305,6 +315,51 @@ def special_tokens(x, tokens, S, tpf):
     _check(_lib.vx_special_tokens(_ptr(x), _ptr(tokens.contiguous()), S, tpf, ntok, C, _stream()),
            "vx_special_tokens")
     return x
+
+
+def linear_f32(x, w, bias, epi: int = LF_F32, out=None, prev=None, act_out=None):
+    """fp32 out = epi(x @ w.T + bias) (vx_linear_f32).  x (M, K) or one broadcast row (1, K) with
+    `rows`; LF_SILU_BF16 writes bf16; LF_POSE (N = 9) writes pred = prev + delta to `out` and
+    activate_pose(pred) to `act_out`."""
+    load_library()
+    _req(x, torch.float32, "x")
+    _req(w, torch.float32, "w")
+    ldw = _rowmajor(w, "w")
+    N, K = w.shape
+    if x.dim() != 2 or x.shape[1] != K or (x.stride(1) != 1 and K > 1):
+        raise ValueError(f"linear_f32: x must be (M, {K}) row-major, got {tuple(x.shape)} strides {x.stride()}")
+    M = x.shape[0]
+    ldx = x.stride(0) if M > 1 else K  # stride 0: one row broadcast to all M (expand)
+    if bias is not None:
+        _req(bias, torch.float32, "bias")
+    want = torch.bfloat16 if epi == LF_SILU_BF16 else torch.float32
+    if out is None:
+        out = torch.empty(M, N, device=x.device, dtype=want)
+    _req(out, want, "out")
+    ldo = _rowmajor(out, "out")
+    if epi == LF_POSE:
+        if act_out is None or prev is not None and (prev.shape != out.shape or not prev.is_contiguous()):
+            raise ValueError("linear_f32: pose epilogue needs act_out and a (M, 9) prev like out")
+        _req(act_out, torch.float32, "act_out")
+        if act_out.shape != out.shape or not (out.is_contiguous() and act_out.is_contiguous()):
+            raise ValueError("linear_f32: pose outputs must be contiguous (M, 9)")
+    _check(_lib.vx_linear_f32(epi, _ptr(x), ldx, _ptr(w), ldw, _ptr(bias), M, N, K, _ptr(out), ldo, _ptr(prev),
+                              _ptr(act_out), _stream()), "vx_linear_f32")
+    return out
+
+
+def adaln_modulate(tok, mod, eps: float, out=None):
+    """gate * (LN_noaffine(tok) * (1 + scale) + shift) + tok, mod = [shift | scale | gate] (vx_adaln_modulate)."""
+    load_library()
+    _req(tok, torch.float32, "tok")
+    _req(mod, torch.float32, "mod")
+    S, D = tok.shape
+    if not (tok.is_contiguous() and mod.is_contiguous()) or tuple(mod.shape) != (S, 3 * D):
+        raise ValueError("adaln_modulate: contiguous tok (S, D) and mod (S, 3D) required")
+    if out is None:
+        out = torch.empty_like(tok)
+    _check(_lib.vx_adaln_modulate(_ptr(tok), _ptr(mod), _ptr(out), S, D, eps, _stream()), "vx_adaln_modulate")
+    return out
 
 
 def upsample_bilinear(x: torch.Tensor, size, add=None, out=None, out_pad: bool = False):

@@ -120,7 +120,20 @@ def select_matched_points_arrays(pair_ij, offsets, xy_i, xy_j, w, depth_maps, R,
     for f in np.unique(pair_ij):
         if int(f) not in depth_maps:
             raise MissingDepthMap(f"no depth map for frame index {int(f)}")
-    n = np.asarray(R).shape[0]
+    R, t, Kinv = (np.asarray(a, dtype=np.float64) for a in (R, t, Kinv))
+    n = R.shape[0]
+    if pair_ij.size and (int(pair_ij.min()) < -n or int(pair_ij.max()) >= n):
+        # the reference fails on rig[frame] (IndexError); the kernel would read past the cameras
+        bad = int(pair_ij.min()) if int(pair_ij.min()) < -n else int(pair_ij.max())
+        raise IndexError(f"pair frame index {bad} outside the rig of {n} frames")
+    neg = sorted({int(f) for f in np.unique(pair_ij) if f < 0})
+    virt = {}
+    if neg:  # rig[-k] wraps in the reference while the depth map stays keyed by -k: one virtual frame each
+        virt = {f: n + i for i, f in enumerate(neg)}
+        R = np.concatenate([R, R[neg]])
+        t = np.concatenate([t, t[neg]])
+        Kinv = np.concatenate([Kinv, Kinv[neg]])
+        pair_ij = np.vectorize(lambda f: virt.get(int(f), int(f)), otypes=[np.int32])(pair_ij)
     keys = sorted(int(k) for k in depth_maps)
     def as_map(d):  # DepthMap-like (.values) or a plain 2-D array / tensor
         return torch.as_tensor(d if isinstance(d, (np.ndarray, torch.Tensor)) else d.values)
@@ -128,10 +141,12 @@ def select_matched_points_arrays(pair_ij, offsets, xy_i, xy_j, w, depth_maps, R,
     maps = [as_map(depth_maps[k]) for k in keys]
     f32 = all(m.dtype == torch.float32 for m in maps)
     dt = torch.float32 if f32 else torch.float64
-    slot = np.full(n, 0, dtype=np.int32)
+    slot = np.full(n + len(virt), 0, dtype=np.int32)
     for s, k in enumerate(keys):
         if 0 <= k < n:
             slot[k] = s
+        elif k in virt:
+            slot[virt[k]] = s
     hw = np.array([[m.shape[0], m.shape[1]] for m in maps], dtype=np.int32)
     moff = np.concatenate([[0], np.cumsum([m.numel() for m in maps])[:-1]]).astype(np.int64)
     depth = torch.cat([m.reshape(-1).to(device="cuda", dtype=dt) for m in maps])

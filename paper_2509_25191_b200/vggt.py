@@ -15,7 +15,6 @@ frame slice while `pose_enc` is global.
 """
 from __future__ import annotations
 
-import os
 from typing import Dict, Optional, Tuple
 
 import torch
@@ -26,7 +25,7 @@ from .config import VGGTConfig, vggt_1b
 from .heads import DPTHeadDevice, camera_head
 from .profiling import phase
 from .pose import pose_encoding_to_extri_intri  # noqa: F401  (re-export, upstream location)
-from .weights import make_state_dict
+from .weights import check_state_dict, make_state_dict
 
 
 def _require_b200(device):
@@ -45,11 +44,11 @@ class VGGT:
         _require_b200(self.device)
         ops.load_library()
         sd = state_dict if state_dict is not None else make_state_dict(self.cfg, seed)
+        check_state_dict(sd, self.cfg)
         self.W = DeviceWeights(sd, self.cfg, self.device)
         self.depth_head = DPTHeadDevice(self.W, "depth_head.", "exp")
         self.point_head = DPTHeadDevice(self.W, "point_head.", "inv_log")
         self.dist = dist
-        self.head_streams = os.environ.get("VX_HEAD_STREAMS", "1") != "0"  # diagnostic switch
         self._streams = None
         self.ring = None
         if dist:
@@ -110,34 +109,27 @@ class VGGT:
         depth_conf = torch.empty(Sl, H, W, device=dev)
         pts = torch.empty(Sl, H, W, 3, device=dev)
         pts_conf = torch.empty(Sl, H, W, device=dev)
-        if self.head_streams:
-            # the three heads are independent: depth and point heads on two side streams, the camera
-            # head concurrently on the current stream
-            with phase("heads"):
-                cur = torch.cuda.current_stream(dev)
-                s_d, s_p = self._head_streams(dev)
-                s_d.wait_stream(cur)
-                s_p.wait_stream(cur)
-                with torch.cuda.stream(s_d):
-                    self.depth_head(kept, depth, depth_conf, cfg.head_chunk)
-                with torch.cuda.stream(s_p):
-                    self.point_head(kept, pts, pts_conf, cfg.head_chunk)
-                pose_list = camera_head(self.W, cam)
-                cur.wait_stream(s_d)
-                cur.wait_stream(s_p)
-                for t in kept.values():  # read on the side streams
-                    t.record_stream(s_d)
-                    t.record_stream(s_p)
-                depth.record_stream(s_d)
-                depth_conf.record_stream(s_d)
-                pts.record_stream(s_p)
-                pts_conf.record_stream(s_p)
-        else:
-            with phase("camera_head"):
-                pose_list = camera_head(self.W, cam)
-            with phase("dpt_heads"):
+        # the three heads are independent: depth and point heads on two side streams, the camera head
+        # concurrently on the current stream
+        with phase("heads"):
+            cur = torch.cuda.current_stream(dev)
+            s_d, s_p = self._head_streams(dev)
+            s_d.wait_stream(cur)
+            s_p.wait_stream(cur)
+            with torch.cuda.stream(s_d):
                 self.depth_head(kept, depth, depth_conf, cfg.head_chunk)
+            with torch.cuda.stream(s_p):
                 self.point_head(kept, pts, pts_conf, cfg.head_chunk)
+            pose_list = camera_head(self.W, cam)
+            cur.wait_stream(s_d)
+            cur.wait_stream(s_p)
+            for t in kept.values():  # read on the side streams
+                t.record_stream(s_d)
+                t.record_stream(s_p)
+            depth.record_stream(s_d)
+            depth_conf.record_stream(s_d)
+            pts.record_stream(s_p)
+            pts_conf.record_stream(s_p)
         return {
             "pose_enc": pose_list[-1][None],
             "pose_enc_list": [p[None] for p in pose_list],

@@ -88,6 +88,7 @@ def param_shapes(cfg: VGGTConfig) -> "OrderedDict[str, tuple]":
     s[ch + "token_norm.bias"] = (D,)
     s[ch + "trunk_norm.weight"] = (D,)
     s[ch + "trunk_norm.bias"] = (D,)
+    s[ch + "empty_pose_tokens"] = (1, 1, 9)  # learnable iteration-0 input of embed_pose (upstream zeros)
     s[ch + "embed_pose.weight"] = (D, 9)
     s[ch + "embed_pose.bias"] = (D,)
     s[ch + "poseLN_modulation.1.weight"] = (3 * D, D)
@@ -152,6 +153,8 @@ def _init_one(name: str, shape: tuple, cfg: VGGTConfig, seed: int) -> torch.Tens
     nd = len(shape)
     if name.endswith("camera_token") or name.endswith("register_token"):
         return _normal(shape, 0.5, seed, name, trunc=False)
+    if name == "camera_head.empty_pose_tokens":
+        return torch.zeros(shape)  # upstream init; a trained checkpoint carries its own values
     if name.endswith(".gamma"):
         base = cfg.cam_init_values if name.startswith("camera_head.") else cfg.init_values
         return _normal(shape, 0.1 * base, seed, name, mean=base)
@@ -187,6 +190,17 @@ def is_bf16_param(name: str, shape: tuple) -> bool:
     if len(shape) < 2 or not name.endswith(".weight"):
         return False
     return not name.startswith(FP32_PREFIXES)
+
+
+def check_state_dict(sd, cfg: VGGTConfig) -> None:
+    """Every upstream-named parameter of this path must be present with its shape: a checkpoint that
+    lacks one (e.g. camera_head.empty_pose_tokens) must not silently run with a made-up value."""
+    missing = [k for k in param_shapes(cfg) if k not in sd]
+    if missing:
+        raise KeyError(f"state_dict lacks {len(missing)} parameter(s) of the VGGT path, e.g. {missing[:4]}")
+    bad = [(k, tuple(sd[k].shape), s) for k, s in param_shapes(cfg).items() if tuple(sd[k].shape) != tuple(s)]
+    if bad:
+        raise ValueError(f"state_dict shape mismatch: {bad[:4]}")
 
 
 def make_state_dict(cfg: VGGTConfig, seed: int = 0) -> "OrderedDict[str, torch.Tensor]":

@@ -250,3 +250,37 @@ def test_device_align_dense_scene_matches_oracle(ga):
     assert tr.max() < 1e-8, tr.max()
     assert np.abs(o["out_R"] - ref["out_R"]).max() < 1e-8
     np.testing.assert_allclose(o["report"][:3], ref["report"][:3], rtol=1e-8)
+
+
+def test_match_arrays_confidence_checked_on_live_pairs_only():
+    """aligner.py:358-360 drops empty pairs before weighting.py:108-111 checks confidences, so an empty
+    pair without confidences must not make weight_mode='confidence' fail."""
+    from paper_2509_25191_b200.ga import _match_arrays
+    d = CASES["focal6"]
+    o = d["offsets"]
+    rng = np.random.default_rng(0)
+    pairs = [_PM(int(i), int(j), d["xy_i"][o[p]:o[p + 1]], d["xy_j"][o[p]:o[p + 1]], rng.random(o[p + 1] - o[p]))
+             for p, (i, j) in enumerate(d["pair_ij"])]
+    pairs.insert(1, _PM(0, 1, np.zeros((0, 2)), np.zeros((0, 2)), None))
+    pij, off, xi, xj, conf = _match_arrays(_MS(tuple(pairs)))
+    assert conf is not None and conf.shape == (int(off[-1]),)
+    np.testing.assert_array_equal(conf, np.concatenate([p.confidence for p in pairs if len(p.xy_i)]))
+    pairs[2] = _PM(pairs[2].frame_i, pairs[2].frame_j, pairs[2].xy_i, pairs[2].xy_j, None)
+    assert _match_arrays(_MS(tuple(pairs)))[4] is None
+
+
+@pytest.mark.gpu
+def test_device_problem_status_does_not_stick(ga):
+    """A DeviceProblem that raised on a degenerate 6D rotation evaluates valid parameters afterwards."""
+    d = CASES["noisy5"]
+    R, t, intr = d["R"], d["t"], d["intr"]
+    Kinv = np.stack([np.linalg.inv(np.array([[x[0], 0, x[2]], [0, x[1], x[3]], [0, 0, 1.0]])) for x in intr])
+    prob = ga.DeviceProblem(R, t, Kinv, d["pair_ij"], d["offsets"], d["xy_i"], d["xy_j"], 1, False, 0)
+    good = ga.identity_params(len(R), False)
+    bad = good.copy()
+    bad[1, :6] = 0.0
+    with pytest.raises(ga.DegenerateRotation6D):
+        prob.set_params(bad)
+    prob.set_params(good)
+    lg = prob.loss_and_gradient()
+    assert np.isfinite(lg.loss)

@@ -391,3 +391,93 @@ def test_c_abi_rejects_bad_shapes(ops):
     x = torch.randn(4, 128, device="cuda")
     y = ops.layernorm(x, None, None, 1e-5)
     assert torch.isfinite(y.float()).all()
+
+
+# ---------------------------------------------------------------------------------------------------
+# camera head (a12): fp32 linears, AdaLN modulation, head-major trunk qkv
+@pytest.mark.parametrize("M,N,K", [(200, 1024, 2048), (37, 2048, 9), (1, 64, 100), (130, 9, 1024)])
+def test_linear_f32_epilogues(ops, M, N, K):
+    g = torch.Generator(device="cuda").manual_seed(7)
+    x = torch.randn(M, K, device="cuda", generator=g)
+    w = torch.randn(N, K, device="cuda", generator=g) / math.sqrt(K)
+    b = torch.randn(N, device="cuda", generator=g)
+    ref = torch.nn.functional.linear(x.double(), w.double(), b.double())
+    assert rel(ops.linear_f32(x, w, b, ops.LF_F32), ref) < 1e-5
+    assert rel(ops.linear_f32(x, w, b, ops.LF_GELU), F.gelu(ref)) < 1e-5
+    s = ops.linear_f32(x, w, b, ops.LF_SILU_BF16)
+    assert s.dtype == torch.bfloat16 and rel(s, F.silu(ref)) < 5e-3
+    if N == 9:
+        prev = torch.randn(M, 9, device="cuda", generator=g)
+        pred = torch.empty(M, 9, device="cuda")
+        act = torch.empty(M, 9, device="cuda")
+        ops.linear_f32(x, w, b, ops.LF_POSE, out=pred, prev=prev, act_out=act)
+        want = prev.double() + ref
+        assert rel(pred, want) < 1e-5
+        assert rel(act, torch.cat([want[:, :7], F.relu(want[:, 7:])], 1)) < 1e-5
+
+
+def test_linear_f32_broadcast_row(ops):
+    """ldx = 0: the (1, 1, 9) empty_pose_tokens expanded over all views."""
+    e = torch.randn(1, 9, device="cuda")
+    w = torch.randn(256, 9, device="cuda")
+    b = torch.randn(256, device="cuda")
+    out = ops.linear_f32(e.expand(50, 9), w, b, ops.LF_F32)
+    assert rel(out, (e @ w.T + b).expand(50, 256)) < 1e-6
+
+
+@pytest.mark.parametrize("D", [256, 2048])
+def test_adaln_modulate(ops, D):
+    g = torch.Generator(device="cuda").manual_seed(8)
+    S = 77
+    tok = torch.randn(S, D, device="cuda", generator=g) * 2 + 0.5
+    mod = torch.randn(S, 3 * D, device="cuda", generator=g) * 0.3
+    shift, scale, gate = mod.chunk(3, dim=-1)
+    ref = gate * (F.layer_norm(tok, (D,), None, None, 1e-6) * (1 + scale) + shift) + tok
+    assert rel(ops.adaln_modulate(tok, mod, 1e-6), ref) < 1e-5
+
+
+@pytest.mark.parametrize("S", [9, 200])
+def test_gemm_qkv_plain_scatter_d128(ops, S):
+    """Camera-trunk qkv (no qk-norm, no RoPE, head_dim 128): head-major q/k/v straight from the epilogue."""
+    D, H = 512, 4
+    d = D // H
+    x = _bf(S, D, seed=9)
+    w = _bf(3 * D, D, scale=0.05, seed=10)
+    bias = torch.randn(3 * D, device="cuda")
+    q, k, v = (torch.empty(H, S, d, device="cuda", dtype=torch.bfloat16) for _ in range(3))
+    ops.gemm(x, w, ops.EPI_QKV, bias=bias, qkv=(q, k, v), head_dim=d, tokens_total=S)
+    ref = (x.float() @ w.float().T + bias).view(S, 3, H, d).permute(1, 2, 0, 3)
+    for got, want in zip((q, k, v), ref):
+        assert rel(got, want) < 5e-3
+
+
+@pytest.mark.parametrize("cfg_name,S", [("tiny", 8), ("1b", 20)])
+def test_camera_head_matches_oracle(cfg_name, S):
+    """The whole camera head (a12) on the device against the fp32 oracle on the same fp32 camera
+    tokens, with a non-zero learnable `empty_pose_tokens` (a trained checkpoint's value is used)."""
+    from oracle import vggt_ref as R
+    from paper_2509_25191_b200.aggregator import DeviceWeights
+    from paper_2509_25191_b200.config import vggt_1b, vggt_tiny
+    from paper_2509_25191_b200.heads import camera_head
+    from paper_2509_25191_b200.weights import make_state_dict
+    cfg = vggt_tiny() if cfg_name == "tiny" else vggt_1b()
+    sd = make_state_dict(cfg, 0)
+    sd["camera_head.empty_pose_tokens"] = torch.tensor([[[0.1, -0.2, 0.3, 0.05, -0.05, 0.02, 0.9, 0.5, 0.6]]])
+    D = 2 * cfg.embed_dim
+    g = torch.Generator().manual_seed(11)
+    tok = (torch.randn(S, D, generator=g) * 0.5).to(torch.bfloat16).float()  # bf16-representable input
+    fake = torch.zeros(S, cfg.tokens_per_frame, D)
+    fake[:, 0] = tok
+    ref = R.camera_head(fake, sd, cfg)
+    got = camera_head(DeviceWeights(sd, cfg, "cuda"), tok.cuda())
+    assert len(got) == len(ref) == cfg.cam_iters
+    for i, (a, b) in enumerate(zip(got, ref)):
+        assert a.shape == (S, 9)
+        ang, terr = R.pose_errors(a.cpu(), b)
+        assert ang.max() < 1e-2 and terr.max() < 1e-2, (i, ang.max().item(), terr.max().item())
+        assert rel(a.cpu(), b) < 1e-2, i
+    # the learnable iteration-0 input matters: the zeros the round-1 code used give another result
+    sd0 = dict(sd)
+    sd0["camera_head.empty_pose_tokens"] = torch.zeros(1, 1, 9)
+    other = camera_head(DeviceWeights(sd0, cfg, "cuda"), tok.cuda())
+    assert rel(other[0].cpu(), ref[0]) > 2e-2

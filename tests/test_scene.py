@@ -188,3 +188,40 @@ def test_device_matched_points_mixed_map_sizes(sc):
                                                     MP["R"], MP["t"], _kinv(MP["intr"]), 0.3)
     assert sk == ref_sk and pts.shape == ref_pts.shape
     np.testing.assert_allclose(pts, ref_pts, rtol=1e-12, atol=1e-12)
+
+
+def test_matched_points_rejects_out_of_rig_frame_index():
+    """A pair naming a frame past the rig fails like the reference's rig[frame] (IndexError), before any
+    device work (the kernel would otherwise read past the camera arrays)."""
+    from paper_2509_25191_b200 import scene
+    dm = MP["depth_sparse"]
+    n = len(MP["R"])
+    pij = MP["pair_ij"].copy()
+    pij[0, 1] = n
+    maps = {f: dm[0] for f in range(n + 1)}
+    with pytest.raises(IndexError):
+        scene.select_matched_points_arrays(pij, MP["offsets"], MP["xy_i"], MP["xy_j"], MP["w"], maps, MP["R"],
+                                           MP["t"], _kinv(MP["intr"]), 0.3)
+    pij[0, 1] = -n - 1
+    maps[-n - 1] = dm[0]
+    with pytest.raises(IndexError):
+        scene.select_matched_points_arrays(pij, MP["offsets"], MP["xy_i"], MP["xy_j"], MP["w"], maps, MP["R"],
+                                           MP["t"], _kinv(MP["intr"]), 0.3)
+
+
+@pytest.mark.gpu
+def test_device_matched_points_negative_frame_index_wraps(sc):
+    """rig[-1] wraps in the reference while the depth map is looked up under the key -1."""
+    dm = MP["depth_dense"]
+    n = len(MP["R"])
+    pij = MP["pair_ij"].copy()
+    j_old = int(pij[0, 1])
+    pij[0, 1] = j_old - n  # same camera, negative index
+    depths = {f: dm[f] for f in range(len(dm))}
+    depths[j_old - n] = dm[(j_old + 1) % len(dm)]  # a different map under the negative key
+    ref_pts, ref_sc, ref_sk = scene_ref.select_matched_points(pij, MP["offsets"], MP["xy_i"], MP["xy_j"], MP["w"],
+                                                              depths, MP["R"], MP["t"], MP["intr"], 0.3)
+    pts, cons, sk = sc.select_matched_points_arrays(pij, MP["offsets"], MP["xy_i"], MP["xy_j"], MP["w"], depths,
+                                                    MP["R"], MP["t"], _kinv(MP["intr"]), 0.3)
+    assert sk == ref_sk and pts.shape == ref_pts.shape
+    np.testing.assert_allclose(pts, ref_pts, rtol=1e-12, atol=1e-12)

@@ -28,45 +28,79 @@ def rel(a, b):
     return ((a - b).norm() / b.norm()).item()
 
 
-def _check(cfg, sd, images, ref, label):
+def inc_rel(got, ref, x0):
+    """Residual-increment error ||got - ref|| / ||ref - x0||: the error measured against what the
+    blocks ADDED to the embedding x0, not against the token norm (which the embedding dominates at
+    LayerScale 0.01, so a broken cross-view path could hide under a plain relative error)."""
+    got, ref, x0 = got.detach().float().cpu(), ref.detach().float().cpu(), x0.detach().float().cpu()
+    return ((got - ref).norm() / (ref - x0).norm()).item()
+
+
+def _run(cfg, sd, images):
     from paper_2509_25191_b200.vggt import VGGT
     model = VGGT(cfg, state_dict=sd)
     out = model(images.cuda())
     kept, psi = model.aggregator(images.cuda())
     assert psi == cfg.patch_start_idx
-    report = {}
+    return out, kept
+
+
+def _report(cfg, out, kept, ref):
+    """Every output against the oracle: kept layers as residual increments (frame / global halves),
+    dense maps and confidences as relative errors, decoded poses as angles / translation errors."""
+    C = cfg.embed_dim
+    x0 = ref["kept0_in"]
+    rep = {}
     for i in cfg.kept_layers:
-        C = cfg.embed_dim
         got = kept[i][0]
         assert got.dtype == torch.bfloat16 and got.shape == ref["kept"][i].shape
-        report[f"kept{i}"] = rel(got, ref["kept"][i])
-        report[f"kept{i}_frame"] = rel(got[..., :C], ref["kept"][i][..., :C])
-        report[f"kept{i}_global"] = rel(got[..., C:], ref["kept"][i][..., C:])
-        assert report[f"kept{i}"] <= TOL_TOKENS, (label, report)
-    report["depth"] = rel(out["depth"], ref["depth"])
-    report["depth_conf"] = rel(out["depth_conf"], ref["depth_conf"])
-    report["world_points"] = rel(out["world_points"], ref["world_points"])
-    report["world_points_conf"] = rel(out["world_points_conf"], ref["world_points_conf"])
+        rep[f"kept{i}"] = rel(got, ref["kept"][i])
+        rep[f"kept{i}_frame_inc"] = inc_rel(got[..., :C], ref["kept"][i][..., :C], x0)
+        rep[f"kept{i}_global_inc"] = inc_rel(got[..., C:], ref["kept"][i][..., C:], x0)
+    for k in ("depth", "depth_conf", "world_points", "world_points_conf"):
+        rep[k] = rel(out[k], ref[k])
     ang, terr = R.pose_errors(out["pose_enc"][0].cpu(), ref["pose_enc"][0])
-    report["rot_rad_max"] = ang.max().item()
-    report["trans_rel_max"] = terr.max().item()
-    print(label, {k: f"{v:.2e}" for k, v in report.items()})
-    assert report["depth"] <= TOL_DEPTH, (label, report)
-    assert report["world_points"] <= 2e-2, (label, report)
-    assert report["rot_rad_max"] <= TOL_ROT, (label, report)
-    assert report["trans_rel_max"] <= TOL_TRANS, (label, report)
-    assert out["pose_enc"].shape == (1, images.shape[0], 9)
-    assert out["depth"].shape == (1, images.shape[0], cfg.img_size, cfg.img_size, 1)
-    assert out["world_points"].shape == (1, images.shape[0], cfg.img_size, cfg.img_size, 3)
-    return report
+    rep["rot_rad_max"] = ang.max().item()
+    rep["trans_rel_max"] = terr.max().item()
+    return rep
+
+
+def _violations(rep, tol_tokens=TOL_TOKENS, increments=False):
+    """Names of the outputs outside the north-star tolerances (relative <= 1e-2 on aggregator tokens,
+    depth, points and confidences; <= 1e-2 rad / 1% translation on poses).  `increments` scores the
+    kept tokens on their residual increments: only meaningful where the blocks add a sizeable part of
+    the token (LayerScale ~1); at LayerScale 0.01 the increment is a few 1e-3 of the token norm, below
+    the bf16 storage rounding of the kept tokens (2^-9), so those configs use the plain error."""
+    if increments:
+        bad = [k for k, v in rep.items() if k.endswith("_inc") and v > tol_tokens]
+    else:
+        bad = [k for k, v in rep.items() if k.startswith("kept") and "_" not in k and v > tol_tokens]
+    bad += [k for k in ("depth", "depth_conf", "world_points", "world_points_conf") if rep[k] > TOL_DEPTH]
+    if rep["rot_rad_max"] > TOL_ROT:
+        bad.append("rot_rad_max")
+    if rep["trans_rel_max"] > TOL_TRANS:
+        bad.append("trans_rel_max")
+    return bad
+
+
+def _check(cfg, sd, images, ref, label, tol_tokens=TOL_TOKENS, increments=False):
+    out, kept = _run(cfg, sd, images)
+    rep = _report(cfg, out, kept, ref)
+    print(label, {k: f"{v:.2e}" for k, v in rep.items()})
+    bad = _violations(rep, tol_tokens, increments)
+    assert not bad, (label, bad, rep)
+    S = images.shape[0]
+    assert out["pose_enc"].shape == (1, S, 9)
+    assert out["depth"].shape == (1, S, cfg.img_size, cfg.img_size, 1)
+    assert out["world_points"].shape == (1, S, cfg.img_size, cfg.img_size, 3)
+    return rep
 
 
 def _oracle(cfg, sd, images):
     torch.set_num_threads(max(1, os.cpu_count() or 1))
     ref = R.vggt_forward(images, sd, cfg)
     S = images.shape[0]
-    x0 = torch.cat([R.special_tokens(sd, cfg, S), R.patch_embed(images, sd, cfg)], dim=1)
-    ref["kept0_in"] = x0
+    ref["kept0_in"] = torch.cat([R.special_tokens(sd, cfg, S), R.patch_embed(images, sd, cfg)], dim=1)
     return ref
 
 
@@ -88,7 +122,7 @@ def test_small_d64(init_values):
     cfg = vggt_small().with_(init_values=init_values)
     sd = make_state_dict(cfg, 0)
     images = synthetic_images(cfg, 5, 1)
-    _check(cfg, sd, images, _oracle(cfg, sd, images), f"small(ls={init_values})")
+    _check(cfg, sd, images, _oracle(cfg, sd, images), f"small(ls={init_values})", increments=init_values >= 0.5)
 
 
 def test_vggt1b_two_views():
@@ -99,10 +133,80 @@ def test_vggt1b_two_views():
     _check(cfg, sd, images, _oracle(cfg, sd, images), "1b-s2")
 
 
+# ---------------------------------------------------------------------------------------------------
+# Discriminative end-to-end parity: LayerScale 1.0, so the 48 blocks carry most of the kept tokens, and
+# the kept layers are scored on their residual increments.  The negative controls break the cross-view
+# paths on purpose (alternating frame-wise and GLOBAL attention; the camera head attends
+# across frames) and must fail the same checks.
+@pytest.fixture(scope="module")
+def ls1_case():
+    cfg = vggt_1b().with_(init_values=1.0, cam_init_values=1.0)  # aggregator and camera-trunk LayerScale
+    sd = make_state_dict(cfg, 0)
+    images = synthetic_images(cfg, 4, 1)
+    return cfg, sd, images, _oracle(cfg, sd, images)
+
+
+def test_vggt1b_layerscale1_increments(ls1_case):
+    """VGGT-1B-shaped, S = 4, LayerScale 1.0: kept tokens within 1e-2 on their residual increments."""
+    cfg, sd, images, ref = ls1_case
+    _check(cfg, sd, images, ref, "1b-s4-ls1", increments=True)
+
+
+def _patch_attention(monkeypatch, rule):
+    from paper_2509_25191_b200 import ops
+    real = ops.attention
+
+    def patched(q, k, v, out, nseq, Lq, Lk, lse=None):
+        return rule(real, q, k, v, out, nseq, Lq, Lk, lse)
+
+    monkeypatch.setattr(ops, "attention", patched)
+
+
+def test_negative_control_frame_only_global_attention_fails(ls1_case, monkeypatch):
+    """Every global block attends within its own frame only (no token crosses views): the global
+    halves of the kept layers must leave the tolerance."""
+    cfg, sd, images, ref = ls1_case
+    S, N = images.shape[0], cfg.tokens_per_frame
+
+    def frame_only(real, q, k, v, out, nseq, Lq, Lk, lse):
+        if nseq == 1 and Lq == S * N:  # a global block
+            return real(q, k, v, out, nseq=S, Lq=N, Lk=N, lse=lse)
+        return real(q, k, v, out, nseq=nseq, Lq=Lq, Lk=Lk, lse=lse)
+
+    _patch_attention(monkeypatch, frame_only)
+    out, kept = _run(cfg, sd, images)
+    rep = _report(cfg, out, kept, ref)
+    print("frame-only global attention", {k: f"{v:.2e}" for k, v in rep.items()})
+    bad = _violations(rep, increments=True)
+    assert [k for k in bad if k.endswith("_global_inc")], rep
+    assert max(rep[f"kept{i}_global_inc"] for i in cfg.kept_layers) > 3 * TOL_TOKENS, rep
+
+
+def test_negative_control_camera_trunk_self_attention_fails(ls1_case, monkeypatch):
+    """The camera-head trunk attends to each view's own token only (no attention across frames): the
+    decoded poses must leave the tolerance."""
+    cfg, sd, images, ref = ls1_case
+    S = images.shape[0]
+
+    def self_only(real, q, k, v, out, nseq, Lq, Lk, lse):
+        if q.shape[-1] == 2 * cfg.embed_dim // cfg.cam_num_heads and Lq == S:  # the camera trunk (d = 128)
+            H, _, d = v.shape
+            out.copy_(v.permute(1, 0, 2).reshape(S, H * d))  # softmax over one key = that key's value
+            return out
+        return real(q, k, v, out, nseq=nseq, Lq=Lq, Lk=Lk, lse=lse)
+
+    _patch_attention(monkeypatch, self_only)
+    out, kept = _run(cfg, sd, images)
+    rep = _report(cfg, out, kept, ref)
+    print("camera trunk self-attention only", {k: f"{v:.2e}" for k, v in rep.items()})
+    bad = _violations(rep, increments=True)
+    assert "rot_rad_max" in bad or "trans_rel_max" in bad, rep
+
+
 def test_frame_chunking_is_exact():
-    """frame_chunk changes only the schedule: bit-identical aggregator tokens (the vx
-    kernels are row-deterministic); heads within 1e-5 (cuDNN picks batch-dependent
-    conv algorithms)."""
+    """frame_chunk / head_chunk change only the schedule: bit-identical aggregator tokens (the vx
+    kernels are row-deterministic); heads within 1e-5 (the DPT GEMM tiles and the FMHA's KV split
+    depend on the chunk's row count)."""
     from paper_2509_25191_b200.vggt import VGGT
     cfg = vggt_small()
     sd = make_state_dict(cfg, 0)

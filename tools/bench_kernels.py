@@ -3,6 +3,7 @@ comparators (torch SDPA / cuBLAS).  CUDA events, warm-up, L2 flushed between rep
 
     python tools/bench_kernels.py [--views 20] [--only attn|gemm|ln]
 """
+import _vxdiag  # noqa: F401  (VX_LIB=<path> binds a -DVX_DIAG build)
 import argparse
 import json
 import os

@@ -4,6 +4,7 @@ Shape of rank r's step at S views over g ranks: Lq = Lk = (S/g) * 1374 tokens, 1
 Prints ms per step and TFLOP/s (best of --reps after warm-up); VX_FMHA_SPLIT=0 disables the
 KV-split tail for A/B runs.
 """
+import _vxdiag  # noqa: F401  (VX_LIB=<path> binds a -DVX_DIAG build)
 import argparse
 import json
 import os

@@ -1,3 +1,4 @@
+import _vxdiag  # noqa: F401  (VX_LIB=<path> binds a -DVX_DIAG build)
 import torch, math, sys
 sys.path.insert(0, '.')
 from paper_2509_25191_b200 import ops

@@ -1,4 +1,5 @@
 """A/B of two library builds (VX_LIB) on the DPT heads phase at 20 / 200 views (heads on side streams)."""
+import _vxdiag  # noqa: F401  (VX_LIB=<path> binds a -DVX_DIAG build)
 import os, sys
 sys.path.insert(0, os.getcwd())
 import torch

@@ -1,3 +1,4 @@
+import _vxdiag  # noqa: F401  (VX_LIB=<path> binds a -DVX_DIAG build)
 import sys, os, time, dataclasses
 sys.path.insert(0, os.getcwd())
 import torch

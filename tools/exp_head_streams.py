@@ -1,4 +1,5 @@
 """DPT heads on two streams vs sequential (VX_HEAD_STREAMS), 20 and 200 views."""
+import _vxdiag  # noqa: F401  (VX_LIB=<path> binds a -DVX_DIAG build)
 import os, sys
 sys.path.insert(0, os.getcwd())
 import torch

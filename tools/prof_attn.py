@@ -1,4 +1,5 @@
 """Minimal driver for ncu: one global-attention launch at the S=20 VGGT-1B shape (+1 warm-up)."""
+import _vxdiag  # noqa: F401  (VX_LIB=<path> binds a -DVX_DIAG build)
 import os, sys
 import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))

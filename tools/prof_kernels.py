@@ -5,6 +5,7 @@ Launch order (second pass is the profiled one): layernorm, gemm QKV, fmha frame,
 gemm proj (resid), gemm fc1 (gelu), gemm fc2 (resid), DPT 3x3 conv (148^2, 256->256),
 DPT fused output head (518^2), upsample 296->518.
 """
+import _vxdiag  # noqa: F401  (VX_LIB=<path> binds a -DVX_DIAG build)
 import os
 import sys
 

@@ -7,6 +7,7 @@ so alternate configurations from the shell: tools/sustain_attn.sh.
 """
 from __future__ import annotations
 
+import _vxdiag  # noqa: F401  (VX_LIB=<path> binds a -DVX_DIAG build)
 import argparse
 import json
 import os

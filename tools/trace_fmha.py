@@ -6,6 +6,7 @@ unit: wait-for-S, S->max, exps, tail (store P, rescale, arrive), and the MMA thr
     python tools/trace_fmha.py build     # here (nvcc)
     python tools/trace_fmha.py run       # on the GPU box
 """
+import _vxdiag  # noqa: F401  (VX_LIB=<path> binds a -DVX_DIAG build)
 import ctypes
 import os
 import subprocess
@@ -33,10 +34,9 @@ def build():
 
 
 def run():
-    os.environ["VX_LIB"] = LIB
     import torch
     from paper_2509_25191_b200 import ops
-    lib = ops.load_library()
+    lib = ops.use_library(LIB)
     buf = torch.zeros(8192, dtype=torch.int64, device="cuda")
     lib.vx_fmha_set_trace.argtypes = [ctypes.c_void_p]
     views = int(os.environ.get("VIEWS", "20"))
