@@ -48,6 +48,25 @@ def load_peaks():
     return d
 
 
+def self_launch(args) -> None:
+    """`bench.py --gpus N` outside torchrun: re-exec this command under torch.distributed.run with N
+    ranks (one process per GPU, rendezvous on 127.0.0.1); fail loudly if fewer than N GPUs exist."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ or args.impl == "reference":
+        return  # the reference arm runs on rank 0's host cores only: nothing to launch
+    n = torch.cuda.device_count()
+    if n < args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {n}")
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -99,7 +118,7 @@ def run_reference(args):
         secs.append(r["measured_s"])
     v = statistics.median(vals)
     line = {
-        "impl": "reference", "metric": METRIC, "value": v, "unit": "views/s", "n_gpus": world,
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "views/s", "n_gpus": max(world, args.gpus),
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * statistics.median(secs),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (torch.rand views seed 1, random-init weights seed 0)",
@@ -168,6 +187,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-heads", action="store_true", help="aggregator only (diagnostic)")
     args = ap.parse_args()
+    self_launch(args)
+    if "WORLD_SIZE" in os.environ and int(os.environ["WORLD_SIZE"]) != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={os.environ['WORLD_SIZE']}")
     if args.impl == "reference":
         return run_reference(args)
 

@@ -79,16 +79,27 @@ class Workspace:
     h: torch.Tensor
 
 
-def alloc_workspace(cfg: VGGTConfig, S: int, device="cuda") -> Workspace:
+def alloc_workspace(cfg: VGGTConfig, S: int, device="cuda", rows_per_head: Optional[int] = None,
+                    kv: Optional[tuple] = None) -> Workspace:
+    """Per-forward buffers for S views.  `rows_per_head` (>= S * tokens_per_frame) is the per-head row
+    stride of q/k/v; `kv` = (k, v) [H, rows_per_head, d] supplied by the frame-sharded ring (its send
+    buffer: the QKV epilogue then writes the local K/V where the first ring step sends them from)."""
     T = S * cfg.tokens_per_frame
+    R = rows_per_head or T
+    if R < T:
+        raise ValueError(f"rows_per_head {R} < {T} tokens")
     C, H, d = cfg.embed_dim, cfg.num_heads, cfg.head_dim
     chunk_rows = min(S, cfg.frame_chunk) * cfg.tokens_per_frame
+    if kv is None:
+        kv = tuple(torch.empty(H, R, d, device=device, dtype=torch.bfloat16) for _ in range(2))
+    elif any(tuple(t.shape) != (H, R, d) or not t.is_contiguous() for t in kv):
+        raise ValueError("kv buffers must be contiguous [H, rows_per_head, d]")
     return Workspace(
         x=torch.empty(T, C, device=device, dtype=torch.float32),
         xn=torch.empty(T, C, device=device, dtype=torch.bfloat16),
-        q=torch.empty(H, T, d, device=device, dtype=torch.bfloat16),
-        k=torch.empty(H, T, d, device=device, dtype=torch.bfloat16),
-        v=torch.empty(H, T, d, device=device, dtype=torch.bfloat16),
+        q=torch.empty(H, R, d, device=device, dtype=torch.bfloat16),
+        k=kv[0],
+        v=kv[1],
         o=torch.empty(T, C, device=device, dtype=torch.bfloat16),
         h=torch.empty(chunk_rows, cfg.mlp_hidden, device=device, dtype=torch.bfloat16),
     )
@@ -113,7 +124,7 @@ def run_block(W: DeviceWeights, name: str, ws: Workspace, S: int, frame_attn: bo
                  qkv=(ws.q, ws.k, ws.v),
                  qk_norm=(W[name + ".attn.q_norm.weight"], W[name + ".attn.q_norm.bias"],
                           W[name + ".attn.k_norm.weight"], W[name + ".attn.k_norm.bias"]),
-                 rope=W.rope, head_dim=cfg.head_dim, tokens_total=T, tokens_per_frame=N,
+                 rope=W.rope, head_dim=cfg.head_dim, tokens_total=ws.q.shape[1], tokens_per_frame=N,
                  patch_start=cfg.patch_start_idx, grid_w=cfg.grid, eps=cfg.ln_eps)
     if frame_attn:
         with phase("attn_frame"):

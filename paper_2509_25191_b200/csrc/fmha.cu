@@ -58,7 +58,14 @@ struct AttnArgs {
   int split_from, parts, work;
   float* part_o;
   float* part_lse;
+  // dynamic work distribution: sched[0] = next work-item ticket past the first wave, sched[1] = CTAs
+  // finished (the last one resets both, so the counters are zero again for the next launch on the
+  // stream); nullptr = static round-robin (while a stream is being captured before the counters exist)
+  unsigned* sched;
 };
+
+// work-item queue depth (shared-memory ring from the TMA producer to the MMA and softmax warps)
+constexpr int WQ = 4;
 
 // work item w -> unit, first KV tile, KV tile count, part (-1: whole unit), tail index
 struct WorkItem {
@@ -190,7 +197,10 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
   uint64_t* p_full = s_free + NT;    // [NT] softmax -> MMA: P_i(j) written (O rescaled)
   uint64_t* p_free = p_full + NT;    // [NT] MMA -> softmax: PV_i(j) done (P reusable, O stable)
   uint64_t* o_empty = p_free + NT;   // [NT] softmax -> MMA: O_i read by the epilogue
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + NT);
+  uint64_t* wq_full = o_empty + NT;  // [WQ] producer -> consumers: work item published
+  uint64_t* wq_empty = wq_full + WQ; // [WQ] MMA warp + softmax warps -> producer: slot read
+  volatile int* wq = reinterpret_cast<volatile int*>(wq_empty + WQ);  // [WQ] work item indices
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wq_empty + WQ) + WQ;
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -214,6 +224,10 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
       mbar_init(&p_free[i], 1);
       mbar_init(&o_empty[i], 4);
     }
+    for (int i = 0; i < WQ; ++i) {
+      mbar_init(&wq_full[i], 1);
+      mbar_init(&wq_empty[i], 1 + 4 * NT);  // the MMA warp and every softmax warp
+    }
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, 512);
@@ -233,14 +247,34 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
 
   const int per_head = a.nseq * a.q_blocks;
 
+  // the n-th work item of this CTA is published by the producer through wq[n % WQ]: the first is
+  // blockIdx.x, later ones come from the launch's atomic ticket counter, so a CTA that started late
+  // (its SM busy with a concurrent kernel, e.g. the NCCL ring transfer) simply takes fewer units
+  auto wq_take = [&](uint32_t n) -> int {  // warp-collective consumer side
+    const uint32_t slot = n % WQ;
+    mbar_wait(&wq_full[slot], (n / WQ) & 1);
+    const int w = wq[slot];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&wq_empty[slot]);
+    return w;
+  };
+
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (elect_one()) {
       const uint64_t pol_kv = policy_evict_last();
       const uint64_t pol_q = policy_evict_first();
       uint32_t c = 0;  // global K/V tile counter
-      uint32_t n = 0;  // local unit counter
-      for (int w = blockIdx.x; w < a.work; w += gridDim.x, ++n) {
+      for (uint32_t n = 0;; ++n) {  // n: local unit counter
+        const int w = n == 0 ? int(blockIdx.x)
+                             : (a.sched ? int(gridDim.x + atomicAdd(a.sched, 1u)) : int(blockIdx.x + n * gridDim.x));
+        {
+          const uint32_t slot = n % WQ;
+          mbar_wait(&wq_empty[slot], ((n / WQ) & 1) ^ 1);
+          wq[slot] = w;
+          mbar_arrive(&wq_full[slot]);
+        }
+        if (w >= a.work) break;
         const WorkItem wi = work_item(a, w);
         const int u = wi.u;
         const int h = u / per_head;
@@ -305,7 +339,9 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
       uint32_t n = 0;  // local unit counter
       uint32_t sfree_ph = 0, pfull_ph = 0;
       if constexpr (ALIAS) {
-        for (int w = blockIdx.x; w < a.work; w += gridDim.x, ++n) {
+        for (;; ++n) {
+          const int w = wq_take(n);
+          if (w >= a.work) break;
           const int nkv = work_item(a, w).cnt;
           mbar_wait(q_full, n & 1);
           tc_fence_after();
@@ -353,7 +389,9 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
           }
         }
       } else {
-        for (int w = blockIdx.x; w < a.work; w += gridDim.x, ++n) {
+        for (;; ++n) {
+          const int w = wq_take(n);
+          if (w >= a.work) break;
           const int nkv = work_item(a, w).cnt;
           mbar_wait(q_full, n & 1);
           tc_fence_after();
@@ -417,7 +455,9 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
     const uint64_t SL2 = f2_pack(sl2, sl2);
     uint32_t sph = 0, pv_cnt = 0;
     [[maybe_unused]] int unit_n = 0;
-    for (int w = blockIdx.x; w < a.work; w += gridDim.x, ++unit_n) {
+    for (;; ++unit_n) {
+      const int w = wq_take(uint32_t(unit_n));
+      if (w >= a.work) break;
       const WorkItem wi = work_item(a, w);
       const int nkv = wi.cnt;
       const int u = wi.u;
@@ -657,6 +697,13 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
+  if (a.sched && threadIdx.x == 0) {  // every ticket of this CTA is taken: the last CTA resets the counters
+    __threadfence();
+    if (atomicAdd(a.sched + 1, 1u) == gridDim.x - 1) {
+      atomicExch(a.sched, 0u);
+      atomicExch(a.sched + 1, 0u);
+    }
+  }
 }
 
 // Combines the KV-split tail items: one thread per (tail row, 4 output columns); the threads of a
@@ -755,6 +802,33 @@ static float* split_scratch(cudaStream_t st, size_t floats) {
   return p;
 }
 
+// Per-stream work-ticket counters of the FMHA (2 x u32, zero between launches: each launch's last
+// CTA resets them). Allocated and zeroed once per stream; not while the stream is being captured
+// (the launch then falls back to static round-robin scheduling).
+static unsigned* sched_counters(cudaStream_t st) {
+#ifdef VX_DIAG
+  static const bool off = [] {
+    const char* e = getenv("VX_FMHA_STATIC");  // diagnostic build only: 1 = static round-robin
+    return e && atoi(e) == 1;
+  }();
+  if (off) return nullptr;
+#endif
+  static std::mutex mu;
+  static std::map<cudaStream_t, unsigned*> ctrs;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = ctrs.find(st);
+  if (it != ctrs.end()) return it->second;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
+  unsigned* p = nullptr;
+  if (cudaMalloc(&p, 2 * sizeof(unsigned)) != cudaSuccess || cudaMemset(p, 0, 2 * sizeof(unsigned)) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  ctrs[st] = p;
+  return p;
+}
+
 template <int D, int EMU, int NT = (D == 128 ? 1 : 2), int BKV = 128, bool ALIAS = false, bool SUMV = false,
           bool NOHINT = false, bool SPEC = false, bool LDSPLIT = false>
 static int launch_fmha(const void* q, const void* k, const void* v, AttnArgs args, cudaStream_t st) {
@@ -805,6 +879,7 @@ static int launch_fmha(const void* q, const void* k, const void* v, AttnArgs arg
     attr_set = true;
   }
   const int grid = args.work < sms ? args.work : sms;
+  args.sched = args.work > grid ? sched_counters(st) : nullptr;  // one wave: nothing to distribute
   kern<<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(tq, tk, tv, args);
   VX_CHECK_LAUNCH("fmha launch");
   if (args.split_from < args.units) {

@@ -11,12 +11,21 @@ log-sum-exp rule inside the FMHA epilogue (vx_attention_merge: no separate
 merge kernels; the last step writes the bf16 output).  Because RoPE positions are per frame and attention is
 non-causal, every step has identical work (no zig-zag needed).
 
+Memory: the two packed ring buffers and the fp32 (O, lse) accumulators are
+allocated once per forward (`begin`), and the QKV GEMM epilogue of every block
+writes this rank's K/V straight into ring buffer 0 (`kv_buffers`), so a global
+layer starts its first ring step without a copy.  The FMHA hands out its work
+units through an atomic ticket counter, so the SMs an NCCL transfer kernel
+occupies at the start of a ring step only delay the units they would have run.
+
 Every rank passes the full view batch (or its own slice); frame 0 carries the
 "first frame" special tokens, so only the rank that owns global frame 0 uses
 them (aggregator.embed(frame0_is_first=...)).
 
-The attention / merge functions are injectable so the ring schedule is tested
-on CPU with gloo (tests/test_ring_cpu.py) against monolithic attention.
+The communicator (`TorchDistComm`: torch.distributed, NCCL on B200) and the
+attention / merge functions are injectable, so the ring schedule is tested on
+CPU with gloo (tests/test_ring_cpu.py) and the whole sharded forward with g
+simulated ranks in threads on one GPU (tests/test_sharded_forward.py).
 """
 from __future__ import annotations
 
@@ -52,29 +61,50 @@ def _vx_partial(q, k, v, out, lse, Lq, Lk):
     ops.attention(q, k, v, out, nseq=1, Lq=Lq, Lk=Lk, lse=lse)
 
 
-class FrameShardedRing:
-    def __init__(self, cfg: VGGTConfig, device, group=None,
-                 partial_attention: Optional[Callable] = None, merge: Callable = lse_merge):
+class TorchDistComm:
+    """The ring's exchange over torch.distributed (NCCL P2P on B200, gloo in the CPU tests)."""
+
+    def __init__(self, group=None):
         if not dist.is_initialized():
             raise RuntimeError("FrameShardedRing needs torch.distributed to be initialised (torchrun)")
-        self.cfg = cfg
-        self.device = torch.device(device)
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+
+    def sendrecv(self, send: torch.Tensor, recv: torch.Tensor, to: int, frm: int) -> list:
+        """Start sending `send` to rank `to` and receiving `recv` from rank `frm`; returns requests to
+        wait() on (torch orders the NCCL stream after the current stream at issue, and wait() orders
+        the current stream after the transfer)."""
+        ops_ = [dist.P2POp(dist.isend, send, to, group=self.group),
+                dist.P2POp(dist.irecv, recv, frm, group=self.group)]
+        return dist.batch_isend_irecv(ops_)
+
+    def all_gather(self, outs: List[torch.Tensor], x: torch.Tensor) -> None:
+        dist.all_gather(outs, x, group=self.group)
+
+
+class FrameShardedRing:
+    def __init__(self, cfg: VGGTConfig, device, group=None, comm=None,
+                 partial_attention: Optional[Callable] = None, merge: Callable = lse_merge):
+        self.cfg = cfg
+        self.device = torch.device(device)
+        self.comm = comm if comm is not None else TorchDistComm(group)
+        self.rank = self.comm.rank
+        self.world = self.comm.world
         # default: vx_attention_merge (LSE merge fused into the FMHA epilogue); injected functions are
         # for the CPU (gloo) tests of the ring schedule
         self.fused = partial_attention is None
         self.partial = partial_attention or _vx_partial
         self.merge = merge
         self.split: Optional[List[Tuple[int, int]]] = None
+        self._bufs = None  # (ring buffers [2, 2, H, Tmax, d], o_acc, lse_acc) of the current forward
 
     # -- frame partition ---------------------------------------------------
     def local_frames(self, images: torch.Tensor, sharded_input: bool):
         if sharded_input:
             n = torch.tensor([images.shape[0]], device=self.device if self.device.type == "cuda" else "cpu")
             sizes = [torch.zeros_like(n) for _ in range(self.world)]
-            dist.all_gather(sizes, n, group=self.group)
+            self.comm.all_gather(sizes, n)
             sizes = [int(s.item()) for s in sizes]
             offs = [sum(sizes[:r]) for r in range(self.world)]
             self.split = [(offs[r], offs[r] + sizes[r]) for r in range(self.world)]
@@ -91,22 +121,47 @@ class FrameShardedRing:
         lo, hi = self.split[r]
         return (hi - lo) * self.cfg.tokens_per_frame
 
+    @property
+    def rows_per_head(self) -> int:
+        """Tmax: rows per head of the packed ring blocks (the largest shard's tokens)."""
+        return max(self.tokens_of(i) for i in range(self.world))
+
+    # -- per-forward buffers -------------------------------------------------
+    def begin(self, H: Optional[int] = None, d: Optional[int] = None, dtype=torch.bfloat16):
+        """Allocate (or reuse, when the shapes did not change) the two packed ring buffers and the fp32
+        accumulators for this forward's shard."""
+        H = H or self.cfg.num_heads
+        d = d or self.cfg.head_dim
+        Tmax, Tl = self.rows_per_head, self.tokens_of(self.rank)
+        shape = (2, 2, H, Tmax, d)
+        if (self._bufs is None or tuple(self._bufs[0].shape) != shape or self._bufs[0].dtype != dtype
+                or self._bufs[1].shape[0] != Tl):
+            bufs = torch.empty(shape, device=self.device, dtype=dtype)
+            o_acc = torch.empty(Tl, H * d, device=self.device, dtype=torch.float32)
+            lse_acc = torch.empty(H, Tmax, device=self.device, dtype=torch.float32)
+            self._bufs = (bufs, o_acc, lse_acc)
+        return self._bufs
+
+    def kv_buffers(self) -> Tuple[torch.Tensor, torch.Tensor]:
+        """K and V of ring buffer 0 ([H, Tmax, d] each): the QKV epilogue writes the local K/V here."""
+        bufs = self._bufs[0]
+        return bufs[0, 0], bufs[0, 1]
+
     # -- global attention --------------------------------------------------
     def global_attention(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, o: torch.Tensor):
-        """q/k/v: local [H, T_local, d] bf16; o: [T_local, H*d] bf16 (written)."""
-        H, Tl, d = q.shape
+        """q/k/v: local [H, R, d] bf16 (rows 0..T_local-1 of each head valid, R >= T_local);
+        o: [T_local, H*d] bf16 (written)."""
+        H, _, d = q.shape
         g, r = self.world, self.rank
+        Tl = self.tokens_of(r)
         if g == 1:
             self.partial(q, k, v, o, None, Tl, Tl)
             return
-        Tmax = max(self.tokens_of(i) for i in range(g))
-        bufs = [torch.empty(2, H, Tmax, d, device=q.device, dtype=q.dtype) for _ in range(2)]
-        bufs[0][0, :, :Tl].copy_(k)
-        bufs[0][1, :, :Tl].copy_(v)
-        if self.fused:
-            o_acc = torch.empty(Tl, H * d, device=q.device, dtype=torch.float32)
-            lse_acc = torch.empty(H, Tl, device=q.device, dtype=torch.float32)
-        else:
+        bufs, o_acc, lse_acc = self.begin(H, d, q.dtype)  # no-op after VGGT._aggregate's begin()
+        if k.data_ptr() != bufs[0, 0].data_ptr():  # K/V not produced in place (tests, custom callers)
+            bufs[0, 0, :, :Tl].copy_(k[:, :Tl])
+            bufs[0, 1, :, :Tl].copy_(v[:, :Tl])
+        if not self.fused:
             o_acc = torch.zeros(Tl, H * d, device=q.device, dtype=torch.float32)
             lse_acc = torch.full((H, Tl), float("-inf"), device=q.device, dtype=torch.float32)
             o_s = torch.empty(Tl, H * d, device=q.device, dtype=o.dtype)
@@ -117,18 +172,16 @@ class FrameShardedRing:
             src = (r - step) % g            # owner of the K/V block held in bufs[cur]
             reqs = []
             if step < g - 1:
-                ops_ = [dist.P2POp(dist.isend, bufs[cur], nxt, group=self.group),
-                        dist.P2POp(dist.irecv, bufs[cur ^ 1], prv, group=self.group)]
-                reqs = dist.batch_isend_irecv(ops_)
+                reqs = self.comm.sendrecv(bufs[cur], bufs[cur ^ 1], nxt, prv)
             Lk = self.tokens_of(src)
-            kb = bufs[cur][0]
-            vb = bufs[cur][1]
+            kb = bufs[cur, 0]
+            vb = bufs[cur, 1]
             if self.fused:  # one launch: partial attention + running log-sum-exp merge (+ final bf16 write)
                 from . import ops
                 mode = 1 if step == 0 else (3 if step == g - 1 else 2)
                 ops.attention_merge(q, kb, vb, mode, o_acc, lse_acc, out=o, Lq=Tl, Lk=Lk)
             else:
-                self.partial(q, kb, vb, o_s, lse_s, Tl, Lk)
+                self.partial(q[:, :Tl], kb, vb, o_s, lse_s, Tl, Lk)
                 self.merge(o_acc, lse_acc, o_s, lse_s)
             for rq in reqs:
                 rq.wait()
@@ -144,5 +197,5 @@ class FrameShardedRing:
         pad = torch.zeros(m, *x.shape[1:], device=x.device, dtype=x.dtype)
         pad[: x.shape[0]].copy_(x)
         outs = [torch.empty_like(pad) for _ in range(self.world)]
-        dist.all_gather(outs, pad, group=self.group)
+        self.comm.all_gather(outs, pad)
         return torch.cat([o[:s] for o, s in zip(outs, sizes)], dim=0)

@@ -38,7 +38,9 @@ def _require_b200(device):
 
 class VGGT:
     def __init__(self, cfg: Optional[VGGTConfig] = None, state_dict=None, seed: int = 0, device="cuda",
-                 dist: bool = False):
+                 dist: bool = False, comm=None):
+        """dist=True: frame-sharded over the ranks of torch.distributed (or of `comm`, an object with
+        rank / world / sendrecv / all_gather like ring.TorchDistComm)."""
         self.cfg = cfg or vggt_1b()
         self.device = torch.device(device)
         _require_b200(self.device)
@@ -53,7 +55,7 @@ class VGGT:
         self.ring = None
         if dist:
             from .ring import FrameShardedRing
-            self.ring = FrameShardedRing(self.cfg, self.device)
+            self.ring = FrameShardedRing(self.cfg, self.device, comm=comm)
 
     # -- helpers ------------------------------------------------------------
     def _head_streams(self, dev):
@@ -86,8 +88,14 @@ class VGGT:
         return {i: t[None] for i, t in kept.items()}, self.cfg.patch_start_idx
 
     def _aggregate(self, local: torch.Tensor, f0: int) -> Dict[int, torch.Tensor]:
-        ws = alloc_workspace(self.cfg, local.shape[0], self.device)
-        gattn = None if self.ring is None else self.ring.global_attention
+        if self.ring is None:
+            ws = alloc_workspace(self.cfg, local.shape[0], self.device)
+            gattn = None
+        else:  # K/V produced straight into the ring's send buffer, ring buffers allocated once per forward
+            self.ring.begin()
+            ws = alloc_workspace(self.cfg, local.shape[0], self.device, rows_per_head=self.ring.rows_per_head,
+                                 kv=self.ring.kv_buffers())
+            gattn = self.ring.global_attention
         kept = aggregator_forward(self.W, local, ws, global_attn=gattn, frame0_is_first=(f0 == 0))
         del ws
         return kept

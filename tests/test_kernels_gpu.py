@@ -462,7 +462,10 @@ def test_camera_head_matches_oracle(cfg_name, S):
     from paper_2509_25191_b200.weights import make_state_dict
     cfg = vggt_tiny() if cfg_name == "tiny" else vggt_1b()
     sd = make_state_dict(cfg, 0)
-    sd["camera_head.empty_pose_tokens"] = torch.tensor([[[0.1, -0.2, 0.3, 0.05, -0.05, 0.02, 0.9, 0.5, 0.6]]])
+    sd["camera_head.empty_pose_tokens"] = torch.tensor([[[1.0, -2.0, 3.0, 0.5, -0.5, 0.2, 0.9, 1.5, 2.0]]])
+    # the seeded pose-branch output layer is scaled down for well-conditioned quaternions (weights.py);
+    # 10x here so the decoded poses respond to everything upstream of it (a sensitive check)
+    sd["camera_head.pose_branch.fc2.weight"] = sd["camera_head.pose_branch.fc2.weight"] * 10
     D = 2 * cfg.embed_dim
     g = torch.Generator().manual_seed(11)
     tok = (torch.randn(S, D, generator=g) * 0.5).to(torch.bfloat16).float()  # bf16-representable input
@@ -476,8 +479,11 @@ def test_camera_head_matches_oracle(cfg_name, S):
         ang, terr = R.pose_errors(a.cpu(), b)
         assert ang.max() < 1e-2 and terr.max() < 1e-2, (i, ang.max().item(), terr.max().item())
         assert rel(a.cpu(), b) < 1e-2, i
-    # the learnable iteration-0 input matters: the zeros the round-1 code used give another result
+    # the learnable iteration-0 input matters: the zeros the round-1 code used give a result further
+    # from the oracle than the device's own error
     sd0 = dict(sd)
     sd0["camera_head.empty_pose_tokens"] = torch.zeros(1, 1, 9)
     other = camera_head(DeviceWeights(sd0, cfg, "cuda"), tok.cuda())
-    assert rel(other[0].cpu(), ref[0]) > 2e-2
+    e_real, e_zero = rel(got[0].cpu(), ref[0]), rel(other[0].cpu(), ref[0])
+    print(cfg_name, "camera head iter-0 error", e_real, "with zero empty_pose_tokens", e_zero)
+    assert e_zero > 5 * e_real

@@ -122,7 +122,7 @@ def test_small_d64(init_values):
     cfg = vggt_small().with_(init_values=init_values)
     sd = make_state_dict(cfg, 0)
     images = synthetic_images(cfg, 5, 1)
-    _check(cfg, sd, images, _oracle(cfg, sd, images), f"small(ls={init_values})", increments=init_values >= 0.5)
+    _check(cfg, sd, images, _oracle(cfg, sd, images), f"small(ls={init_values})")
 
 
 def test_vggt1b_two_views():
@@ -142,6 +142,10 @@ def test_vggt1b_two_views():
 def ls1_case():
     cfg = vggt_1b().with_(init_values=1.0, cam_init_values=1.0)  # aggregator and camera-trunk LayerScale
     sd = make_state_dict(cfg, 0)
+    # the seeded pose-branch output layer is scaled down for well-conditioned quaternions (weights.py):
+    # 3x here so the decoded poses respond more to the camera tokens and the trunk (measured: the real
+    # build's rotation error is ~1.4e-3 rad per 1x of this scale, the self-attention-only trunk's ~5e-2)
+    sd["camera_head.pose_branch.fc2.weight"] = sd["camera_head.pose_branch.fc2.weight"] * 3
     images = synthetic_images(cfg, 4, 1)
     return cfg, sd, images, _oracle(cfg, sd, images)
 

@@ -1,8 +1,14 @@
-"""Time one ring step of frame-sharded global attention (vx_attention_merge, mode 2) on one GPU.
+"""Time one ring step of frame-sharded global attention (vx_attention_merge, mode 2) on one GPU, alone and
+with the ring's K/V transfer running concurrently.
 
-Shape of rank r's step at S views over g ranks: Lq = Lk = (S/g) * 1374 tokens, 16 heads, d=64.
-Prints ms per step and TFLOP/s (best of --reps after warm-up); VX_FMHA_SPLIT=0 disables the
-KV-split tail for A/B runs.
+Shape of rank r's step at S views over g ranks: Lq = Lk = (S/g) * 1374 tokens, 16 heads, d=64.  The
+concurrent transfer is a real NCCL send/recv of the step's packed K/V block (2 * 16 * Lk * 64 bf16,
+140 MB at S=200, g=8) through a world-size-1 process group (rank 0 sends to itself), issued exactly as
+ring.TorchDistComm does before the step's FMHA: its kernel takes SMs while the persistent FMHA grid
+starts.  Reports ms per step alone, NCCL alone, step + concurrent NCCL, and the overhead.
+
+A/B against static round-robin units: VX_LIB=exp/libvx_diag.so VX_FMHA_STATIC=1 (diagnostic build,
+paper_2509_25191_b200.build.build_diag).
 """
 import _vxdiag  # noqa: F401  (VX_LIB=<path> binds a -DVX_DIAG build)
 import argparse
@@ -20,27 +26,66 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     args = ap.parse_args()
     import torch
+    import torch.distributed as dist
     from paper_2509_25191_b200 import ops
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
     H, d = 16, 64
     res = {}
+
+    def timed(fn, reps):
+        ts = []
+        for _ in range(reps):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            s.record()
+            fn()
+            e.record()
+            e.synchronize()
+            ts.append(s.elapsed_time(e))
+        ts.sort()
+        return ts[len(ts) // 2]  # median
+
     for g in args.ranks:
         T = (args.views // g) * 1374
         q, k, v = (torch.randn(H, T, d, device="cuda").bfloat16() for _ in range(3))
         o_acc = torch.zeros(T, H * d, device="cuda")
         lse = torch.zeros(H, T, device="cuda")
-        for _ in range(3):
+        blk = torch.empty(2, H, T, d, device="cuda", dtype=torch.bfloat16)
+        rcv = torch.empty_like(blk)
+
+        def step():
             ops.attention_merge(q, k, v, 2, o_acc, lse, Lq=T, Lk=T)
+
+        def xfer():
+            return dist.batch_isend_irecv([dist.P2POp(dist.isend, blk, 0), dist.P2POp(dist.irecv, rcv, 0)])
+
+        def xfer_only():
+            for r in xfer():
+                r.wait()
+
+        def step_with_xfer():
+            reqs = xfer()
+            step()
+            for r in reqs:
+                r.wait()
+
+        for f in (step, xfer_only, step_with_xfer):
+            for _ in range(3):
+                f()
         torch.cuda.synchronize()
-        best = 1e30
-        for _ in range(args.reps):
-            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s.record()
-            ops.attention_merge(q, k, v, 2, o_acc, lse, Lq=T, Lk=T)
-            e.record()
-            e.synchronize()
-            best = min(best, s.elapsed_time(e))
-        res[f"g{g}"] = {"tokens": T, "ms": round(best, 3), "tflops": round(4.0 * H * T * T * d / best / 1e9, 1)}
-    print(json.dumps({"split": os.environ.get("VX_FMHA_SPLIT", "1"), "views": args.views, **res}))
+        t_step = timed(step, args.reps)
+        t_x = timed(xfer_only, args.reps)
+        t_both = timed(step_with_xfer, args.reps)
+        res[f"g{g}"] = {"tokens": T, "block_mb": round(blk.numel() * 2 / 1e6, 1), "step_ms": round(t_step, 3),
+                        "nccl_ms": round(t_x, 3), "step_with_nccl_ms": round(t_both, 3),
+                        "overhead_pct": round(100 * (t_both / t_step - 1), 2),
+                        "tflops": round(4.0 * H * T * T * d / t_step / 1e9, 1)}
+    sched = "static" if os.environ.get("VX_FMHA_STATIC") == "1" else "dynamic"
+    print(json.dumps({"sched": sched, "views": args.views, **res}))
+    dist.destroy_process_group()
 
 
 if __name__ == "__main__":
