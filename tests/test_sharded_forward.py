@@ -106,7 +106,7 @@ def test_sharded_forward_matches_single_gpu(cfg_name, world, S):
     ref = single(images.cuda())
     ref_kept, _ = single.aggregator(images.cuda())
     res, hub, split = _sharded(cfg, sd, images, world)
-    assert hub.exchanges == 2 * 2 * cfg.depth * (world - 1)  # forward + aggregator, g - 1 steps per global layer
+    assert hub.exchanges == 2 * cfg.depth * (world - 1)  # forward + aggregator: g - 1 ring steps per global layer
     pose0 = res[0][0]["pose_enc"]
     C = cfg.embed_dim
     for r, (out, kept) in enumerate(res):

@@ -8,7 +8,11 @@ ring.TorchDistComm does before the step's FMHA: its kernel takes SMs while the p
 starts.  Reports ms per step alone, NCCL alone, step + concurrent NCCL, and the overhead.
 
 A/B against static round-robin units: VX_LIB=exp/libvx_diag.so VX_FMHA_STATIC=1 (diagnostic build,
-paper_2509_25191_b200.build.build_diag).
+paper_2509_25191_b200.build.build_diag).  With the diagnostic build, --hog K also measures the step
+with K SMs held for --hog-us microseconds by a kernel launched just before it (512 threads and 120 KB
+of shared memory per CTA, so no FMHA CTA fits next to it): an NCCL transfer kernel that keeps its SMs
+for the transfer's duration, which the world-size-1 self send/recv above may not (it can take the copy
+engine).
 """
 import _vxdiag  # noqa: F401  (VX_LIB=<path> binds a -DVX_DIAG build)
 import argparse
@@ -24,6 +28,8 @@ def main():
     ap.add_argument("--views", type=int, default=200)
     ap.add_argument("--ranks", type=int, nargs="+", default=[2, 4, 8])
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--hog", type=int, nargs="*", default=[])
+    ap.add_argument("--hog-us", type=float, default=300.0)
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -83,8 +89,27 @@ def main():
                         "nccl_ms": round(t_x, 3), "step_with_nccl_ms": round(t_both, 3),
                         "overhead_pct": round(100 * (t_both / t_step - 1), 2),
                         "tflops": round(4.0 * H * T * T * d / t_step / 1e9, 1)}
+        if args.hog:
+            import ctypes
+            lib = ops.load_library() if ops._lib is None else ops._lib
+            if not hasattr(lib, "vx_diag_sm_hog"):
+                raise SystemExit("--hog needs the diagnostic library (VX_LIB=exp/libvx_diag.so)")
+            lib.vx_diag_sm_hog.argtypes = [ctypes.c_int, ctypes.c_longlong, ctypes.c_int, ctypes.c_void_p]
+            hog_stream = torch.cuda.Stream()
+            cycles = int(args.hog_us * 1e-6 * 1.9e9)
+            for k in args.hog:
+                def step_with_hog():
+                    hog_stream.wait_stream(torch.cuda.current_stream())
+                    assert lib.vx_diag_sm_hog(k, cycles, 120 * 1024, ctypes.c_void_p(hog_stream.cuda_stream)) == 0
+                    step()
+                    torch.cuda.current_stream().wait_stream(hog_stream)
+                for _ in range(2):
+                    step_with_hog()
+                t_h = timed(step_with_hog, args.reps)
+                res[f"g{g}"][f"step_with_hog{k}_ms"] = round(t_h, 3)
+                res[f"g{g}"][f"hog{k}_overhead_pct"] = round(100 * (t_h / t_step - 1), 2)
     sched = "static" if os.environ.get("VX_FMHA_STATIC") == "1" else "dynamic"
-    print(json.dumps({"sched": sched, "views": args.views, **res}))
+    print(json.dumps({"sched": sched, "views": args.views, "hog_us": args.hog_us if args.hog else None, **res}))
     dist.destroy_process_group()
 
 
