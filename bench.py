@@ -105,11 +105,12 @@ def run_reference(args):
     threads = os.cpu_count() or 1
     for _ in range(args.warmup):
         cpu_oracle_sample(cfg, sd, args.views, threads=threads)
-    vals, secs, r = [], [], None
+    vals, secs, fwd, r = [], [], [], None
     for _ in range(args.steps):
         r = cpu_oracle_sample(cfg, sd, args.views, threads=threads)
         vals.append(r["value"])
-        secs.append(r["forward_s"])
+        secs.append(r["measured_s"])  # wall time of the step's bounded sample
+        fwd.append(r["forward_s"])    # the composed S-view forward it measures
     v = statistics.median(vals)
     cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
     cpu["value"] = v
@@ -127,7 +128,7 @@ def run_reference(args):
                          "shape on a bounded slice and composes the forward, see cpu_baseline.sample)"},
         "cpu_baseline": cpu,
         "e2e": {"value": v, "unit": "views/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "step_wall_s": statistics.median(r2 for r2 in [r["measured_s"]]),
+        "composed_forward_s": statistics.median(fwd),
     }
     print(json.dumps(line), flush=True)
     return 0

@@ -97,17 +97,17 @@ def main():
             lib.vx_diag_sm_hog.argtypes = [ctypes.c_int, ctypes.c_longlong, ctypes.c_int, ctypes.c_void_p]
             hog_stream = torch.cuda.Stream()
             cycles = int(args.hog_us * 1e-6 * 1.9e9)
-            for k in args.hog:
+            for nh in args.hog:
                 def step_with_hog():
                     hog_stream.wait_stream(torch.cuda.current_stream())
-                    assert lib.vx_diag_sm_hog(k, cycles, 120 * 1024, ctypes.c_void_p(hog_stream.cuda_stream)) == 0
+                    assert lib.vx_diag_sm_hog(nh, cycles, 120 * 1024, ctypes.c_void_p(hog_stream.cuda_stream)) == 0
                     step()
                     torch.cuda.current_stream().wait_stream(hog_stream)
                 for _ in range(2):
                     step_with_hog()
                 t_h = timed(step_with_hog, args.reps)
-                res[f"g{g}"][f"step_with_hog{k}_ms"] = round(t_h, 3)
-                res[f"g{g}"][f"hog{k}_overhead_pct"] = round(100 * (t_h / t_step - 1), 2)
+                res[f"g{g}"][f"step_with_hog{nh}_ms"] = round(t_h, 3)
+                res[f"g{g}"][f"hog{nh}_overhead_pct"] = round(100 * (t_h / t_step - 1), 2)
     sched = "static" if os.environ.get("VX_FMHA_STATIC") == "1" else "dynamic"
     print(json.dumps({"sched": sched, "views": args.views, "hog_us": args.hog_us if args.hog else None, **res}))
     dist.destroy_process_group()
