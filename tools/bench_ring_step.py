@@ -19,6 +19,7 @@ import argparse
 import json
 import os
 import sys
+import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
@@ -30,6 +31,7 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--hog", type=int, nargs="*", default=[])
     ap.add_argument("--hog-us", type=float, default=300.0)
+    ap.add_argument("--hog-first", type=float, default=0.0, help="host delay (us) between the hog and the FMHA launch")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -101,6 +103,8 @@ def main():
                 def step_with_hog():
                     hog_stream.wait_stream(torch.cuda.current_stream())
                     assert lib.vx_diag_sm_hog(nh, cycles, 120 * 1024, ctypes.c_void_p(hog_stream.cuda_stream)) == 0
+                    if args.hog_first:  # let the hog CTAs become resident before the FMHA grid is launched
+                        time.sleep(args.hog_first * 1e-6)
                     step()
                     torch.cuda.current_stream().wait_stream(hog_stream)
                 for _ in range(2):
@@ -109,7 +113,8 @@ def main():
                 res[f"g{g}"][f"step_with_hog{nh}_ms"] = round(t_h, 3)
                 res[f"g{g}"][f"hog{nh}_overhead_pct"] = round(100 * (t_h / t_step - 1), 2)
     sched = "static" if os.environ.get("VX_FMHA_STATIC") == "1" else "dynamic"
-    print(json.dumps({"sched": sched, "views": args.views, "hog_us": args.hog_us if args.hog else None, **res}))
+    print(json.dumps({"sched": sched, "views": args.views, "hog_us": args.hog_us if args.hog else None,
+                      "hog_first_us": args.hog_first, **res}))
     dist.destroy_process_group()
 
 
