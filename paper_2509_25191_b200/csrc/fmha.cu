@@ -807,11 +807,10 @@ static float* split_scratch(cudaStream_t st, size_t floats) {
 // (the launch then falls back to static round-robin scheduling).
 static unsigned* sched_counters(cudaStream_t st) {
 #ifdef VX_DIAG
-  static const bool off = [] {
-    const char* e = getenv("VX_FMHA_STATIC");  // diagnostic build only: 1 = static round-robin
-    return e && atoi(e) == 1;
-  }();
-  if (off) return nullptr;
+  {  // diagnostic build only: VX_FMHA_STATIC=1 = static round-robin (read per launch for in-process A/B)
+    const char* e = getenv("VX_FMHA_STATIC");
+    if (e && atoi(e) == 1) return nullptr;
+  }
 #endif
   static std::mutex mu;
   static std::map<cudaStream_t, unsigned*> ctrs;

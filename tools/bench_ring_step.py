@@ -101,18 +101,41 @@ def main():
             cycles = int(args.hog_us * 1e-6 * 1.9e9)
             for nh in args.hog:
                 def step_with_hog():
+                    """FMHA step launched while `nh` SMs are held (the hog is resident first); timed from the
+                    FMHA launch to the later of the step's and the hog's end."""
                     hog_stream.wait_stream(torch.cuda.current_stream())
                     assert lib.vx_diag_sm_hog(nh, cycles, 120 * 1024, ctypes.c_void_p(hog_stream.cuda_stream)) == 0
-                    if args.hog_first:  # let the hog CTAs become resident before the FMHA grid is launched
-                        time.sleep(args.hog_first * 1e-6)
+                    time.sleep(args.hog_first * 1e-6)
+                    s_, e_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    s_.record()
                     step()
                     torch.cuda.current_stream().wait_stream(hog_stream)
-                for _ in range(2):
-                    step_with_hog()
-                t_h = timed(step_with_hog, args.reps)
-                res[f"g{g}"][f"step_with_hog{nh}_ms"] = round(t_h, 3)
-                res[f"g{g}"][f"hog{nh}_overhead_pct"] = round(100 * (t_h / t_step - 1), 2)
-    sched = "static" if os.environ.get("VX_FMHA_STATIC") == "1" else "dynamic"
+                    e_.record()
+                    e_.synchronize()
+                    return s_.elapsed_time(e_)
+
+                # alternate dynamic / static units (diagnostic build: VX_FMHA_STATIC read per launch) and the
+                # undisturbed step, so clock drift hits all three alike
+                ts = {"alone": [], "dynamic": [], "static": []}
+                for _ in range(args.reps):
+                    for mode in ("alone", "dynamic", "static"):
+                        os.environ["VX_FMHA_STATIC"] = "1" if mode == "static" else "0"
+                        torch.cuda.synchronize()
+                        if mode == "alone":
+                            s_, e_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                            s_.record()
+                            step()
+                            e_.record()
+                            e_.synchronize()
+                            ts[mode].append(s_.elapsed_time(e_))
+                        else:
+                            ts[mode].append(step_with_hog())
+                os.environ["VX_FMHA_STATIC"] = "0"
+                med = {k: sorted(v)[len(v) // 2] for k, v in ts.items()}
+                res[f"g{g}"][f"hog{nh}"] = {k: round(v, 3) for k, v in med.items()}
+                res[f"g{g}"][f"hog{nh}"].update({f"{k}_overhead_pct": round(100 * (med[k] / med["alone"] - 1), 2)
+                                                  for k in ("dynamic", "static")})
+    sched = "static" if os.environ.get("VX_FMHA_STATIC") == "1" else "dynamic"  # of the NCCL rows
     print(json.dumps({"sched": sched, "views": args.views, "hog_us": args.hog_us if args.hog else None,
                       "hog_first_us": args.hog_first, **res}))
     dist.destroy_process_group()
