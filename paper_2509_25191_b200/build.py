@@ -100,6 +100,8 @@ def build_diag(out: Path = ROOT / "exp" / "libvx_diag.so", defines=("VX_DIAG",))
     r = subprocess.run([NVCC, *ARCH, "-shared", "-o", str(out), *map(str, objs)], capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc link failed:\n{r.stderr[-4000:]}")
+    for o in objs:
+        o.unlink()
     return out
 
 

@@ -365,11 +365,13 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
             const uint32_t nks = smem_u32(sK + nst * Cfg::KV_TILE_BYTES);
             mbar_wait(&v_full[st], ph);
             if (has_next) mbar_wait(&k_full[nst], nph);
-            if (j == 0)
-              for (int i = 0; i < NT; ++i) mbar_wait(&o_empty[i], (n & 1) ^ 1);
             for (int i = 0; i < NT; ++i) {
               if (NOHINT) mbar_wait_nohint(&p_full[i], pfull_ph);
               else mbar_wait(&p_full[i], pfull_ph);
+              // tile i's previous-unit epilogue has read O_i (per tile, so a unit boundary does not hold
+              // every tile back to the slowest tile's epilogue; the softmax warps arrive o_empty before
+              // this unit's first p_full, so the wait is already satisfied)
+              if (j == 0) mbar_wait(&o_empty[i], (n & 1) ^ 1);
               VX_TRACE(trace_slot_mma(int(n), j, i, 0));
               tc_fence_after();
               issue_pv(i, vs, j > 0);
