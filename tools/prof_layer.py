@@ -1,0 +1,45 @@
+"""Minimal ncu driver: one warm-up and one measured launch of a VGGT-1B layer kernel at S views.
+
+    python tools/prof_layer.py attn_global 200 | attn_frame 200 | proj 200 | fc2 200 | qkv 200
+(ncu -k regex:<kernel> -s 1 -c 1 captures the second launch.)
+"""
+import _vxdiag  # noqa: F401  (VX_LIB=<path> binds a -DVX_DIAG build)
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2509_25191_b200 import ops  # noqa: E402
+
+what, views = sys.argv[1], int(sys.argv[2])
+N, H, d, C = 1374, 16, 64, 1024
+T = views * N
+if what.startswith("attn"):
+    q, k, v = (torch.randn(H, T, d, device="cuda", dtype=torch.bfloat16) for _ in range(3))
+    o = torch.empty(T, H * d, device="cuda", dtype=torch.bfloat16)
+    nseq, L = (1, T) if what == "attn_global" else (views, N)
+    run = lambda: ops.attention(q, k, v, o, nseq, L, L)  # noqa: E731
+else:
+    K = 4 * C if what == "fc2" else C
+    Nout = 3 * C if what == "qkv" else C
+    a = torch.randn(T, K, device="cuda").to(torch.bfloat16)
+    w = (torch.randn(Nout, K, device="cuda") * 0.02).to(torch.bfloat16)
+    bias = torch.randn(Nout, device="cuda")
+    if what == "qkv":
+        from paper_2509_25191_b200.aggregator import rope_tables
+        qq, kk, vv = (torch.empty(H, T, d, device="cuda", dtype=torch.bfloat16) for _ in range(3))
+        nw = tuple(torch.rand(d, device="cuda") + 0.5 for _ in range(4))
+        rope = tuple(r.cuda() for r in rope_tables(64, 38, 100.0))
+        run = lambda: ops.gemm(a, w, ops.EPI_QKV, bias=bias, qkv=(qq, kk, vv), qk_norm=nw, rope=rope,  # noqa: E731
+                               head_dim=d, tokens_total=T, tokens_per_frame=N, patch_start=5, grid_w=37)
+    else:
+        x = torch.randn(T, C, device="cuda")
+        g = torch.rand(C, device="cuda") * 0.1
+        kept = torch.empty(T, 2 * C, device="cuda", dtype=torch.bfloat16)
+        run = lambda: ops.gemm(a, w, ops.EPI_RESID, bias=bias, resid=x, gamma=g,  # noqa: E731
+                               kept=kept[:, :C] if what == "fc2" else None)
+for _ in range(2):
+    run()
+torch.cuda.synchronize()
+print("ok")
