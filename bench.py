@@ -232,8 +232,10 @@ def main():
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record()
+    torch.cuda.nvtx.range_push("timed_steps")  # ncu --nvtx --nvtx-include "timed_steps/": steady-state launches
     for _ in range(args.steps):
         step(images_dev)
+    torch.cuda.nvtx.range_pop()
     t1.record()
     torch.cuda.synchronize()
     if world > 1:
