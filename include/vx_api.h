@@ -140,6 +140,13 @@ int vx_layernorm_gather(const void* x, int x_dtype, int64_t ldx, void* y, int y_
 int vx_patchify(const float* images, void* out, int S, int H, int W, int patch, int Kpad,
                 void* stream);
 
+/* DINOv2 ViT-L/14-reg token assembly (a2', upstream DinoVisionTransformer.prepare_tokens_with_masks as
+ * built by the VGGT aggregator) on the patch-embedded stream x fp32 [S * tpf, C] whose patch p of frame f
+ * sits at row f*tpf + 1 + nreg + p: row f*tpf = cls + pos[0]; rows 1..nreg = reg (no position);
+ * patch rows += pos[1 + p].  cls [C], reg [nreg, C], pos [1 + P, C] (already interpolated to the grid). */
+int vx_dino_tokens(float* x, const float* cls, const float* reg, const float* pos, int S, int tpf, int nreg, int C,
+                   void* stream);
+
 /* Write camera (1) and register (R) tokens into the fp32 residual stream:
  * x[f*tpf + t] = (f == 0 ? tok[0] : tok[1])[t] for t < 1+R.  tokens: fp32 [2, 1+R, C]
  * (slice_expand_and_flatten + cat, a3) */

@@ -118,13 +118,49 @@ def block(x, sd, name, num_heads, eps, pos=None, freq=100.0, qk_norm=True):
 # Aggregator (a1-a3, a11, a16)
 # --------------------------------------------------------------------------
 def patch_embed(images, sd, cfg):
-    """a1 + a2: ResNet normalisation then conv 14x14/14 (== im2col GEMM)."""
+    """a1 + a2: ResNet normalisation then conv 14x14/14 (== im2col GEMM), or (a2') the DINOv2 encoder."""
     mean = torch.tensor(RESNET_MEAN).view(1, 3, 1, 1)
     std = torch.tensor(RESNET_STD).view(1, 3, 1, 1)
     x = (images - mean) / std
+    if cfg.patch_embed == "dinov2":
+        return dinov2_patch_tokens(x, sd, cfg)
     x = F.conv2d(x, sd["aggregator.patch_embed.proj.weight"], sd["aggregator.patch_embed.proj.bias"],
                  stride=cfg.patch_size)
     return x.flatten(2).transpose(1, 2)  # (S, P, C)
+
+
+def dino_pos_embed(pos_embed, grid: int):
+    """DINOv2 interpolate_pos_encoding for square inputs (upstream dinov2 vision_transformer, as built by
+    the VGGT aggregator: bicubic, antialias, interpolate_offset 0): the stored (1, 1 + M*M, C) table
+    unchanged when M == grid, else the patch part resized to grid x grid."""
+    N = pos_embed.shape[1] - 1
+    if N == grid * grid:
+        return pos_embed
+    M = int(math.sqrt(N))
+    C = pos_embed.shape[-1]
+    pos = pos_embed.float()
+    patch = F.interpolate(pos[:, 1:].reshape(1, M, M, C).permute(0, 3, 1, 2), size=(grid, grid), mode="bicubic",
+                          antialias=True)
+    return torch.cat([pos[:, :1], patch.permute(0, 2, 3, 1).reshape(1, grid * grid, C)], dim=1)
+
+
+def dinov2_patch_tokens(x, sd, cfg):
+    """a2': DINOv2 ViT-L/14-reg forward_features -> x_norm_patchtokens (S, P, C).
+
+    conv patch embed; cls token + (interpolated) learned position embedding; 4 register tokens inserted
+    after cls (no position embedding); `dino_depth` pre-norm blocks (LayerNorm eps 1e-6, no RoPE, no
+    qk-norm, LayerScale); final LayerNorm; patch tokens only."""
+    d_ = "aggregator.patch_embed."
+    S = x.shape[0]
+    C = cfg.embed_dim
+    t = F.conv2d(x, sd[d_ + "patch_embed.proj.weight"], sd[d_ + "patch_embed.proj.bias"], stride=cfg.patch_size)
+    t = t.flatten(2).transpose(1, 2)
+    t = torch.cat([sd[d_ + "cls_token"].expand(S, 1, C), t], dim=1) + dino_pos_embed(sd[d_ + "pos_embed"], cfg.grid)
+    t = torch.cat([t[:, :1], sd[d_ + "register_tokens"].expand(S, -1, C), t[:, 1:]], dim=1)
+    for i in range(cfg.dino_depth):
+        t = block(t, sd, f"{d_}blocks.{i}", cfg.num_heads, cfg.dino_eps, None, qk_norm=False)
+    t = layer_norm(t, sd[d_ + "norm.weight"], sd[d_ + "norm.bias"], cfg.dino_eps)
+    return t[:, 1 + cfg.num_register_tokens:]
 
 
 def special_tokens(sd, cfg, S):

@@ -44,6 +44,20 @@ def rope_tables(head_dim: int, max_pos: int, freq: float):
     return ang.cos().contiguous(), ang.sin().contiguous()
 
 
+def dino_pos_table(pos_embed: torch.Tensor, grid: int) -> torch.Tensor:
+    """DINOv2 interpolate_pos_encoding for square views (upstream dinov2 as built by the VGGT aggregator:
+    bicubic, antialias, offset 0), applied once at weight load: (1, 1 + M*M, C) -> [1 + grid*grid, C]."""
+    C = pos_embed.shape[-1]
+    pos = pos_embed.float().reshape(1, -1, C)
+    N = pos.shape[1] - 1
+    if N != grid * grid:
+        M = round(N ** 0.5)
+        patch = torch.nn.functional.interpolate(pos[:, 1:].reshape(1, M, M, C).permute(0, 3, 1, 2),
+                                                size=(grid, grid), mode="bicubic", antialias=True)
+        pos = torch.cat([pos[:, :1], patch.permute(0, 2, 3, 1).reshape(1, grid * grid, C)], dim=1)
+    return pos[0]
+
+
 class DeviceWeights:
     """Device copies of the state dict: bf16 matrix weights, fp32 everything else."""
 
@@ -55,7 +69,9 @@ class DeviceWeights:
             self.t[name] = v.to(device=device, dtype=dt).contiguous()
         a = "aggregator."
         C = cfg.embed_dim
-        pw = sd[a + "patch_embed.proj.weight"].reshape(C, -1)
+        pe = a + ("patch_embed.proj." if cfg.patch_embed == "conv" else "patch_embed.patch_embed.proj.")
+        self.patch_b = self.t[pe + "bias"]
+        pw = sd[pe + "weight"].reshape(C, -1)
         pad = torch.zeros(C, cfg.patch_k_padded)
         pad[:, : cfg.patch_k] = pw
         self.patch_w = pad.to(device=device, dtype=torch.bfloat16)
@@ -63,6 +79,12 @@ class DeviceWeights:
             device=device, dtype=torch.float32).contiguous()  # (2, 1+R, C)
         cos, sin = rope_tables(cfg.head_dim, cfg.grid + 1, cfg.rope_freq)
         self.rope = (cos.to(device), sin.to(device))
+        if cfg.patch_embed == "dinov2":  # cls / registers / position table of the DINOv2 encoder (a2')
+            d_ = a + "patch_embed."
+            self.dino_cls = self.t[d_ + "cls_token"].reshape(C).contiguous()
+            self.dino_reg = self.t[d_ + "register_tokens"].reshape(-1, C).contiguous()
+            self.dino_pos = dino_pos_table(sd[d_ + "pos_embed"], cfg.grid).to(device=device,
+                                                                               dtype=torch.float32).contiguous()
 
     def __getitem__(self, k):
         return self.t[k]
@@ -111,21 +133,26 @@ GlobalAttnFn = Callable[[torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor]
 
 
 def run_block(W: DeviceWeights, name: str, ws: Workspace, S: int, frame_attn: bool,
-              kept_half: Optional[torch.Tensor], global_attn: Optional[GlobalAttnFn] = None):
-    """One pre-norm VGGT Block on the whole residual stream."""
+              kept_half: Optional[torch.Tensor], global_attn: Optional[GlobalAttnFn] = None,
+              vggt_attn: bool = True, eps: Optional[float] = None):
+    """One pre-norm Block on the whole residual stream.  vggt_attn: the
+    aggregator's attention (q/k LayerNorm + 2D RoPE); False for the DINOv2 encoder blocks (a2')."""
     cfg = W.cfg
     N = cfg.tokens_per_frame
     T = S * N
     C = cfg.embed_dim
+    eps = cfg.ln_eps if eps is None else eps
     with phase("layernorm"):
-        ops.layernorm(ws.x, W[name + ".norm1.weight"], W[name + ".norm1.bias"], cfg.ln_eps, out=ws.xn)
+        ops.layernorm(ws.x, W[name + ".norm1.weight"], W[name + ".norm1.bias"], eps, out=ws.xn)
     with phase("gemm_qkv"):
+        extra = {}
+        if vggt_attn:
+            extra = dict(qk_norm=(W[name + ".attn.q_norm.weight"], W[name + ".attn.q_norm.bias"],
+                                  W[name + ".attn.k_norm.weight"], W[name + ".attn.k_norm.bias"]),
+                         rope=W.rope, tokens_per_frame=N, patch_start=cfg.patch_start_idx, grid_w=cfg.grid,
+                         eps=cfg.ln_eps)
         ops.gemm(ws.xn, W[name + ".attn.qkv.weight"], ops.EPI_QKV, bias=W[name + ".attn.qkv.bias"],
-                 qkv=(ws.q, ws.k, ws.v),
-                 qk_norm=(W[name + ".attn.q_norm.weight"], W[name + ".attn.q_norm.bias"],
-                          W[name + ".attn.k_norm.weight"], W[name + ".attn.k_norm.bias"]),
-                 rope=W.rope, head_dim=cfg.head_dim, tokens_total=ws.q.shape[1], tokens_per_frame=N,
-                 patch_start=cfg.patch_start_idx, grid_w=cfg.grid, eps=cfg.ln_eps)
+                 qkv=(ws.q, ws.k, ws.v), head_dim=cfg.head_dim, tokens_total=ws.q.shape[1], **extra)
     if frame_attn:
         with phase("attn_frame"):
             ops.attention(ws.q, ws.k, ws.v, ws.o, nseq=S, Lq=N, Lk=N)
@@ -139,7 +166,7 @@ def run_block(W: DeviceWeights, name: str, ws: Workspace, S: int, frame_attn: bo
         ops.gemm(ws.o, W[name + ".attn.proj.weight"], ops.EPI_RESID, bias=W[name + ".attn.proj.bias"],
                  resid=ws.x, gamma=W[name + ".ls1.gamma"])
     with phase("layernorm"):
-        ops.layernorm(ws.x, W[name + ".norm2.weight"], W[name + ".norm2.bias"], cfg.ln_eps, out=ws.xn)
+        ops.layernorm(ws.x, W[name + ".norm2.weight"], W[name + ".norm2.bias"], eps, out=ws.xn)
     rows = ws.h.shape[0]
     for r0 in range(0, T, rows):
         r1 = min(T, r0 + rows)
@@ -162,10 +189,29 @@ def embed(W: DeviceWeights, images: torch.Tensor, ws: Workspace, frame0_is_first
     if not frame0_is_first:  # a shard that does not own global frame 0 uses the "other" tokens
         special = special[1:2].expand(2, -1, -1).contiguous()
     with phase("embed"):
-        ops.special_tokens(ws.x, special, S, N)
         a = ops.patchify(images, cfg.patch_size, cfg.patch_k_padded)
-        ops.gemm(a, W.patch_w, ops.EPI_PATCH, bias=W["aggregator.patch_embed.proj.bias"], resid=ws.x,
-                 tokens_per_frame=N, patch_start=cfg.patch_start_idx)
+        ops.gemm(a, W.patch_w, ops.EPI_PATCH, bias=W.patch_b, resid=ws.x, tokens_per_frame=N,
+                 patch_start=cfg.patch_start_idx)
+        del a
+        if cfg.patch_embed == "dinov2":
+            dinov2_encode(W, ws, S)
+        ops.special_tokens(ws.x, special, S, N)
+
+
+def dinov2_encode(W: DeviceWeights, ws: Workspace, S: int):
+    """a2': DINOv2 ViT-L/14-reg forward_features on the patch-embedded stream, in place.
+
+    The encoder's tokens (cls + 4 registers + patches) have the aggregator's per-frame layout, so it runs
+    in the aggregator's own residual stream: token assembly (cls + pos, registers, patches + pos), the
+    `dino_depth` pre-norm blocks as frame-attention blocks without qk-norm / RoPE (LayerNorm eps 1e-6),
+    then the final LayerNorm in place; the caller overwrites rows 0..4 of every frame with the
+    aggregator's camera / register tokens, leaving x_norm_patchtokens as the patch rows."""
+    cfg = W.cfg
+    d_ = "aggregator.patch_embed."
+    ops.dino_tokens(ws.x, W.dino_cls, W.dino_reg, W.dino_pos, S, cfg.tokens_per_frame)
+    for i in range(cfg.dino_depth):
+        run_block(W, f"{d_}blocks.{i}", ws, S, True, None, vggt_attn=False, eps=cfg.dino_eps)
+    ops.layernorm(ws.x, W[d_ + "norm.weight"], W[d_ + "norm.bias"], cfg.dino_eps, out=ws.x)
 
 
 def aggregator_forward(W: DeviceWeights, images: torch.Tensor, ws: Optional[Workspace] = None,

@@ -36,6 +36,13 @@ class VGGTConfig:
     dpt_features: int = 256
     dpt_out_channels: tuple = (256, 512, 1024, 1024)
     dpt_head_features_2: int = 32
+    # patch embedding (SURVEY.md §8a a2 / a2'): "conv" = Conv2d 14x14/14 as an im2col GEMM (the north
+    # star's "patch-embed as a GEMM"); "dinov2" = the DINOv2 ViT-L/14-reg `forward_features` upstream
+    # VGGT-1B checkpoints carry (aggregator.patch_embed.*), x_norm_patchtokens as the patch tokens
+    patch_embed: str = "conv"
+    dino_depth: int = 24
+    dino_init_values: float = 1.0     # LayerScale of the DINOv2 blocks (init_values=1.0 upstream)
+    dino_eps: float = 1e-6            # DINOv2 LayerNorm eps
     # memory discipline (VGGT-X "VGGT--")
     frame_chunk: int = 128             # frames per chunk for frame-wise MLP work
     head_chunk: int = 16               # frames per DPT-head chunk (16: -9% head time vs 8 for +4 GB, tools/exp_dpt_chunk.py)
@@ -47,6 +54,10 @@ class VGGTConfig:
                 raise ValueError(f"DPT channel counts must be multiples of 64 (got {c})")
         if self.dpt_head_features_2 != 32:
             raise ValueError("dpt_head_features_2 must be 32 (fused output head)")
+        if self.patch_embed not in ("conv", "dinov2"):
+            raise ValueError(f"patch_embed must be 'conv' or 'dinov2' (got {self.patch_embed!r})")
+        if self.patch_embed == "dinov2" and self.num_register_tokens != 4:
+            raise ValueError("the DINOv2-reg patch embedding has 4 register tokens (cls + 4 + patches = tokens_per_frame)")
 
     @property
     def grid(self) -> int:

@@ -155,7 +155,43 @@ __global__ void special_tokens_kernel(float* __restrict__ x, const float* __rest
   }
 }
 
+// DINOv2 token assembly over the patch-embedded residual stream x [S * tpf, C] fp32 (patch p of frame
+// f at row f*tpf + 1 + nreg + p): row f*tpf = cls + pos[0], rows 1..nreg = registers, patch rows += pos[1 + p].
+// float4 per thread; C % 4 == 0.
+__global__ void dino_tokens_kernel(float* __restrict__ x, const float* __restrict__ cls, const float* __restrict__ reg,
+                                   const float* __restrict__ pos, int S, int tpf, int nreg, int C) {
+  const int C4 = C / 4;
+  const int64_t total = (int64_t)S * tpf * C4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int c4 = int(i % C4);
+    const int t = int((i / C4) % tpf);
+    float4* xp = reinterpret_cast<float4*>(x) + i;
+    if (t == 0) {
+      const float4 a = reinterpret_cast<const float4*>(cls)[c4], b = reinterpret_cast<const float4*>(pos)[c4];
+      *xp = make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+    } else if (t <= nreg) {
+      *xp = reinterpret_cast<const float4*>(reg)[(int64_t)(t - 1) * C4 + c4];
+    } else {
+      const float4 b = reinterpret_cast<const float4*>(pos)[(int64_t)(t - nreg) * C4 + c4];
+      float4 v = *xp;
+      *xp = make_float4(v.x + b.x, v.y + b.y, v.z + b.z, v.w + b.w);
+    }
+  }
+}
+
 }  // namespace vx
+
+extern "C" int vx_dino_tokens(float* x, const float* cls, const float* reg, const float* pos, int S, int tpf,
+                              int nreg, int C, void* stream) {
+  using namespace vx;
+  VX_CHECK_ARG(x && cls && pos && (nreg == 0 || reg) && S > 0 && tpf > 1 + nreg && C % 4 == 0,
+               "vx_dino_tokens: bad args");
+  const int64_t total = (int64_t)S * tpf * (C / 4);
+  const int grid = int((total + 255) / 256 < 148 * 16 ? (total + 255) / 256 : 148 * 16);
+  dino_tokens_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(x, cls, reg, pos, S, tpf, nreg, C);
+  VX_CHECK_LAUNCH("dino tokens launch");
+  return VX_OK;
+}
 
 extern "C" int vx_layernorm_gather(const void* x, int x_dtype, int64_t ldx, void* y, int y_dtype, int64_t ldy,
                                    const float* w, const float* b, int rows, int cols, float eps, int group_rows,

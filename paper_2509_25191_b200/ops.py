@@ -59,7 +59,7 @@ class GaProblem(ctypes.Structure):
 
 
 EXPORTED_SYMBOLS = ("vx_gemm", "vx_attention", "vx_attention_merge", "vx_layernorm", "vx_layernorm_gather", "vx_patchify",
-                    "vx_special_tokens", "vx_linear_f32", "vx_adaln_modulate",
+                    "vx_special_tokens", "vx_dino_tokens", "vx_linear_f32", "vx_adaln_modulate",
                     "vx_upsample_bilinear", "vx_gemm_spatial", "vx_epipolar_residuals",
                     "vx_epipolar_accumulate", "vx_ga_decode", "vx_ga_residuals", "vx_ga_loss_grad",
                     "vx_ga_adam", "vx_ga_adaptive_weights", "vx_matched_points", "vx_unproject_depth",
@@ -89,6 +89,7 @@ def load_library(path: os.PathLike | None = None) -> ctypes.CDLL:
     lib.vx_linear_f32.argtypes = [_i32, _vp, _i64, _vp, _i64, _vp, _i32, _i32, _i32, _vp, _i64, _vp, _vp, _vp]
     lib.vx_adaln_modulate.argtypes = [_vp, _vp, _vp, _i32, _i32, _f32, _vp]
     lib.vx_special_tokens.argtypes = [_vp, _vp, _i32, _i32, _i32, _i32, _vp]
+    lib.vx_dino_tokens.argtypes = [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp]
     lib.vx_upsample_bilinear.argtypes = [_vp, _i32, _i32, _i32, _i32, _vp, _i32, _i32, _vp, _i32, _vp]
     lib.vx_gemm_spatial.argtypes = [_vp, _vp, _i32, _i32, _vp, ctypes.POINTER(Spatial), _vp]
     lib.vx_epipolar_residuals.argtypes = [_vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp]
@@ -360,6 +361,22 @@ def adaln_modulate(tok, mod, eps: float, out=None):
         out = torch.empty_like(tok)
     _check(_lib.vx_adaln_modulate(_ptr(tok), _ptr(mod), _ptr(out), S, D, eps, _stream()), "vx_adaln_modulate")
     return out
+
+
+def dino_tokens(x, cls, reg, pos, S: int, tpf: int):
+    """DINOv2 cls / register tokens and position embedding on the patch-embedded stream x [S*tpf, C] fp32."""
+    load_library()
+    for t, nm in ((x, "x"), (cls, "cls"), (reg, "reg"), (pos, "pos")):
+        _req(t, torch.float32, nm)
+        if not t.is_contiguous():
+            raise ValueError(f"dino_tokens: {nm} must be contiguous")
+    C = x.shape[-1]
+    nreg = reg.numel() // C
+    if pos.numel() != (tpf - nreg) * C:
+        raise ValueError("dino_tokens: pos must be [1 + patches, C]")
+    _check(_lib.vx_dino_tokens(_ptr(x), _ptr(cls), _ptr(reg), _ptr(pos), S, tpf, nreg, C, _stream()),
+           "vx_dino_tokens")
+    return x
 
 
 def upsample_bilinear(x: torch.Tensor, size, add=None, out=None, out_pad: bool = False):

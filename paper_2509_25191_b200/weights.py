@@ -56,8 +56,35 @@ def param_shapes(cfg: VGGTConfig) -> "OrderedDict[str, tuple]":
     P = cfg.patch_size
     s = OrderedDict()
     a = "aggregator."
-    s[a + "patch_embed.proj.weight"] = (C, 3, P, P)
-    s[a + "patch_embed.proj.bias"] = (C,)
+    if cfg.patch_embed == "conv":
+        s[a + "patch_embed.proj.weight"] = (C, 3, P, P)
+        s[a + "patch_embed.proj.bias"] = (C,)
+    else:  # DINOv2 ViT-L/14-reg (upstream vit_large as built by the VGGT aggregator)
+        d_ = a + "patch_embed."
+        s[d_ + "cls_token"] = (1, 1, C)
+        s[d_ + "pos_embed"] = (1, 1 + cfg.num_patches, C)
+        s[d_ + "register_tokens"] = (1, cfg.num_register_tokens, C)
+        s[d_ + "mask_token"] = (1, C)
+        s[d_ + "patch_embed.proj.weight"] = (C, 3, P, P)
+        s[d_ + "patch_embed.proj.bias"] = (C,)
+        for i in range(cfg.dino_depth):
+            b = f"{d_}blocks.{i}."
+            s[b + "norm1.weight"] = (C,)
+            s[b + "norm1.bias"] = (C,)
+            s[b + "attn.qkv.weight"] = (3 * C, C)
+            s[b + "attn.qkv.bias"] = (3 * C,)
+            s[b + "attn.proj.weight"] = (C, C)
+            s[b + "attn.proj.bias"] = (C,)
+            s[b + "ls1.gamma"] = (C,)
+            s[b + "norm2.weight"] = (C,)
+            s[b + "norm2.bias"] = (C,)
+            s[b + "mlp.fc1.weight"] = (hid, C)
+            s[b + "mlp.fc1.bias"] = (hid,)
+            s[b + "mlp.fc2.weight"] = (C, hid)
+            s[b + "mlp.fc2.bias"] = (C,)
+            s[b + "ls2.gamma"] = (C,)
+        s[d_ + "norm.weight"] = (C,)
+        s[d_ + "norm.bias"] = (C,)
     s[a + "camera_token"] = (1, 2, 1, C)
     s[a + "register_token"] = (1, 2, cfg.num_register_tokens, C)
     for kind in ("frame_blocks", "global_blocks"):
@@ -153,10 +180,14 @@ def _init_one(name: str, shape: tuple, cfg: VGGTConfig, seed: int) -> torch.Tens
     nd = len(shape)
     if name.endswith("camera_token") or name.endswith("register_token"):
         return _normal(shape, 0.5, seed, name, trunc=False)
+    if name.endswith(("patch_embed.cls_token", "patch_embed.pos_embed", "patch_embed.register_tokens",
+                      "patch_embed.mask_token")):
+        return _normal(shape, 0.02, seed, name)
     if name == "camera_head.empty_pose_tokens":
         return torch.zeros(shape)  # upstream init; a trained checkpoint carries its own values
     if name.endswith(".gamma"):
-        base = cfg.cam_init_values if name.startswith("camera_head.") else cfg.init_values
+        base = (cfg.cam_init_values if name.startswith("camera_head.") else
+                cfg.dino_init_values if name.startswith("aggregator.patch_embed.") else cfg.init_values)
         return _normal(shape, 0.1 * base, seed, name, mean=base)
     if name == "camera_head.pose_branch.fc2.weight":
         return _normal(shape, 0.002, seed, name)
@@ -198,7 +229,14 @@ def check_state_dict(sd, cfg: VGGTConfig) -> None:
     missing = [k for k in param_shapes(cfg) if k not in sd]
     if missing:
         raise KeyError(f"state_dict lacks {len(missing)} parameter(s) of the VGGT path, e.g. {missing[:4]}")
-    bad = [(k, tuple(sd[k].shape), s) for k, s in param_shapes(cfg).items() if tuple(sd[k].shape) != tuple(s)]
+    def ok(k, want):
+        got = tuple(sd[k].shape)
+        if k.endswith("patch_embed.pos_embed") and len(got) == 3:  # any square grid (interpolated at load)
+            m = round((got[1] - 1) ** 0.5)
+            return got[0] == 1 and m * m == got[1] - 1 and got[2] == want[2]
+        return got == tuple(want)
+
+    bad = [(k, tuple(sd[k].shape), s) for k, s in param_shapes(cfg).items() if not ok(k, s)]
     if bad:
         raise ValueError(f"state_dict shape mismatch: {bad[:4]}")
 
