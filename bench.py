@@ -186,6 +186,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-heads", action="store_true", help="aggregator only (diagnostic)")
+    ap.add_argument("--patch-embed", default="conv", choices=["conv", "dinov2"],
+                    help="conv (the north star's patch-embed GEMM, default) or the DINOv2 encoder of released checkpoints")
     args = ap.parse_args()
     self_launch(args)
     if "WORLD_SIZE" in os.environ and int(os.environ["WORLD_SIZE"]) != args.gpus:
@@ -204,7 +206,7 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    cfg = vggt_1b()
+    cfg = vggt_1b().with_(patch_embed=args.patch_embed)
     S = args.views
     sd = make_state_dict(cfg, 0)
     model = VGGT(cfg, state_dict=sd, dist=world > 1)
@@ -335,7 +337,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (torch.rand views seed 1, random-init weights seed 0)",
-            "config": {"workload": f"vggt1b_518_S{S}" + ("_aggregator_only" if args.no_heads else ""),
+            "config": {"workload": f"vggt1b_518_S{S}" + ("_dinov2" if args.patch_embed == "dinov2" else "")
+                       + ("_aggregator_only" if args.no_heads else ""),
                        "views": S, "img": 518, "tokens_per_view": N, "model": "VGGT-1B-shaped (24x2 blocks, C=1024)",
                        "parallelism": "frame-sharded ring" if world > 1 else "single GPU",
                        "l2": "inputs larger than L2 (views 644 MB fp32 at S=200, weights 1.8 GB bf16)"},

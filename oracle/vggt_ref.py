@@ -420,6 +420,8 @@ def forward_flops(cfg: VGGTConfig, S: int, with_heads: bool = True) -> float:
     attn_glob = 4 * S * N * N * C                          # per view
     patch = 2 * cfg.num_patches * cfg.patch_k * C
     f = S * (L * (2 * lin + attn_frame + attn_glob) + patch)
+    if cfg.patch_embed == "dinov2":  # DINOv2 encoder blocks: frame-attention blocks (+1.01 TF/view)
+        f += S * cfg.dino_depth * (lin + attn_frame)
     if with_heads:
         f += 2 * S * dpt_flops(cfg)
     return float(f)
