@@ -341,7 +341,8 @@ def main():
                        + ("_aggregator_only" if args.no_heads else ""),
                        "views": S, "img": 518, "tokens_per_view": N, "model": "VGGT-1B-shaped (24x2 blocks, C=1024)",
                        "parallelism": "frame-sharded ring" if world > 1 else "single GPU",
-                       "l2": "inputs larger than L2 (views 644 MB fp32 at S=200, weights 1.8 GB bf16)"},
+                       "l2": f"inputs larger than L2 (views {S * 3 * 518 * 518 * 4 / 1e6:.0f} MB fp32, weights "
+                             f"1.8 GB bf16, both read every step; L2 126 MB)"},
             "peak_hbm_gb_per_gpu": peak_hbm,
             "model_tflops_per_gpu": model_tflops,
             "model_frac_of_peak": model_tflops / peaks["bf16_tflops_sustained"],

@@ -30,16 +30,20 @@ struct GemmArgs {
 
 constexpr int VX_EPI_SPATIAL = 6;
 constexpr int VX_EPI_HEADOUT = 7;
+// VX_EPI_RESID without the kept copy on 256-wide tiles (Attention.proj): the fp32 residual tile moves
+// through shared memory with TMA loads / stores instead of per-lane global loads and stores
+constexpr int VX_EPI_RESID_TMA = 8;
 
 constexpr int GEMM_BM = 128;
 constexpr int GEMM_BK = 64;
 constexpr int GEMM_THREADS = 384;  // w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4..w11 epilogue
 constexpr int GEMM_EPI_WARPS = 8;  // two warps per TMEM lane quarter, each owning half of the tile columns
 
-template <int BN, bool CG2 = false>
+template <int BN, bool CG2 = false, bool RT = false>
 struct GemmCfg {
-  // CG2 (CTA pair, cta_group::2): each CTA stages its 128 A rows and half of the B tile
-  static constexpr int STAGES = CG2 ? 6 : (BN == 256 ? 4 : (BN == 128 ? 6 : 8));
+  // CG2 (CTA pair, cta_group::2): each CTA stages its 128 A rows and half of the B tile; RT (TMA
+  // residual epilogue): 4 stages, leaving 64 KB for the residual boxes
+  static constexpr int STAGES = RT ? 4 : (CG2 ? 6 : (BN == 256 ? 4 : (BN == 128 ? 6 : 8)));
   static constexpr uint32_t A_BYTES = GEMM_BM * GEMM_BK * 2;
   static constexpr uint32_t B_BYTES = (CG2 ? BN / 2 : BN) * GEMM_BK * 2;
   static constexpr uint32_t RING = STAGES * (A_BYTES + B_BYTES);
@@ -53,9 +57,13 @@ struct GemmCfg {
 // write walks row segments with the 32 lanes on consecutive columns (one 128 B sector run per
 // row) instead of 32 rows per instruction (32 half-used sectors)
 constexpr uint32_t RESID_TILE_FLOATS = 32 * 33;
+// RESID_TMA: per epilogue warp two 32 x 32 fp32 residual boxes (4 KB each, 128-byte swizzled rows),
+// 1024-byte aligned after the barrier block
+constexpr uint32_t RT_BOX_BYTES = 32 * 32 * 4;
 template <int EPI>
 constexpr uint32_t epi_smem_bytes() {
-  return EPI == VX_EPI_RESID ? GEMM_EPI_WARPS * RESID_TILE_FLOATS * 4 : 0;
+  return EPI == VX_EPI_RESID ? GEMM_EPI_WARPS * RESID_TILE_FLOATS * 4
+                             : (EPI == VX_EPI_RESID_TMA ? 1024 + GEMM_EPI_WARPS * 2 * RT_BOX_BYTES : 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -379,8 +387,8 @@ VX_DEVICE void epi_headout(const GemmArgs& a, const PixInfo& pi, const uint32_t*
 template <int BN, int EPI, int HD, bool MC, bool CG2 = false>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                const GemmArgs args) {
-  using Cfg = GemmCfg<BN, CG2>;
+                const __grid_constant__ CUtensorMap tmR, const GemmArgs args) {
+  using Cfg = GemmCfg<BN, CG2, EPI == VX_EPI_RESID_TMA>;
   constexpr bool PAIRED = MC || CG2;
   constexpr int STAGES = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -395,6 +403,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   // offset from smem_raw (not the integer-aligned pointer) so the compiler keeps the shared state
   // space and emits LDS / STS for the transpose tile rather than generic LD / ST
   [[maybe_unused]] float* epi_buf = reinterpret_cast<float*>(smem_raw + (smem - smem_raw) + Cfg::RING + 256);
+  // RESID_TMA: per-warp residual boxes and their TMA-load barriers
+  [[maybe_unused]] float* rbox = reinterpret_cast<float*>(smem_raw + (smem - smem_raw) + Cfg::RING + 1024);
+  [[maybe_unused]] uint64_t* rbar = reinterpret_cast<uint64_t*>(smem + Cfg::RING + 128);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -425,6 +436,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       // CG2: the leader's accumulator is released by both CTAs' epilogue warps
       mbar_init(&tempty[s], CG2 ? 2 * GEMM_EPI_WARPS : GEMM_EPI_WARPS);
     }
+    if constexpr (EPI == VX_EPI_RESID_TMA)
+      for (int i = 0; i < 2 * GEMM_EPI_WARPS; ++i) mbar_init(&rbar[i], 1);
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -513,6 +526,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       }
     }
   } else if (warp >= 4) {
+    [[maybe_unused]] uint32_t rph = 0;    // RESID_TMA: phase bit per residual box
     const int ew = (warp - 4) & 3;        // TMEM lane quarter
     // column half (a 32-wide tile is handled whole by warps 4..7; warps 8..11 only arrive)
     const int c_beg = BN <= 32 ? ((warp - 4) >> 2) * BN : ((warp - 4) >> 2) * (BN / 2);
@@ -534,6 +548,22 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       };
       if constexpr (EPI == VX_EPI_RESID) {
         if (n_blk * BN + c_beg < N) load_resid(n_blk * BN + c_beg);
+      }
+      // RESID_TMA: the warp's first two 32 x 32 residual boxes are requested before the accumulator
+      // wait (their load overlaps the tile's main loop); later boxes reuse a buffer once its store has
+      // read it
+      [[maybe_unused]] const int wcol0 = n_blk * BN + c_beg;
+      [[maybe_unused]] const int nbox = wcol0 < N ? ((N - wcol0 < c_end - c_beg ? N - wcol0 : c_end - c_beg) / 32) : 0;
+      [[maybe_unused]] float* wbox = rbox + (warp - 4) * 2 * (RT_BOX_BYTES / 4);
+      [[maybe_unused]] uint64_t* wbar = rbar + (warp - 4) * 2;
+      if constexpr (EPI == VX_EPI_RESID_TMA) {
+        if (lane == 0) {
+          bulk_wait_read<0>();  // the previous tile's stores have read both boxes
+          for (int b = 0; b < 2 && b < nbox; ++b) {
+            mbar_expect_tx(&wbar[b], RT_BOX_BYTES);
+            tma_load_2d(wbox + b * (RT_BOX_BYTES / 4), &tmR, &wbar[b], wcol0 + 32 * b, rrow0);
+          }
+        }
       }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
@@ -576,6 +606,45 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           tmem_wait_ld();
           if constexpr (EPI == VX_EPI_SPATIAL) epi_spatial32(args, pi, col, r);
           else epi_headout(args, pi, r);
+        }
+      } else if constexpr (EPI == VX_EPI_RESID_TMA) {
+        const vx_epilogue& e = args.ep;
+#pragma unroll 1
+        for (int cb = 0; cb < nbox; ++cb) {
+          const int b = cb & 1;
+          float* box = wbox + b * (RT_BOX_BYTES / 4);
+          const int col = wcol0 + 32 * cb;
+          uint32_t r[32];
+          tmem_ld32(taddr + c_beg + 32 * cb, r);
+          mbar_wait(&wbar[b], (rph >> b) & 1);
+          rph ^= 1u << b;
+          tmem_wait_ld();
+          // this thread's row of the box: 8 float4 at 128-byte-swizzled positions (conflict-free)
+          float* rowp = box + lane * 32;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            float4* p4 = reinterpret_cast<float4*>(rowp + ((j ^ (lane & 7)) * 4));
+            const float4 x = *p4;
+            const float4 g = __ldg(reinterpret_cast<const float4*>(e.gamma + col) + j);
+            const float4 bb = e.bias ? __ldg(reinterpret_cast<const float4*>(e.bias + col) + j)
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+            *p4 = make_float4(x.x + g.x * (__uint_as_float(r[4 * j + 0]) + bb.x),
+                              x.y + g.y * (__uint_as_float(r[4 * j + 1]) + bb.y),
+                              x.z + g.z * (__uint_as_float(r[4 * j + 2]) + bb.z),
+                              x.w + g.w * (__uint_as_float(r[4 * j + 3]) + bb.w));
+          }
+          fence_proxy_async_smem();  // generic-proxy writes visible to the TMA store
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmR, box, col, rrow0);  // rows >= M are clipped by the tensor map
+            bulk_commit();
+            if (cb + 2 < nbox) {  // refill this buffer with box cb + 2 once the store has read it
+              bulk_wait_read<0>();
+              mbar_expect_tx(&wbar[b], RT_BOX_BYTES);
+              tma_load_2d(box, &tmR, &wbar[b], col + 64, rrow0);
+            }
+          }
+          __syncwarp();
         }
       } else if constexpr (EPI == VX_EPI_RESID) {
         float* tb = epi_buf + (warp - 4) * RESID_TILE_FLOATS;
@@ -632,6 +701,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   }
+  if constexpr (EPI == VX_EPI_RESID_TMA) {
+    if (warp >= 4 && lane_id() == 0) bulk_wait<0>();  // residual stores complete before the CTA exits
+  }
   tc_fence_before();
   __syncthreads();
   if constexpr (PAIRED) cluster_sync();  // no CTA leaves while its peer may still multicast / arrive
@@ -643,8 +715,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 }
 
 template <int BN, int EPI, int HD, bool MC = false, bool CG2 = false>
-static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& args, cudaStream_t st) {
-  using Cfg = GemmCfg<BN, CG2>;
+static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& args, cudaStream_t st,
+                       const CUtensorMap* tr = nullptr) {
+  using Cfg = GemmCfg<BN, CG2, EPI == VX_EPI_RESID_TMA>;
+  static const CUtensorMap no_map{};
+  const CUtensorMap& trr = tr ? *tr : no_map;
   constexpr uint32_t SMEM = Cfg::SMEM + epi_smem_bytes<EPI>();
   static_assert(SMEM <= 227 * 1024, "GEMM stage ring + epilogue buffer exceed the 227 KB smem per CTA");
   auto kern = gemm_kernel<BN, EPI, HD, MC, CG2>;
@@ -670,12 +745,12 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmA
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, args);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, trr, args);
     if (e != cudaSuccess) return fail_cuda(e, "gemm cluster launch");
   } else {
     const int tiles = num_m * num_n;
     const int grid = tiles < num_sms() ? tiles : num_sms();
-    kern<<<grid, GEMM_THREADS, SMEM, st>>>(ta, tb, args);
+    kern<<<grid, GEMM_THREADS, SMEM, st>>>(ta, tb, trr, args);
   }
   VX_CHECK_LAUNCH("gemm launch");
   return VX_OK;
@@ -760,6 +835,12 @@ extern "C" int vx_gemm(int epi, const void* A, int64_t lda, const void* B, int64
       case VX_EPI_QKV: return launch_gemm<64, VX_EPI_QKV, 0>(ta, tb, args, st);
       default: break;
     }
+  }
+  if (epi == VX_EPI_RESID && !ep->kept && pm == 2 && (reinterpret_cast<uintptr_t>(ep->resid) & 15) == 0 &&
+      ep->ldr % 4 == 0) {  // proj on CTA pairs: residual tile through TMA boxes (VX_EPI_RESID_TMA)
+    CUtensorMap tr;
+    if (!make_tmap_2d(&tr, ep->resid, true, M, N, ep->ldr, 32, 32, 128)) return VX_E_ARG;
+    return launch_gemm<256, VX_EPI_RESID_TMA, 0, false, true>(ta, tb, args, st, &tr);
   }
   if (pm == 2) return dispatch_epi<256, false, true>(epi, ta, tb, args, st);
 #ifdef VX_DIAG

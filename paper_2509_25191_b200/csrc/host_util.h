@@ -19,6 +19,9 @@ void count_launches(uint64_t n);
 // swizzle_bytes in {0, 32, 64, 128}.
 bool make_tmap_2d_bf16(CUtensorMap* m, const void* ptr, uint64_t rows, uint64_t cols, uint64_t ld,
                        uint32_t box_rows, uint32_t box_cols, int swizzle_bytes);
+// same for bf16 (f32 = false) or fp32 (f32 = true) elements
+bool make_tmap_2d(CUtensorMap* m, const void* ptr, bool f32, uint64_t rows, uint64_t cols, uint64_t ld,
+                  uint32_t box_rows, uint32_t box_cols, int swizzle_bytes);
 
 }  // namespace vx
 
