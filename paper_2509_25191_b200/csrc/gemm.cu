@@ -34,6 +34,9 @@ constexpr int VX_EPI_HEADOUT = 7;
 // through shared memory with TMA loads / stores instead of per-lane global loads and stores
 constexpr int VX_EPI_RESID_TMA = 8;
 
+#ifndef VX_RT_NBOX
+#define VX_RT_NBOX 2
+#endif
 constexpr int GEMM_BM = 128;
 constexpr int GEMM_BK = 64;
 constexpr int GEMM_THREADS = 384;  // w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4..w11 epilogue
@@ -43,7 +46,7 @@ template <int BN, bool CG2 = false, bool RT = false>
 struct GemmCfg {
   // CG2 (CTA pair, cta_group::2): each CTA stages its 128 A rows and half of the B tile; RT (TMA
   // residual epilogue): 4 stages, leaving 64 KB for the residual boxes
-  static constexpr int STAGES = RT ? 4 : (CG2 ? 6 : (BN == 256 ? 4 : (BN == 128 ? 6 : 8)));
+  static constexpr int STAGES = RT ? (VX_RT_NBOX >= 4 ? 3 : 4) : (CG2 ? 6 : (BN == 256 ? 4 : (BN == 128 ? 6 : 8)));
   static constexpr uint32_t A_BYTES = GEMM_BM * GEMM_BK * 2;
   static constexpr uint32_t B_BYTES = (CG2 ? BN / 2 : BN) * GEMM_BK * 2;
   static constexpr uint32_t RING = STAGES * (A_BYTES + B_BYTES);
@@ -60,10 +63,11 @@ constexpr uint32_t RESID_TILE_FLOATS = 32 * 33;
 // RESID_TMA: per epilogue warp two 32 x 32 fp32 residual boxes (4 KB each, 128-byte swizzled rows),
 // 1024-byte aligned after the barrier block
 constexpr uint32_t RT_BOX_BYTES = 32 * 32 * 4;
+constexpr int RT_NBOX = VX_RT_NBOX;  // boxes per epilogue warp (4: the warp's whole 32 x 128 tile share)
 template <int EPI>
 constexpr uint32_t epi_smem_bytes() {
   return EPI == VX_EPI_RESID ? GEMM_EPI_WARPS * RESID_TILE_FLOATS * 4
-                             : (EPI == VX_EPI_RESID_TMA ? 1024 + GEMM_EPI_WARPS * 2 * RT_BOX_BYTES : 0);
+                             : (EPI == VX_EPI_RESID_TMA ? 1024 + GEMM_EPI_WARPS * RT_NBOX * RT_BOX_BYTES : 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -437,7 +441,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       mbar_init(&tempty[s], CG2 ? 2 * GEMM_EPI_WARPS : GEMM_EPI_WARPS);
     }
     if constexpr (EPI == VX_EPI_RESID_TMA)
-      for (int i = 0; i < 2 * GEMM_EPI_WARPS; ++i) mbar_init(&rbar[i], 1);
+      for (int i = 0; i < RT_NBOX * GEMM_EPI_WARPS; ++i) mbar_init(&rbar[i], 1);
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -554,12 +558,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       // read it
       [[maybe_unused]] const int wcol0 = n_blk * BN + c_beg;
       [[maybe_unused]] const int nbox = wcol0 < N ? ((N - wcol0 < c_end - c_beg ? N - wcol0 : c_end - c_beg) / 32) : 0;
-      [[maybe_unused]] float* wbox = rbox + (warp - 4) * 2 * (RT_BOX_BYTES / 4);
-      [[maybe_unused]] uint64_t* wbar = rbar + (warp - 4) * 2;
+      [[maybe_unused]] float* wbox = rbox + (warp - 4) * RT_NBOX * (RT_BOX_BYTES / 4);
+      [[maybe_unused]] uint64_t* wbar = rbar + (warp - 4) * RT_NBOX;
       if constexpr (EPI == VX_EPI_RESID_TMA) {
         if (lane == 0) {
-          bulk_wait_read<0>();  // the previous tile's stores have read both boxes
-          for (int b = 0; b < 2 && b < nbox; ++b) {
+          bulk_wait_read<0>();  // the previous tile's stores have read the boxes
+          for (int b = 0; b < RT_NBOX && b < nbox; ++b) {
             mbar_expect_tx(&wbar[b], RT_BOX_BYTES);
             tma_load_2d(wbox + b * (RT_BOX_BYTES / 4), &tmR, &wbar[b], wcol0 + 32 * b, rrow0);
           }
@@ -611,7 +615,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const vx_epilogue& e = args.ep;
 #pragma unroll 1
         for (int cb = 0; cb < nbox; ++cb) {
-          const int b = cb & 1;
+          const int b = cb % RT_NBOX;
           float* box = wbox + b * (RT_BOX_BYTES / 4);
           const int col = wcol0 + 32 * cb;
           uint32_t r[32];
@@ -638,10 +642,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           if (lane == 0) {
             tma_store_2d(&tmR, box, col, rrow0);  // rows >= M are clipped by the tensor map
             bulk_commit();
-            if (cb + 2 < nbox) {  // refill this buffer with box cb + 2 once the store has read it
+            if (cb + RT_NBOX < nbox) {  // refill this buffer with box cb + NBOX once the store has read it
               bulk_wait_read<0>();
               mbar_expect_tx(&wbar[b], RT_BOX_BYTES);
-              tma_load_2d(box, &tmR, &wbar[b], col + 64, rrow0);
+              tma_load_2d(box, &tmR, &wbar[b], col + 32 * RT_NBOX, rrow0);
             }
           }
           __syncwarp();
