@@ -1,7 +1,7 @@
 """Drop-in `VGGT` inference module (SURVEY.md §8b "Python API to keep").
 
     model = VGGT(cfg)                 # seeded random-init weights (no checkpoints on disk)
-    preds = model(images)             # images (S,3,H,W) or (1,S,3,H,W) in [0, 1]
+    preds = model(images)             # images (S,3,H,W) or (B,S,3,H,W) in [0, 1] (B scenes run in turn)
     preds["pose_enc"]                 # (1, S, 9) fp32  [T(3), quat XYZW(4), fov_h, fov_w]
     preds["depth"], ["depth_conf"]    # (1, S, H, W, 1), (1, S, H, W) fp32
     preds["world_points"], [..._conf] # (1, S, H, W, 3), (1, S, H, W) fp32
@@ -70,7 +70,7 @@ class VGGT:
         moves only its own views over PCIe."""
         if images.dim() == 5:
             if images.shape[0] != 1:
-                raise ValueError("batch size B must be 1 (frames are the batch dimension)")
+                raise ValueError("one scene per call here (forward / aggregator loop over B)")
             images = images[0]
         if images.dim() != 4 or images.shape[1] != 3:
             raise ValueError(f"images must be (S,3,H,W) or (1,S,3,H,W); got {tuple(images.shape)}")
@@ -81,8 +81,17 @@ class VGGT:
         return local.to(self.device, torch.float32, non_blocking=True).contiguous(), f0, S
 
     # -- API ------------------------------------------------------------------
+    @staticmethod
+    def _scenes(images: torch.Tensor):
+        """(B, S, 3, H, W) with B > 1: the upstream batch of independent scenes, run one after another."""
+        return [images[b:b + 1] for b in range(images.shape[0])] if images.dim() == 5 and images.shape[0] > 1 else None
+
     @torch.no_grad()
     def aggregator(self, images: torch.Tensor, sharded_input: bool = False) -> Tuple[Dict[int, torch.Tensor], int]:
+        scenes = self._scenes(images)
+        if scenes is not None:
+            parts = [self.aggregator(x, sharded_input)[0] for x in scenes]
+            return {i: torch.cat([p[i] for p in parts]) for i in parts[0]}, self.cfg.patch_start_idx
         local, f0, S = self._local(images, sharded_input)
         kept = self._aggregate(local, f0)
         return {i: t[None] for i, t in kept.items()}, self.cfg.patch_start_idx
@@ -102,6 +111,14 @@ class VGGT:
 
     @torch.no_grad()
     def forward(self, images: torch.Tensor, sharded_input: bool = False) -> Dict[str, torch.Tensor]:
+        scenes = self._scenes(images)
+        if scenes is not None:  # outputs stacked along the upstream batch dimension B
+            outs = [self.forward(x, sharded_input) for x in scenes]
+            res = {k: torch.cat([o[k] for o in outs]) for k, v in outs[0].items() if isinstance(v, torch.Tensor)}
+            res["pose_enc_list"] = [torch.cat([o["pose_enc_list"][i] for o in outs])
+                                    for i in range(len(outs[0]["pose_enc_list"]))]
+            res["frame_offset"] = outs[0]["frame_offset"]
+            return res
         cfg = self.cfg
         local, f0, S = self._local(images, sharded_input)
         kept = self._aggregate(local, f0)

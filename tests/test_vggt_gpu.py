@@ -284,3 +284,19 @@ def test_vggt1b_eight_views():
     sd = make_state_dict(cfg, 0)
     images = synthetic_images(cfg, 8, 3)
     _check(cfg, sd, images, _oracle(cfg, sd, images), "1b-s8")
+
+
+def test_batch_of_scenes():
+    """(B, S, 3, H, W) with B > 1: independent scenes, outputs stacked along B like upstream VGGT."""
+    from paper_2509_25191_b200.vggt import VGGT
+    cfg = vggt_tiny()
+    m = VGGT(cfg)
+    a, b = synthetic_images(cfg, 3, 1).cuda(), synthetic_images(cfg, 3, 2).cuda()
+    out = m(torch.stack([a, b]))
+    oa, ob = m(a), m(b)
+    assert out["pose_enc"].shape == (2, 3, 9) and out["depth"].shape == (2, 3, 112, 112, 1)
+    assert len(out["pose_enc_list"]) == cfg.cam_iters and out["pose_enc_list"][0].shape == (2, 3, 9)
+    for k in ("pose_enc", "depth", "world_points_conf"):
+        assert torch.equal(out[k][0], oa[k][0]) and torch.equal(out[k][1], ob[k][0])
+    kept, _ = m.aggregator(torch.stack([a, b]))
+    assert kept[cfg.kept_layers[-1]].shape == (2, 3, cfg.tokens_per_frame, 2 * cfg.embed_dim)
