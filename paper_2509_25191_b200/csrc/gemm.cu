@@ -840,8 +840,10 @@ extern "C" int vx_gemm(int epi, const void* A, int64_t lda, const void* B, int64
       default: break;
     }
   }
-  if (epi == VX_EPI_RESID && !ep->kept && pm == 2 && (reinterpret_cast<uintptr_t>(ep->resid) & 15) == 0 &&
-      ep->ldr % 4 == 0) {  // proj on CTA pairs: residual tile through TMA boxes (VX_EPI_RESID_TMA)
+  // proj (K = C) on CTA pairs: residual tile through TMA boxes (VX_EPI_RESID_TMA). Not for fc2 (K = 4C):
+  // its main loop needs the 6-stage ring the boxes would take (measured 10-16% slower with 4 stages)
+  if (epi == VX_EPI_RESID && !ep->kept && pm == 2 && K <= 2048 && (reinterpret_cast<uintptr_t>(ep->resid) & 15) == 0 &&
+      ep->ldr % 4 == 0) {
     CUtensorMap tr;
     if (!make_tmap_2d(&tr, ep->resid, true, M, N, ep->ldr, 32, 32, 128)) return VX_E_ARG;
     return launch_gemm<256, VX_EPI_RESID_TMA, 0, false, true>(ta, tb, args, st, &tr);

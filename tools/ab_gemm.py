@@ -27,12 +27,12 @@ def main():
         M = views * 1374
         x = torch.randn(M, C, device="cuda")
         kept = torch.empty(M, 2 * C, device="cuda", dtype=torch.bfloat16)
-        for name, K in (("fc2", 4 * C), ("proj", C)):
+        for name, K in (("fc2", 4 * C), ("fc2nokept", 4 * C), ("proj", C)):
             a = torch.randn(M, K, device="cuda").to(torch.bfloat16)
             w = (torch.randn(C, K, device="cuda") * 0.02).to(torch.bfloat16)
             bias = torch.randn(C, device="cuda")
             g = torch.rand(C, device="cuda") * 0.1
-            kw = dict(bias=bias, resid=x, gamma=g, kept=kept[:, :C] if name == "fc2" else None)
+            kw = dict(bias=bias, resid=x, gamma=g, kept=kept[:, :C] if name == "fc2" else None)  # fc2nokept: layers not kept
             reps = 10 if views >= 100 else 40
             ts = [[], []]
             for r in range(args.rounds):
