@@ -17,6 +17,11 @@ SURVEY.md Appendix A, with the VGGT-X modifications the paper describes:
                    (`frame_chunk`), which must not change the result;
   * `PAPER.md:146` chunk S = 128.
 
+Partial external anchors (tests/test_oracle_anchors.py): `dinov2_patch_tokens` equals the
+`transformers` Dinov2WithRegistersModel and `_fusion` / `_rcu` equal its DPTFeatureFusionLayer on
+shared random weights; nothing pins the VGGT-specific parts (2D RoPE, q/k LayerNorm, camera head,
+DPT reassembly).
+
 Everything runs in fp32 on the CPU with the seeded weights from
 `paper_2509_25191_b200.weights` (matrix weights already bf16-representable).
 The conventions reused from the reference are the world-to-camera extrinsic
