@@ -45,23 +45,34 @@ __global__ void __launch_bounds__(256) upsample_bilinear_nhwc_kernel(
   }
   const int64_t opix = out_pad ? ((int64_t)(f * (H + 2) + y + 1) * (W + 2) + x + 1) : (((int64_t)f * H + y) * W + x);
   uint4* po = reinterpret_cast<uint4*>(out + opix * C + c8 * 8);
+  // packed fp32x2 arithmetic (FFMA2): a bf16x2 word widens with one shift / mask per half, the 4-tap
+  // sum is one FMUL2 + three FFMA2 per channel pair, in the scalar expression's order
+  const uint64_t W00 = f2_pack(w00, w00), W01 = f2_pack(w01, w01), W10 = f2_pack(w10, w10), W11 = f2_pack(w11, w11);
+  auto widen = [](uint32_t x) { return f2_pack(__uint_as_float(x << 16), __uint_as_float(x & 0xffff0000u)); };
 #pragma unroll
   for (int v = 0; v < V; ++v) {
-    const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a[v]);
-    const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&b[v]);
-    const __nv_bfloat162* c2 = reinterpret_cast<const __nv_bfloat162*>(&c[v]);
-    const __nv_bfloat162* d2 = reinterpret_cast<const __nv_bfloat162*>(&d[v]);
-    const __nv_bfloat162* e2 = reinterpret_cast<const __nv_bfloat162*>(&ad[v]);
+    const uint32_t* a2 = reinterpret_cast<const uint32_t*>(&a[v]);
+    const uint32_t* b2 = reinterpret_cast<const uint32_t*>(&b[v]);
+    const uint32_t* c2 = reinterpret_cast<const uint32_t*>(&c[v]);
+    const uint32_t* d2 = reinterpret_cast<const uint32_t*>(&d[v]);
+    const uint32_t* e2 = reinterpret_cast<const uint32_t*>(&ad[v]);
     uint32_t o[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const float2 fa = __bfloat1622float2(a2[k]), fb = __bfloat1622float2(b2[k]);
-      const float2 fc = __bfloat1622float2(c2[k]), fd = __bfloat1622float2(d2[k]);
-      const float2 e = add_hwc ? __bfloat1622float2(e2[k]) : make_float2(0.f, 0.f);
-      // interpolate (rounded to bf16 like the library op), then add
-      const float v0 = __bfloat162float(__float2bfloat16_rn(w00 * fa.x + w01 * fb.x + w10 * fc.x + w11 * fd.x));
-      const float v1 = __bfloat162float(__float2bfloat16_rn(w00 * fa.y + w01 * fb.y + w10 * fc.y + w11 * fd.y));
-      o[k] = pack_bf16(v0 + e.x, v1 + e.y);
+      uint64_t t = f2_mul(widen(a2[k]), W00);
+      t = f2_fma(widen(b2[k]), W01, t);
+      t = f2_fma(widen(c2[k]), W10, t);
+      t = f2_fma(widen(d2[k]), W11, t);
+      float t0, t1;
+      f2_unpack(t, t0, t1);
+      const uint32_t r = pack_bf16(t0, t1);  // interpolated value rounded to bf16 like the library op
+      if (add_hwc) {
+        float u0, u1;
+        f2_unpack(f2_add(widen(r), widen(e2[k])), u0, u1);
+        o[k] = pack_bf16(u0, u1);
+      } else {
+        o[k] = r;
+      }
     }
     po[v] = make_uint4(o[0], o[1], o[2], o[3]);
   }
