@@ -54,7 +54,7 @@ def self_launch(args) -> None:
     if args.gpus <= 1 or "WORLD_SIZE" in os.environ or args.impl == "reference":
         return  # the reference arm runs on rank 0's host cores only: nothing to launch
     n = torch.cuda.device_count()
-    if n < args.gpus:
+    if n < args.gpus and args.dist_backend == "nccl":
         raise SystemExit(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {n}")
     import socket
     s = socket.socket()
@@ -186,6 +186,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-heads", action="store_true", help="aggregator only (diagnostic)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: ranks may share GPUs and the ring exchange is staged through host memory "
+                         "(tests the multi-rank flow on one GPU; not a performance configuration)")
     ap.add_argument("--patch-embed", default="conv", choices=["conv", "dinov2"],
                     help="conv (the north star's patch-embed GEMM, default) or the DINOv2 encoder of released checkpoints")
     args = ap.parse_args()
@@ -203,9 +206,14 @@ def main():
     from oracle.vggt_ref import forward_flops
 
     world, rank, local = dist_env()
+    if args.dist_backend == "gloo":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     cfg = vggt_1b().with_(patch_embed=args.patch_embed)
     S = args.views
     sd = make_state_dict(cfg, 0)
@@ -340,7 +348,8 @@ def main():
             "config": {"workload": f"vggt1b_518_S{S}" + ("_dinov2" if args.patch_embed == "dinov2" else "")
                        + ("_aggregator_only" if args.no_heads else ""),
                        "views": S, "img": 518, "tokens_per_view": N, "model": "VGGT-1B-shaped (24x2 blocks, C=1024)",
-                       "parallelism": "frame-sharded ring" if world > 1 else "single GPU",
+                       "parallelism": (f"frame-sharded ring over {world} ranks ({args.dist_backend})" if world > 1
+                                       else "single GPU"),
                        "l2": f"inputs larger than L2 (views {S * 3 * 518 * 518 * 4 / 1e6:.0f} MB fp32, weights "
                              f"1.8 GB bf16, both read every step; L2 126 MB)"},
             "peak_hbm_gb_per_gpu": peak_hbm,

@@ -70,16 +70,32 @@ class TorchDistComm:
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+        # gloo moves host memory only: device tensors are staged through host copies (synchronous);
+        # NCCL (the B200 path) exchanges device memory directly and asynchronously
+        self.stage = dist.get_backend(group) != "nccl"
 
     def sendrecv(self, send: torch.Tensor, recv: torch.Tensor, to: int, frm: int) -> list:
         """Start sending `send` to rank `to` and receiving `recv` from rank `frm`; returns requests to
         wait() on (torch orders the NCCL stream after the current stream at issue, and wait() orders
         the current stream after the transfer)."""
+        if self.stage and send.is_cuda:
+            hs, hr = send.cpu(), torch.empty(recv.shape, dtype=recv.dtype)
+            for q in dist.batch_isend_irecv([dist.P2POp(dist.isend, hs, to, group=self.group),
+                                             dist.P2POp(dist.irecv, hr, frm, group=self.group)]):
+                q.wait()
+            recv.copy_(hr)
+            return []
         ops_ = [dist.P2POp(dist.isend, send, to, group=self.group),
                 dist.P2POp(dist.irecv, recv, frm, group=self.group)]
         return dist.batch_isend_irecv(ops_)
 
     def all_gather(self, outs: List[torch.Tensor], x: torch.Tensor) -> None:
+        if self.stage and x.is_cuda:
+            houts = [torch.empty(o.shape, dtype=o.dtype) for o in outs]
+            dist.all_gather(houts, x.cpu(), group=self.group)
+            for o, h in zip(outs, houts):
+                o.copy_(h)
+            return
         dist.all_gather(outs, x, group=self.group)
 
 
