@@ -37,6 +37,10 @@
 #include "common.cuh"
 #include "host_util.h"
 
+#ifndef VX_FMHA_PSM
+#define VX_FMHA_PSM 0
+#endif
+
 namespace vx {
 
 struct AttnArgs {
@@ -80,8 +84,14 @@ VX_DEVICE WorkItem work_item(const AttnArgs& a, int w) {
   return {a.split_from + t, j0, j1 - j0, p, t};
 }
 
-template <int D, int NT_ = (D == 128 ? 1 : 2), int BKV_ = 128, bool ALIAS_ = false, bool SUMV_ = false>
+template <int D, int NT_ = (D == 128 ? 1 : 2), int BKV_ = 128, bool ALIAS_ = false, bool SUMV_ = false,
+          bool PSM_ = false>
 struct AttnCfg {
+  // PSM: P goes to shared memory (one 128 x 64-column SW128 tile per Q tile, K-major like Q) and the
+  // PV MMA reads it from there (SS), so TMEM holds only S and O per tile and S_i(j+1) is issued as
+  // soon as the softmax has loaded S_i(j), overlapping its exps (not aliased, 4 tiles still fit)
+  static constexpr bool PSM = PSM_;
+  static_assert(!(PSM_ && ALIAS_), "PSM and ALIAS are exclusive");
   // ALIAS: P is written over the first BKV/2 columns of S (4 tiles fit TMEM); S_i(j+1) is then
   // issued after PV_i(j) instead of running ahead
   static constexpr bool ALIAS = ALIAS_;
@@ -106,11 +116,14 @@ struct AttnCfg {
   static constexpr int THREADS = 128 + 128 * NT;
   static constexpr int ROWS = 128 * NT;                    // query rows per work unit
   static constexpr uint32_t BAR_BYTES = 512;
-  static constexpr uint32_t SMEM = NT * Q_TILE_BYTES + KST * (KV_TILE_BYTES + V_STAGE_BYTES) + 1024 + BAR_BYTES;
-  // TMEM columns: S_i [BKV fp32] ... | P_i [BKV/2] ... | O_i [DO fp32] ...
-  static constexpr uint32_t O_BASE = ((NT * BKV + (ALIAS ? 0 : NT * BKV / 2)) + 63) / 64 * 64;
+  static constexpr uint32_t P_TILE_BYTES = PSM ? 128 * 128 : 0;  // 128 rows x 128 B (BKV <= 64 bf16 used)
+  static constexpr uint32_t SMEM =
+      NT * (Q_TILE_BYTES + P_TILE_BYTES) + KST * (KV_TILE_BYTES + V_STAGE_BYTES) + 1024 + BAR_BYTES;
+  // TMEM columns: S_i [BKV fp32] ... | P_i [BKV/2] (neither ALIAS nor PSM) ... | O_i [DO fp32] ...
+  static constexpr uint32_t O_BASE = ((NT * BKV + (ALIAS || PSM ? 0 : NT * BKV / 2)) + 63) / 64 * 64;
   static_assert(O_BASE + NT * DO <= 512, "TMEM budget");
-  static_assert(!SUMV || (ALIAS && D == 64), "SUMV is implemented for the aliased d=64 kernel");
+  static_assert(!SUMV || ((ALIAS || PSM) && D == 64), "SUMV is implemented for the d=64 kernels");
+  static_assert(!PSM || (D == 64 && BKV <= 64), "PSM: one 128-byte P row per query row");
   static_assert(BKV % 16 == 0 && (BKV <= 64 || BKV % 64 == 0), "KV tile width");
   static __host__ __device__ constexpr uint32_t tS(int i) { return i * BKV; }
   static __host__ __device__ constexpr uint32_t tP(int i) { return ALIAS ? i * BKV : NT * BKV + i * (BKV / 2); }
@@ -165,14 +178,16 @@ constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
 
 // EMU_PAIRS_OF_8: of every 8 exp pairs, this many use the FMA-pipe polynomial
 template <int D, int EMU_PAIRS_OF_8, int NT_, int BKV_, bool ALIAS_, bool SUMV_, bool NOHINT = false,
-          bool SPEC_ = false, bool LDSPLIT = false>
-__global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS, 1)
+          bool SPEC_ = false, bool LDSPLIT = false, bool PSM_ = false>
+__global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_>::THREADS, 1)
     fmha_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                 const __grid_constant__ CUtensorMap tmV, const AttnArgs a) {
-  using Cfg = AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>;
+  using Cfg = AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_>;
   constexpr bool ALIAS = ALIAS_;
-  // speculative exps (step_spec) need P writes that can be repeated before p_full: aliased kernels only
-  constexpr bool SPEC = SPEC_ && ALIAS_;
+  constexpr bool PSM = PSM_;
+  // speculative exps (step_spec) need P writes that can be repeated before p_full: aliased or
+  // shared-memory P only
+  constexpr bool SPEC = SPEC_ && (ALIAS_ || PSM_);
   constexpr bool SUMV = SUMV_;
   constexpr int DO = Cfg::DO;
   constexpr int BKV = Cfg::BKV;
@@ -183,7 +198,8 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   constexpr int NT = Cfg::NT;
   uint8_t* sQ = smem;                                 // NT tiles
-  uint8_t* sK = sQ + NT * Cfg::Q_TILE_BYTES;          // KST tiles
+  [[maybe_unused]] uint8_t* sP = sQ + NT * Cfg::Q_TILE_BYTES;  // PSM: NT P tiles (1024-aligned)
+  uint8_t* sK = sP + NT * Cfg::P_TILE_BYTES;          // KST tiles
   uint8_t* sV = sK + KST * Cfg::KV_TILE_BYTES;        // KST stages (V tile [+ ones panel])
   uint64_t* bar = reinterpret_cast<uint64_t*>(sV + KST * Cfg::V_STAGE_BYTES);
   uint64_t* q_full = bar;
@@ -328,12 +344,18 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
         }
       };
       // V is the MN-major B operand: for D = 128 its two 64-column panels are the two MN atoms (LBO)
+      [[maybe_unused]] const uint64_t pdesc0 = make_sdesc(smem_u32(sP), 16, 1024, 2);  // PSM: K-major SW128
       auto issue_pv = [&](int i, uint32_t vs, uint32_t acc) {
         const uint64_t vd = make_sdesc(vs, Cfg::KVPANEL_BYTES, Cfg::SBO, Cfg::LAYOUT);
 #pragma unroll
-        for (int kk = 0; kk < BKV / 16; ++kk)
-          mma_ts_if(lead, tmem + Cfg::tO(i), tmem + Cfg::tP(i) + kk * 8, vd + ((kk * 16 * Cfg::ROW_BYTES) >> 4),
-                    idesc_pv, (acc | kk) != 0);
+        for (int kk = 0; kk < BKV / 16; ++kk) {
+          if constexpr (PSM)  // P_i from shared memory: 16 bf16 = 32 bytes per k-step within the 128-B row
+            mma_ss_if(lead, tmem + Cfg::tO(i), pdesc0 + ((i * Cfg::P_TILE_BYTES + kk * 32) >> 4),
+                      vd + ((kk * 16 * Cfg::ROW_BYTES) >> 4), idesc_pv, (acc | kk) != 0);
+          else
+            mma_ts_if(lead, tmem + Cfg::tO(i), tmem + Cfg::tP(i) + kk * 8, vd + ((kk * 16 * Cfg::ROW_BYTES) >> 4),
+                      idesc_pv, (acc | kk) != 0);
+        }
       };
       uint32_t c = 0;  // global K/V tile counter
       uint32_t n = 0;  // local unit counter
@@ -430,10 +452,9 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
             }
             const uint32_t vs = smem_u32(sV + st * Cfg::V_STAGE_BYTES);
             mbar_wait(&v_full[st], ph);
-            if (j == 0)  // the previous unit's epilogue must have read O
-              for (int i = 0; i < NT; ++i) mbar_wait(&o_empty[i], (n & 1) ^ 1);
             for (int i = 0; i < NT; ++i) {
               mbar_wait(&p_full[i], pfull_ph);
+              if (j == 0) mbar_wait(&o_empty[i], (n & 1) ^ 1);  // the previous unit's epilogue has read O_i
               tc_fence_after();
               issue_pv(i, vs, j > 0);
               mma_commit_if(lead, &p_free[i]);
@@ -481,7 +502,8 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
         const int valid = a.Lk - BKV * (wi.j0 + j);
         // speculative tiles (48 wide) leave the last 16 S columns in flight: the first 16 exp pairs
         // only need columns 0-31, and the wait for the rest sits just before pair 16
-        constexpr bool SPLIT_LD = SPEC && LDSPLIT && BKV == 48;
+        // (not with PSM: s_free is arrived right after the S load so S(j+1) can be issued into it)
+        constexpr bool SPLIT_LD = SPEC && LDSPLIT && BKV == 48 && !PSM;
         const bool spec_now = SPEC && j > 0 && valid >= BKV;
         if (SPLIT_LD && spec_now) {
           tmem_ld32(S_addr, sr);
@@ -513,6 +535,24 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
         };
         // P = 2^(s * scale * log2e - m) for the whole tile, packed to bf16 and stored over S
         uint64_t acc[4];
+        // PSM: this thread's row of its tile's P buffer (128-byte rows, 16-byte chunks XOR-swizzled by row
+        // % 8 = the SW128 K-major layout the PV MMA reads); P_i(j-1) must have been consumed first
+        [[maybe_unused]] uint8_t* prow = sP + tile * Cfg::P_TILE_BYTES + r * 128;
+        [[maybe_unused]] bool pfree_waited = false;
+        auto wait_pfree = [&]() {
+          if (j > 0 && !pfree_waited) {  // PV_i(j-1) done: P buffer reusable, O stable
+            mbar_wait(&p_free[tile], pv_cnt & 1);
+            ++pv_cnt;
+            tc_fence_after();
+          }
+          pfree_waited = true;
+        };
+        auto store_p_chunks = [&](const uint32_t* pk, int q0, int q1) {
+#pragma unroll
+          for (int q = q0; q < q1; ++q)
+            *reinterpret_cast<uint4*>(prow + ((q ^ (r & 7)) * 16)) =
+                make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+        };
         auto exps = [&](const uint64_t NEGM, auto mid_wait) {
           acc[0] = acc[1] = acc[2] = acc[3] = 0;
           constexpr int NCHUNK = (BKV + 63) / 64;
@@ -539,17 +579,33 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
               pk[c] = pack_bf16(p0, p1);
               // 48-wide tiles: store the first 16 P columns while the last 8 pairs are computed
               if constexpr (PAIRS == 24) {
-                if (c == 15) tmem_st16(P_addr + 32 * hf, pk);
+                if (c == 15) {
+                  if constexpr (PSM) {
+                    wait_pfree();
+                    store_p_chunks(pk, 0, 4);
+                  } else {
+                    tmem_st16(P_addr + 32 * hf, pk);
+                  }
+                }
               }
             }
             VX_TRACE(trace_slot_sm(unit_n, wl, lane, tile, j, 3));
-            if (!ALIAS && hf == 0 && j > 0) {  // P_i(j-1) consumed and O stable (waited after the first exps)
-              mbar_wait(&p_free[tile], pv_cnt & 1);
-              ++pv_cnt;
-              tc_fence_after();
+            if constexpr (PSM) {
+              if constexpr (PAIRS == 24) {
+                store_p_chunks(pk, 4, 6);
+              } else {
+                wait_pfree();
+                store_p_chunks(pk, 0, PAIRS / 4);
+              }
+            } else {
+              if (!ALIAS && hf == 0 && j > 0) {  // P_i(j-1) consumed and O stable (waited after the first exps)
+                mbar_wait(&p_free[tile], pv_cnt & 1);
+                ++pv_cnt;
+                tc_fence_after();
+              }
+              if constexpr (PAIRS == 24) tmem_st8(P_addr + 32 * hf + 16, pk + 16);
+              else tmem_st_n<PAIRS>(P_addr + 32 * hf, pk);
             }
-            if constexpr (PAIRS == 24) tmem_st8(P_addr + 32 * hf + 16, pk + 16);
-            else tmem_st_n<PAIRS>(P_addr + 32 * hf, pk);
           }
         };
         auto rescale_o = [&](const float alpha) {
@@ -613,6 +669,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_>::THREADS,
         else if (spec_now) step_spec();
         else step(BoolTag<false>{});
         tmem_wait_st();
+        if constexpr (PSM) fence_proxy_async_smem();  // P stores visible to the tensor core's async proxy
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[tile]);
@@ -831,9 +888,9 @@ static unsigned* sched_counters(cudaStream_t st) {
 }
 
 template <int D, int EMU, int NT = (D == 128 ? 1 : 2), int BKV = 128, bool ALIAS = false, bool SUMV = false,
-          bool NOHINT = false, bool SPEC = false, bool LDSPLIT = false>
+          bool NOHINT = false, bool SPEC = false, bool LDSPLIT = false, bool PSM = false>
 static int launch_fmha(const void* q, const void* k, const void* v, AttnArgs args, cudaStream_t st) {
-  using Cfg = AttnCfg<D, NT, BKV, ALIAS, SUMV>;
+  using Cfg = AttnCfg<D, NT, BKV, ALIAS, SUMV, PSM>;
   CUtensorMap tq, tk, tv;
   constexpr int PC = Cfg::PANEL_COLS;
   if (!make_tmap_2d_bf16(&tq, q, (uint64_t)args.H * args.Tq, D, D, 128, PC, Cfg::SWIZZLE)) return VX_E_ARG;
@@ -872,7 +929,7 @@ static int launch_fmha(const void* q, const void* k, const void* v, AttnArgs arg
     }
   }
   args.work = args.split_from + (args.units - args.split_from) * args.parts;
-  auto kern = fmha_kernel<D, EMU, NT, BKV, ALIAS, SUMV, NOHINT, SPEC, LDSPLIT>;
+  auto kern = fmha_kernel<D, EMU, NT, BKV, ALIAS, SUMV, NOHINT, SPEC, LDSPLIT, PSM>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
@@ -955,7 +1012,11 @@ static int attention_impl(const void* q, const void* k, const void* v, void* out
       default: break;
     }
 #endif
+#if VX_FMHA_PSM
+    return launch_fmha<64, 2, 4, 48, false, true, true, true, false, true>(q, k, v, a, st);
+#else
     return launch_fmha<64, 2, 4, 48, true, true, true, true, true>(q, k, v, a, st);
+#endif
   }
   if (D == 128) return launch_fmha<128, 2>(q, k, v, a, st);
   return launch_fmha<32, 2>(q, k, v, a, st);
