@@ -40,6 +40,9 @@
 #ifndef VX_FMHA_PSM
 #define VX_FMHA_PSM 0
 #endif
+#ifndef VX_FMHA_W96
+#define VX_FMHA_W96 0
+#endif
 
 namespace vx {
 
@@ -120,11 +123,11 @@ struct AttnCfg {
   static constexpr uint32_t SMEM =
       NT * (Q_TILE_BYTES + P_TILE_BYTES) + KST * (KV_TILE_BYTES + V_STAGE_BYTES) + 1024 + BAR_BYTES;
   // TMEM columns: S_i [BKV fp32] ... | P_i [BKV/2] (neither ALIAS nor PSM) ... | O_i [DO fp32] ...
-  static constexpr uint32_t O_BASE = ((NT * BKV + (ALIAS || PSM ? 0 : NT * BKV / 2)) + 63) / 64 * 64;
+  static constexpr uint32_t O_BASE = ((NT * BKV + (ALIAS || PSM ? 0 : NT * BKV / 2)) + 31) / 32 * 32;
   static_assert(O_BASE + NT * DO <= 512, "TMEM budget");
   static_assert(!SUMV || ((ALIAS || PSM) && D == 64), "SUMV is implemented for the d=64 kernels");
   static_assert(!PSM || (D == 64 && BKV <= 64), "PSM: one 128-byte P row per query row");
-  static_assert(BKV % 16 == 0 && (BKV <= 64 || BKV % 64 == 0), "KV tile width");
+  static_assert(BKV % 16 == 0 && (BKV <= 64 || BKV % 64 == 0 || (BKV == 96 && ALIAS && D == 64)), "KV tile width");
   static __host__ __device__ constexpr uint32_t tS(int i) { return i * BKV; }
   static __host__ __device__ constexpr uint32_t tP(int i) { return ALIAS ? i * BKV : NT * BKV + i * (BKV / 2); }
   static __host__ __device__ constexpr uint32_t tO(int i) { return O_BASE + i * DO; }
@@ -498,6 +501,127 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_>::TH
         VX_TRACE(trace_slot_sm(unit_n, wl, lane, tile, j, 1));
         sph ^= 1;
         tc_fence_after();
+        if constexpr (BKV == 96) {
+          // 96-wide KV tiles (3 Q tiles fit TMEM: 3 x (96 S/P + 72 O) = 504 columns), processed as two
+          // 48-column halves A = S[0, 48), B = S[48, 96) so the registers stay those of one half. P (96
+          // bf16 = 48 columns) goes over S[0, 48): P_A to columns 0-23 (once A is loaded), P_B to 24-47
+          // (once A is consumed).
+          const int valid = a.Lk - BKV * (wi.j0 + j);
+          uint32_t sr[48];
+          uint32_t pk[24];
+          auto ld48 = [&](int half) {
+            tmem_ld32(S_addr + 48 * half, sr);
+            tmem_ld16(S_addr + 48 * half + 32, sr + 32);
+            tmem_wait_ld();
+          };
+          auto mask48 = [&](int half) {
+#pragma unroll
+            for (int c = 0; c < 48; ++c)
+              if (48 * half + c >= valid) sr[c] = 0xff800000u;
+          };
+          auto max48 = [&]() -> float {
+            float mq[3];
+#pragma unroll
+            for (int q = 0; q < 3; ++q) mq[q] = fmaxf(__uint_as_float(sr[q]), __uint_as_float(sr[q + 3]));
+#pragma unroll
+            for (int c = 6; c < 48; c += 6)
+#pragma unroll
+              for (int q = 0; q < 3; ++q) mq[q] = max3(mq[q], __uint_as_float(sr[c + q]), __uint_as_float(sr[c + 3 + q]));
+            return fmaxf(fmaxf(mq[0], mq[1]), mq[2]) * sl2;
+          };
+          // 24 exp pairs of the half in sr -> pk; optionally stored as P words [pword, pword + 24)
+          auto exps48 = [&](const float m, uint32_t pword, bool store) {
+            const uint64_t NEGM = f2_pack(-m, -m);
+#pragma unroll
+            for (int c = 0; c < 24; ++c) {
+              const uint64_t x = f2_fma(f2_pack(__uint_as_float(sr[2 * c]), __uint_as_float(sr[2 * c + 1])), SL2, NEGM);
+              float x0, x1, p0, p1;
+              f2_unpack(x, x0, x1);
+              if ((c & 7) >= 8 - EMU_PAIRS_OF_8) {
+                ex2_poly2<2>(x0, x1, p0, p1);
+              } else {
+                p0 = ex2(x0);
+                p1 = ex2(x1);
+              }
+              pk[c] = pack_bf16(p0, p1);
+              if (store && c == 15) tmem_st16(P_addr + pword, pk);
+            }
+            if (store) tmem_st8(P_addr + pword + 16, pk + 16);
+          };
+          auto store_pk = [&](uint32_t pword) {
+            tmem_st16(P_addr + pword, pk);
+            tmem_st8(P_addr + pword + 16, pk + 16);
+          };
+          auto rescale_o96 = [&](const float alpha) {  // O_i (with the row-sum column) *= alpha
+            uint32_t orr[32];
+#pragma unroll
+            for (int c0 = 0; c0 < DO; c0 += 32) {
+              const int wd = DO - c0 >= 32 ? 32 : DO - c0;
+              if (wd == 32) tmem_ld32(O_addr + c0, orr);
+              else tmem_ld16(O_addr + c0, orr);
+              tmem_wait_ld();
+#pragma unroll
+              for (int c = 0; c < 32; ++c) orr[c] = __float_as_uint(__uint_as_float(orr[c]) * alpha);
+              if (wd == 32) tmem_st32(O_addr + c0, orr);
+              else if (wd == 16) tmem_st16(O_addr + c0, orr);
+              else tmem_st8(O_addr + c0, orr);
+            }
+          };
+          constexpr float GUARD = 120.0f;  // log2 units: P_A stays finite, so it can be rescaled in place
+          bool done = false;
+          if (SPEC && j > 0 && valid >= BKV) {
+            // speculative: exps with the running max, tile max alongside
+            ld48(0);
+            exps48(m_run, 0, false);
+            const float mxa = max48();
+            if (!__any_sync(0xffffffff, mxa > m_run + GUARD)) {
+              store_pk(0);
+              ld48(1);
+              exps48(m_run, 24, true);
+              const float m_new = fmaxf(mxa, max48());
+              const bool need = m_new > m_run + RESCALE_THRESHOLD;
+              if (__any_sync(0xffffffff, need)) {  // rare: redo B, rescale P_A in place and O
+                const float alpha = need ? ex2(m_run - m_new) : 1.0f;
+                if (need) m_run = m_new;
+                exps48(m_run, 24, true);
+                uint32_t w[32];
+                tmem_ld32(P_addr, w);
+                tmem_wait_ld();
+#pragma unroll
+                for (int c = 0; c < 24; ++c) {
+                  const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[c]));
+                  w[c] = pack_bf16(f.x * alpha, f.y * alpha);
+                }
+                tmem_st16(P_addr, w);
+                tmem_st8(P_addr + 16, w + 16);
+                rescale_o96(alpha);
+              }
+              done = true;
+            }
+          }
+          if (!done) {  // exact: both halves' max first (first tile, masked tile, guard fallback)
+            ld48(0);
+            if (valid < BKV) mask48(0);
+            const float mxa = max48();
+            ld48(1);
+            if (valid < BKV) mask48(1);
+            const float m_new = fmaxf(mxa, max48());
+            const bool need = m_new > m_run + RESCALE_THRESHOLD;
+            const float alpha = need ? ex2(m_run - m_new) : 1.0f;
+            if (need) m_run = m_new;
+            exps48(m_run, 24, false);  // P_B, held until A has been reloaded (its S columns 24-47 are P_B's)
+            ld48(0);
+            if (valid < BKV) mask48(0);
+            store_pk(24);
+            exps48(m_run, 0, true);
+            if (__any_sync(0xffffffff, need) && j > 0) rescale_o96(alpha);
+          }
+          tmem_wait_st();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&p_full[tile]);
+          continue;
+        }
         uint32_t sr[BKV];
         const int valid = a.Lk - BKV * (wi.j0 + j);
         // speculative tiles (48 wide) leave the last 16 S columns in flight: the first 16 exp pairs
@@ -1014,6 +1138,8 @@ static int attention_impl(const void* q, const void* k, const void* v, void* out
 #endif
 #if VX_FMHA_PSM
     return launch_fmha<64, 2, 4, 48, false, true, true, true, false, true>(q, k, v, a, st);
+#elif VX_FMHA_W96
+    return launch_fmha<64, 2, 3, 96, true, true, true, true, false>(q, k, v, a, st);
 #else
     return launch_fmha<64, 2, 4, 48, true, true, true, true, true>(q, k, v, a, st);
 #endif
