@@ -28,6 +28,9 @@ class _FakeDist:
     def get_world_size(self, group=None):
         return self.world
 
+    def get_backend(self, group=None):
+        return "nccl"  # device tensors go through P2POp directly (no host staging)
+
     class P2POp:
         def __init__(self, op, tensor, peer, group=None):
             self.op, self.tensor, self.peer = op, tensor, peer
