@@ -286,12 +286,17 @@ __host__ __device__ constexpr uint32_t make_idesc_bf16(int M, int N, int a_mn_ma
 }
 
 // shared-memory matrix descriptor. layout: 2 = SWIZZLE_128B, 4 = SWIZZLE_64B, 6 = SWIZZLE_32B
-VX_DEVICE uint64_t make_sdesc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes, uint32_t layout) {
+VX_DEVICE uint64_t make_sdesc(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes, uint32_t layout,
+                              uint32_t base_offset = 0) {
   uint64_t d = 0;
   d |= uint64_t((saddr >> 4) & 0x3FFF);
   d |= uint64_t((lbo_bytes >> 4) & 0x3FFF) << 16;
   d |= uint64_t((sbo_bytes >> 4) & 0x3FFF) << 32;
   d |= uint64_t(1) << 46;  // version (sm_100)
+  // matrix base offset (left 0 by every caller: the swizzle is applied on absolute shared-memory
+  // address bits, so starts a whole number of 128-byte rows into a swizzle atom work without it —
+  // measured with the DPT output head's row-shifted operand views, gemm.cu HALO)
+  d |= uint64_t(base_offset & 7) << 49;
   d |= uint64_t(layout & 7) << 61;
   return d;
 }

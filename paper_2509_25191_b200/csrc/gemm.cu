@@ -42,14 +42,25 @@ constexpr int GEMM_BK = 64;
 constexpr int GEMM_THREADS = 384;  // w0 TMA, w1 MMA, w2 TMEM alloc, w3 idle, w4..w11 epilogue
 constexpr int GEMM_EPI_WARPS = 8;  // two warps per TMEM lane quarter, each owning half of the tile columns
 
-template <int BN, bool CG2 = false, bool RT = false>
+// HALO (implicit 3x3 conv with N <= 32, the DPT output head): one stage per 64 input channels holds
+// the three 130-row bands of the tile's input rows (row shifts dy = 0, 1, 2 of the padded grid) and
+// the 9 taps' B tiles; tap (dy, dx) reads band dy from row dx on, so the input is staged once per
+// channel block instead of once per tap (9x less L2 -> shared traffic; 36 MMAs per stage)
+constexpr int HALO_ROWS = GEMM_BM + 2;
+constexpr int HALO_MAX_CB = 2;  // input channels <= 128 (the DPT output head: features / 2)
+constexpr uint32_t HALO_BAND_BYTES = (HALO_ROWS * GEMM_BK * 2 + 1023) / 1024 * 1024;
+
+template <int BN, bool CG2 = false, bool RT = false, bool HALO = false>
 struct GemmCfg {
   // CG2 (CTA pair, cta_group::2): each CTA stages its 128 A rows and half of the B tile; RT (TMA
   // residual epilogue): 4 stages, leaving 64 KB for the residual boxes
-  static constexpr int STAGES = RT ? (VX_RT_NBOX >= 4 ? 3 : 4) : (CG2 ? 6 : (BN == 256 ? 4 : (BN == 128 ? 6 : 8)));
-  static constexpr uint32_t A_BYTES = GEMM_BM * GEMM_BK * 2;
-  static constexpr uint32_t B_BYTES = (CG2 ? BN / 2 : BN) * GEMM_BK * 2;
-  static constexpr uint32_t RING = STAGES * (A_BYTES + B_BYTES);
+  static constexpr int STAGES =
+      HALO ? 3 : (RT ? (VX_RT_NBOX >= 4 ? 3 : 4) : (CG2 ? 6 : (BN == 256 ? 4 : (BN == 128 ? 6 : 8))));
+  static constexpr uint32_t A_BYTES = HALO ? 3 * HALO_BAND_BYTES : GEMM_BM * GEMM_BK * 2;
+  // HALO: the B (weight) tiles of all 9 taps x up to HALO_MAX_CB channel blocks stay resident
+  static constexpr uint32_t B_BYTES = HALO ? 0 : (CG2 ? BN / 2 : BN) * GEMM_BK * 2;
+  static constexpr uint32_t B_RES_BYTES = HALO ? 9 * HALO_MAX_CB * BN * GEMM_BK * 2 : 0;
+  static constexpr uint32_t RING = STAGES * (A_BYTES + B_BYTES) + B_RES_BYTES;
   static constexpr uint32_t SMEM = RING + 1024 /*align*/ + 256 /*barriers*/;
   static constexpr uint32_t TMEM_COLS = 2 * BN;
   static_assert(SMEM <= 227 * 1024, "GEMM stage ring exceeds the 227 KB smem per CTA");
@@ -392,18 +403,20 @@ template <int BN, int EPI, int HD, bool MC, bool CG2 = false>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmR, const GemmArgs args) {
-  using Cfg = GemmCfg<BN, CG2, EPI == VX_EPI_RESID_TMA>;
+  constexpr bool HALO = EPI == VX_EPI_HEADOUT;
+  using Cfg = GemmCfg<BN, CG2, EPI == VX_EPI_RESID_TMA, HALO>;
   constexpr bool PAIRED = MC || CG2;
   constexpr int STAGES = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * Cfg::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * Cfg::B_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::RING);  // after the stages (+ resident B)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  [[maybe_unused]] uint64_t* bres_full = tempty + 2;  // HALO: resident weight tiles landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 3);
   // offset from smem_raw (not the integer-aligned pointer) so the compiler keeps the shared state
   // space and emits LDS / STS for the transpose tile rather than generic LD / ST
   [[maybe_unused]] float* epi_buf = reinterpret_cast<float*>(smem_raw + (smem - smem_raw) + Cfg::RING + 256);
@@ -442,6 +455,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     if constexpr (EPI == VX_EPI_RESID_TMA)
       for (int i = 0; i < RT_NBOX * GEMM_EPI_WARPS; ++i) mbar_init(&rbar[i], 1);
+    if constexpr (HALO) mbar_init(bres_full, 1);
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -463,6 +477,24 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       for (int u = unit0; u < units; u += ustep) {
         int m_blk, n_blk;
         tile_mn(u, m_blk, n_blk);
+        if constexpr (HALO) {
+          if (u == unit0) {  // the weights of every (tap, channel block), once per CTA (N == BN: one N tile)
+            mbar_expect_tx(bres_full, 9 * args.conv_cin_blocks * BN * GEMM_BK * 2);
+            for (int cb = 0; cb < args.conv_cin_blocks; ++cb)
+              for (int t = 0; t < 9; ++t)
+                tma_load_2d_hint(sB + (cb * 9 + t) * (BN * GEMM_BK * 2), &tmB, bres_full,
+                                 (t * args.conv_cin_blocks + cb) * GEMM_BK, 0, pol_b);
+          }
+          for (int cb = 0; cb < args.conv_cin_blocks; ++cb) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_expect_tx(&full[stage], 3 * HALO_ROWS * GEMM_BK * 2);
+            for (int dy = 0; dy < 3; ++dy)
+              tma_load_2d(sA + stage * Cfg::A_BYTES + dy * HALO_BAND_BYTES, &tmA, &full[stage], cb * GEMM_BK,
+                          m_blk * GEMM_BM + dy * args.conv_w2);
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          }
+          continue;
+        }
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           int a_col = kb * GEMM_BK, a_row = m_blk * GEMM_BM;
@@ -505,6 +537,32 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
+        if constexpr (HALO) {
+          if (u == unit0) mbar_wait(bres_full, 0);
+          for (int cb = 0; cb < args.conv_cin_blocks; ++cb) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint32_t a0 = smem_u32(sA + stage * Cfg::A_BYTES);
+            const uint32_t b0 = smem_u32(sB) + cb * 9 * (BN * GEMM_BK * 2);
+#pragma unroll
+            for (int t = 0; t < 9; ++t) {
+              const int dy = t / 3, dx = t % 3;
+              // band dy from row dx: the 128-byte swizzle is applied on absolute shared-memory address bits,
+              // so a start that is a whole number of 128-byte rows into a swizzle atom needs no base offset
+              const uint32_t at = a0 + dy * HALO_BAND_BYTES + dx * (GEMM_BK * 2);
+              const uint32_t bt = b0 + t * (BN * GEMM_BK * 2);
+#pragma unroll
+              for (int k = 0; k < GEMM_BK / 16; ++k)
+                mma_ss(d_tmem, make_sdesc(at + k * 32, 16, 1024, 2), make_sdesc(bt + k * 32, 16, 1024, 2), idesc,
+                       (cb | t | k) != 0);
+            }
+            mma_commit(&empty[stage]);
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          }
+          mma_commit(&tfull[acc]);
+          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+          continue;
+        }
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
@@ -721,7 +779,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 template <int BN, int EPI, int HD, bool MC = false, bool CG2 = false>
 static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& args, cudaStream_t st,
                        const CUtensorMap* tr = nullptr) {
-  using Cfg = GemmCfg<BN, CG2, EPI == VX_EPI_RESID_TMA>;
+  using Cfg = GemmCfg<BN, CG2, EPI == VX_EPI_RESID_TMA, EPI == VX_EPI_HEADOUT>;
   static const CUtensorMap no_map{};
   const CUtensorMap& trr = tr ? *tr : no_map;
   constexpr uint32_t SMEM = Cfg::SMEM + epi_smem_bytes<EPI>();
@@ -769,7 +827,6 @@ static int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, c
     case VX_EPI_PATCH: return launch_gemm<BN, VX_EPI_PATCH, 0, MC, CG2>(ta, tb, a, st);
     case VX_EPI_F32: return launch_gemm<BN, VX_EPI_F32, 0, MC, CG2>(ta, tb, a, st);
     case VX_EPI_SPATIAL: return launch_gemm<BN, VX_EPI_SPATIAL, 0, MC, CG2>(ta, tb, a, st);
-    case VX_EPI_HEADOUT: return launch_gemm<BN, VX_EPI_HEADOUT, 0, MC, CG2>(ta, tb, a, st);
     case VX_EPI_QKV:
       if (!a.ep.qn_w && !a.ep.rope_cos) return launch_gemm<BN, VX_EPI_QKV, 0, MC, CG2>(ta, tb, a, st);
       if (a.ep.head_dim == 64) return launch_gemm<BN, VX_EPI_QKV, 64, MC, CG2>(ta, tb, a, st);
@@ -866,8 +923,10 @@ extern "C" int vx_gemm_spatial(const void* A, const void* B, int N, int K, const
   VX_CHECK_ARG(N % (s * s) == 0 && (N / (s * s)) % 32 == 0, "vx_gemm_spatial: Cout must be a multiple of 32");
   VX_CHECK_ARG(!(sp->subsample2 && s > 1), "vx_gemm_spatial: subsample2 and shuffle are exclusive");
   if (sp->head_odim > 0) VX_CHECK_ARG(N == 32 && sp->head_w && sp->head_b && sp->head_pred && sp->head_conf &&
-                                      sp->head_odim >= 2 && !sp->subsample2 && s == 1,
-                                      "vx_gemm_spatial: fused head needs N == 32 and head pointers");
+                                      sp->head_odim >= 2 && !sp->subsample2 && s == 1 && sp->conv3x3 &&
+                                      K <= 9 * HALO_MAX_CB * GEMM_BK,
+                                      "vx_gemm_spatial: fused head needs a 3x3 conv with N == 32, <= 128 input "
+                                      "channels and head pointers");
   GemmArgs args = {};
   args.N = N;
   args.K = K;
@@ -889,7 +948,9 @@ extern "C" int vx_gemm_spatial(const void* A, const void* B, int N, int K, const
   const int64_t lda = sp->conv3x3 ? K / 9 : K;
   const int pm = pair_mode(BN, int(rows));
   CUtensorMap ta, tb;
-  if (!make_tmap_2d_bf16(&ta, A, rows, lda, lda, GEMM_BM, GEMM_BK, 128)) return VX_E_ARG;
+  // the output head stages 130-row input bands (HALO)
+  if (!make_tmap_2d_bf16(&ta, A, rows, lda, lda, sp->head_odim > 0 ? HALO_ROWS : GEMM_BM, GEMM_BK, 128))
+    return VX_E_ARG;
   if (!make_tmap_2d_bf16(&tb, B, N, K, K, pm ? BN / 2 : BN, GEMM_BK, 128)) return VX_E_ARG;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int epi = sp->head_odim > 0 ? VX_EPI_HEADOUT : VX_EPI_SPATIAL;

@@ -15,7 +15,18 @@ from paper_2509_25191_b200 import ops  # noqa: E402
 what, views = sys.argv[1], int(sys.argv[2])
 N, H, d, C = 1374, 16, 64, 1024
 T = views * N
-if what.startswith("attn"):
+if what == "headout":  # DPT output head: 3x3 conv 128 -> 32 on 16 views at 518^2 + fused fp32 1x1 + activation
+    Fr, Hh = 16, 518
+    x = torch.zeros(Fr, Hh + 2, Hh + 2, 128, device="cuda", dtype=torch.bfloat16)
+    x[:, 1:-1, 1:-1] = torch.randn(Fr, Hh, Hh, 128, device="cuda").to(torch.bfloat16)
+    w = (torch.randn(32, 9 * 128, device="cuda") * 0.03).to(torch.bfloat16)
+    b = torch.randn(32, device="cuda")
+    hw, hb = torch.randn(3, 32, device="cuda") * 0.1, torch.randn(3, device="cuda")
+    pred = torch.empty(Fr, Hh, Hh, 2, device="cuda")
+    conf = torch.empty(Fr, Hh, Hh, device="cuda")
+    run = lambda: ops.gemm_spatial(x.view(-1, 128), w, b, Fr, Hh, Hh, conv3x3=True,  # noqa: E731
+                                   head=(hw, hb, 1, pred, conf))
+elif what.startswith("attn"):
     q, k, v = (torch.randn(H, T, d, device="cuda", dtype=torch.bfloat16) for _ in range(3))
     o = torch.empty(T, H * d, device="cuda", dtype=torch.bfloat16)
     nseq, L = (1, T) if what == "attn_global" else (views, N)
