@@ -18,9 +18,9 @@ SURVEY.md Appendix A, with the VGGT-X modifications the paper describes:
   * `PAPER.md:146` chunk S = 128.
 
 Partial external anchors (tests/test_oracle_anchors.py): `dinov2_patch_tokens` equals the
-`transformers` Dinov2WithRegistersModel and `_fusion` / `_rcu` equal its DPTFeatureFusionLayer on
-shared random weights; nothing pins the VGGT-specific parts (2D RoPE, q/k LayerNorm, camera head,
-DPT reassembly).
+`transformers` Dinov2WithRegistersModel, `_fusion` / `_rcu` its DPTFeatureFusionLayer and `_reassemble`
+(without the UV pos-embed VGGT adds) its DPTReassembleLayer on shared random weights; nothing pins the
+VGGT-specific parts (2D RoPE, q/k LayerNorm, camera head, UV pos-embed).
 
 Everything runs in fp32 on the CPU with the seeded weights from
 `paper_2509_25191_b200.weights` (matrix weights already bf16-representable).
@@ -337,6 +337,21 @@ def _fusion(sd, name, x0, x1=None, size=None):
     return _conv(out, sd, name + ".out_conv")
 
 
+def _reassemble(x, sd, head, i, pos=None):
+    """Kept layer i's token map (F, 2C, g, g) -> 1x1 projection (+ UV pos-embed) -> resize: ConvTranspose
+    k = s = 4 (i = 0), k = s = 2 (i = 1), identity (i = 2), Conv 3x3 stride 2 (i = 3)."""
+    x = _conv(x, sd, f"{head}projects.{i}", padding=0)
+    if pos is not None:
+        x = x + pos
+    if i == 0:
+        x = F.conv_transpose2d(x, sd[head + "resize_layers.0.weight"], sd[head + "resize_layers.0.bias"], stride=4)
+    elif i == 1:
+        x = F.conv_transpose2d(x, sd[head + "resize_layers.1.weight"], sd[head + "resize_layers.1.bias"], stride=2)
+    elif i == 3:
+        x = _conv(x, sd, head + "resize_layers.3", stride=2, padding=1)
+    return x
+
+
 def _dpt_chunk(layers, sd, head, cfg, img_hw):
     H, W = img_hw
     g = cfg.grid
@@ -346,17 +361,7 @@ def _dpt_chunk(layers, sd, head, cfg, img_hw):
         x = x[:, ps:]
         x = layer_norm(x, sd[head + "norm.weight"], sd[head + "norm.bias"], cfg.ln_eps)
         x = x.permute(0, 2, 1).reshape(x.shape[0], -1, g, g)
-        x = _conv(x, sd, f"{head}projects.{i}", padding=0)
-        x = x + dpt_pos_embed(x.shape[1], g, g, W, H)
-        if i == 0:
-            x = F.conv_transpose2d(x, sd[head + "resize_layers.0.weight"],
-                                   sd[head + "resize_layers.0.bias"], stride=4)
-        elif i == 1:
-            x = F.conv_transpose2d(x, sd[head + "resize_layers.1.weight"],
-                                   sd[head + "resize_layers.1.bias"], stride=2)
-        elif i == 3:
-            x = _conv(x, sd, head + "resize_layers.3", stride=2, padding=1)
-        feats.append(x)
+        feats.append(_reassemble(x, sd, head, i, dpt_pos_embed(cfg.dpt_out_channels[i], g, g, W, H)))
     sc = head + "scratch."
     l1, l2, l3, l4 = [_conv(f, sd, f"{sc}layer{i + 1}_rn") for i, f in enumerate(feats)]
     out = _fusion(sd, sc + "refinenet4", l4, None, size=l3.shape[2:])

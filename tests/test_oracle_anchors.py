@@ -7,11 +7,13 @@ module is installed in this image, the restatement is checked against it on shar
   * DINOv2 ViT/14 with registers (a2'): `transformers` Dinov2WithRegistersModel — token assembly
     (cls + position embedding, registers after cls), pre-norm blocks with LayerScale, final norm;
   * the DPT fusion block (a14): `transformers` DPTFeatureFusionLayer / DPTPreActResidualLayer —
-    pre-activation residual conv units, skip add, x2 bilinear (align_corners=True), 1x1 projection.
+    pre-activation residual conv units, skip add, x2 bilinear (align_corners=True), 1x1 projection;
+  * the DPT reassembly of each kept layer (a14): `transformers` DPTReassembleLayer — 1x1 projection,
+    then ConvTranspose k = s = 4 / 2, identity, or 3x3 stride-2 conv.
 
 These pin the block structure (pre-norm attention / MLP with LayerScale, exact GELU, SDPA scaling)
-and the DPT fusion arithmetic the aggregator and heads share; the VGGT-specific parts (2D RoPE,
-q/k LayerNorm, camera head, DPT reassembly) remain restated, not pinned.
+and the DPT reassembly / fusion arithmetic the aggregator and heads share; the VGGT-specific parts
+(2D RoPE, q/k LayerNorm, camera head, the DPT UV pos-embed) remain restated, not pinned.
 """
 import pytest
 import torch
@@ -99,3 +101,28 @@ def test_dpt_fusion_block_matches_transformers(with_skip):
         want = layer(x0, x1)
         got = R._fusion(sd, name, x0, x1, size=None)
     torch.testing.assert_close(got, want, rtol=1e-5, atol=1e-5)
+
+
+@pytest.mark.parametrize("i,factor", [(0, 4), (1, 2), (2, 1), (3, 0.5)])
+def test_dpt_reassemble_matches_transformers(i, factor):
+    """Projection + resize of kept layer i (VGGT adds a UV pos-embed between them; anchored without it)."""
+    from transformers import DPTConfig
+    from transformers.models.dpt.modeling_dpt import DPTReassembleLayer
+    Cin, Co = 96, 64
+    hc = DPTConfig(hidden_size=Cin)
+    layer = DPTReassembleLayer(hc, channels=Co, factor=factor).eval()
+    g = torch.Generator().manual_seed(10 + i)
+    head = "depth_head."
+    sd = {f"{head}projects.{i}.weight": torch.randn(Co, Cin, 1, 1, generator=g) / 10,
+          f"{head}projects.{i}.bias": torch.randn(Co, generator=g) * 0.1}
+    layer.projection.weight.data.copy_(sd[f"{head}projects.{i}.weight"])
+    layer.projection.bias.data.copy_(sd[f"{head}projects.{i}.bias"])
+    if factor != 1:
+        kshape = (Co, Co, factor, factor) if factor > 1 else (Co, Co, 3, 3)
+        sd[f"{head}resize_layers.{i}.weight"] = torch.randn(*kshape, generator=g) / 20
+        sd[f"{head}resize_layers.{i}.bias"] = torch.randn(Co, generator=g) * 0.1
+        layer.resize.weight.data.copy_(sd[f"{head}resize_layers.{i}.weight"])
+        layer.resize.bias.data.copy_(sd[f"{head}resize_layers.{i}.bias"])
+    x = torch.randn(2, Cin, 9, 9, generator=g)
+    with torch.no_grad():
+        torch.testing.assert_close(R._reassemble(x, sd, head, i), layer(x), rtol=1e-5, atol=1e-5)

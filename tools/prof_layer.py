@@ -26,6 +26,17 @@ if what == "headout":  # DPT output head: 3x3 conv 128 -> 32 on 16 views at 518^
     conf = torch.empty(Fr, Hh, Hh, device="cuda")
     run = lambda: ops.gemm_spatial(x.view(-1, 128), w, b, Fr, Hh, Hh, conv3x3=True,  # noqa: E731
                                    head=(hw, hb, 1, pred, conf))
+elif what == "conv256":  # DPT RCU conv2 at 148^2: 3x3 256 -> 256 + residual, padded + relu'd outputs
+    Fr, Hh, C = 16, 148, 256
+    x = torch.zeros(Fr, Hh + 2, Hh + 2, C, device="cuda", dtype=torch.bfloat16)
+    x[:, 1:-1, 1:-1] = torch.randn(Fr, Hh, Hh, C, device="cuda").to(torch.bfloat16)
+    w = (torch.randn(C, 9 * C, device="cuda") * 0.02).to(torch.bfloat16)
+    b = torch.randn(C, device="cuda")
+    res = x.clone()
+    o1 = torch.zeros_like(x)
+    o2 = torch.zeros_like(x)
+    run = lambda: ops.gemm_spatial(x.view(-1, C), w, b, Fr, Hh, Hh, conv3x3=True, res1=res, res1_pad=True,  # noqa: E731
+                                   out1=o1, out1_pad=True, out2=o2, out2_pad=True)
 elif what.startswith("attn"):
     q, k, v = (torch.randn(H, T, d, device="cuda", dtype=torch.bfloat16) for _ in range(3))
     o = torch.empty(T, H * d, device="cuda", dtype=torch.bfloat16)
