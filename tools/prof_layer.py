@@ -37,6 +37,12 @@ elif what == "conv256":  # DPT RCU conv2 at 148^2: 3x3 256 -> 256 + residual, pa
     o2 = torch.zeros_like(x)
     run = lambda: ops.gemm_spatial(x.view(-1, C), w, b, Fr, Hh, Hh, conv3x3=True, res1=res, res1_pad=True,  # noqa: E731
                                    out1=o1, out1_pad=True, out2=o2, out2_pad=True)
+elif what == "upsample":  # DPT final resize: 296^2 -> 518^2 at C=128 + pos-embed into a padded buffer
+    Fr, h, Hh, C = 16, 296, 518, 128
+    x = torch.randn(Fr, h, h, C, device="cuda").to(torch.bfloat16)
+    add = torch.randn(Hh, Hh, C, device="cuda").to(torch.bfloat16)
+    out = torch.zeros(Fr, Hh + 2, Hh + 2, C, device="cuda", dtype=torch.bfloat16)
+    run = lambda: ops.upsample_bilinear(x, (Hh, Hh), add=add, out=out, out_pad=True)  # noqa: E731
 elif what.startswith("attn"):
     q, k, v = (torch.randn(H, T, d, device="cuda", dtype=torch.bfloat16) for _ in range(3))
     o = torch.empty(T, H * d, device="cuda", dtype=torch.bfloat16)
