@@ -140,7 +140,7 @@ def run_reference(args):
 class ClockSampler:
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+              "clocks_event_reasons.sw_power_cap,memory.used")
 
     def __init__(self, index: int):
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
@@ -157,20 +157,27 @@ class ClockSampler:
         self.p.wait()
         self.f.seek(0)
         rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
-        sm, mx, reasons = [], 0.0, set()
+        sm, mx, reasons, mem, pw = [], 0.0, set(), [], []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for r in rows:
             try:
                 sm.append(float(r[0]))
                 mx = max(mx, float(r[1]))
+                pw.append(float(r[2]))
                 for n, v in zip(names, r[3:7]):
                     if "Active" in v and "Not" not in v:
                         reasons.add(n)
+                mem.append(float(r[7]))
             except (ValueError, IndexError):
                 continue
         if not sm:
             return None
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        out = {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        if pw:
+            out["power_w_median"] = statistics.median(pw)
+        if mem:  # device memory in use (whole process incl. context, NCCL and the allocator's cache), MiB
+            out["memory_used_gb_max"] = round(max(mem) * 1.048576e-3, 2)
+        return out
 
 
 # ---------------------------------------------------------------------------
