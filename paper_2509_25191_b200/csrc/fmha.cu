@@ -55,6 +55,11 @@ struct AttnArgs {
   float* o_acc;
   int64_t ld_acc;
   int q_blocks, kv_tiles, units;
+  // Q tiles are numbered over (head, sequence, 128-row tile) in that order, tps per sequence; unit u
+  // owns tiles [NT*u, NT*u + NT) of total_tiles. tps = q_blocks * NT (units never straddle two
+  // sequences) except for packed frame attention, where tps = ceil(Lq / 128) and a unit may take its
+  // last tiles from the next sequence (then it streams both sequences' K/V)
+  int tps, total_tiles;
   float scale_log2;
   __nv_bfloat16* out;
   int64_t ldo;
@@ -88,8 +93,13 @@ VX_DEVICE WorkItem work_item(const AttnArgs& a, int w) {
 }
 
 template <int D, int NT_ = (D == 128 ? 1 : 2), int BKV_ = 128, bool ALIAS_ = false, bool SUMV_ = false,
-          bool PSM_ = false>
+          bool PSM_ = false, bool PACK_ = false>
 struct AttnCfg {
+  // PACK: a unit's NT Q tiles may come from two consecutive sequences (frame attention, where
+  // 1374 rows = 10.7 tiles would otherwise leave 1.3 of every 12 tile slots empty); every K/V stage
+  // then has a slot per sequence
+  static constexpr bool PACK = PACK_;
+  static constexpr int KV_SLOTS = PACK ? 2 : 1;
   // PSM: P goes to shared memory (one 128 x 64-column SW128 tile per Q tile, K-major like Q) and the
   // PV MMA reads it from there (SS), so TMEM holds only S and O per tile and S_i(j+1) is issued as
   // soon as the softmax has loaded S_i(j), overlapping its exps (not aliased, 4 tiles still fit)
@@ -120,13 +130,16 @@ struct AttnCfg {
   static constexpr int ROWS = 128 * NT;                    // query rows per work unit
   static constexpr uint32_t BAR_BYTES = 512;
   static constexpr uint32_t P_TILE_BYTES = PSM ? 128 * 128 : 0;  // 128 rows x 128 B (BKV <= 64 bf16 used)
+  static constexpr uint32_t K_STAGE_BYTES = KV_SLOTS * KV_TILE_BYTES;   // [K_A | K_B]
+  static constexpr uint32_t VS_STAGE_BYTES = KV_SLOTS * V_STAGE_BYTES;  // [V_A ones | V_B ones]
   static constexpr uint32_t SMEM =
-      NT * (Q_TILE_BYTES + P_TILE_BYTES) + KST * (KV_TILE_BYTES + V_STAGE_BYTES) + 1024 + BAR_BYTES;
+      NT * (Q_TILE_BYTES + P_TILE_BYTES) + KST * (K_STAGE_BYTES + VS_STAGE_BYTES) + 1024 + BAR_BYTES;
   // TMEM columns: S_i [BKV fp32] ... | P_i [BKV/2] (neither ALIAS nor PSM) ... | O_i [DO fp32] ...
   static constexpr uint32_t O_BASE = ((NT * BKV + (ALIAS || PSM ? 0 : NT * BKV / 2)) + 31) / 32 * 32;
   static_assert(O_BASE + NT * DO <= 512, "TMEM budget");
   static_assert(!SUMV || ((ALIAS || PSM) && D == 64), "SUMV is implemented for the d=64 kernels");
   static_assert(!PSM || (D == 64 && BKV <= 64), "PSM: one 128-byte P row per query row");
+  static_assert(!PACK || (ALIAS && !PSM), "PACK is implemented for the aliased kernel");
   static_assert(BKV % 16 == 0 && (BKV <= 64 || BKV % 64 == 0 || (BKV == 96 && ALIAS && D == 64)), "KV tile width");
   static __host__ __device__ constexpr uint32_t tS(int i) { return i * BKV; }
   static __host__ __device__ constexpr uint32_t tP(int i) { return ALIAS ? i * BKV : NT * BKV + i * (BKV / 2); }
@@ -181,12 +194,13 @@ constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
 
 // EMU_PAIRS_OF_8: of every 8 exp pairs, this many use the FMA-pipe polynomial
 template <int D, int EMU_PAIRS_OF_8, int NT_, int BKV_, bool ALIAS_, bool SUMV_, bool NOHINT = false,
-          bool SPEC_ = false, bool LDSPLIT = false, bool PSM_ = false>
-__global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_>::THREADS, 1)
+          bool SPEC_ = false, bool LDSPLIT = false, bool PSM_ = false, bool PACK_ = false>
+__global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PACK_>::THREADS, 1)
     fmha_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                 const __grid_constant__ CUtensorMap tmV, const AttnArgs a) {
-  using Cfg = AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_>;
+  using Cfg = AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PACK_>;
   constexpr bool ALIAS = ALIAS_;
+  constexpr bool PACK = PACK_;
   constexpr bool PSM = PSM_;
   // speculative exps (step_spec) need P writes that can be repeated before p_full: aliased or
   // shared-memory P only
@@ -202,9 +216,9 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_>::TH
   constexpr int NT = Cfg::NT;
   uint8_t* sQ = smem;                                 // NT tiles
   [[maybe_unused]] uint8_t* sP = sQ + NT * Cfg::Q_TILE_BYTES;  // PSM: NT P tiles (1024-aligned)
-  uint8_t* sK = sP + NT * Cfg::P_TILE_BYTES;          // KST tiles
-  uint8_t* sV = sK + KST * Cfg::KV_TILE_BYTES;        // KST stages (V tile [+ ones panel])
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sV + KST * Cfg::V_STAGE_BYTES);
+  uint8_t* sK = sP + NT * Cfg::P_TILE_BYTES;          // KST stages (K tile per slot)
+  uint8_t* sV = sK + KST * Cfg::K_STAGE_BYTES;        // KST stages (V tile [+ ones panel] per slot)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sV + KST * Cfg::VS_STAGE_BYTES);
   uint64_t* q_full = bar;
   uint64_t* q_empty = bar + 1;
   uint64_t* k_full = bar + 2;
@@ -252,8 +266,8 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_>::TH
   if (warp == 2) tmem_alloc(tmem_slot, 512);
   if constexpr (SUMV) {  // the constant ones panel of every V stage (read by the tensor core)
     const uint32_t ones = 0x3f803f80u;  // bf16x2 (1, 1)
-    for (uint32_t o = threadIdx.x * 16; o < KST * Cfg::KVPANEL_BYTES; o += Cfg::THREADS * 16) {
-      const uint32_t st = o / Cfg::KVPANEL_BYTES, off = o % Cfg::KVPANEL_BYTES;
+    for (uint32_t o = threadIdx.x * 16; o < KST * Cfg::KV_SLOTS * Cfg::KVPANEL_BYTES; o += Cfg::THREADS * 16) {
+      const uint32_t st = o / Cfg::KVPANEL_BYTES, off = o % Cfg::KVPANEL_BYTES;  // st: stage x slot
       *reinterpret_cast<uint4*>(sV + st * Cfg::V_STAGE_BYTES + Cfg::KV_TILE_BYTES + off) =
           make_uint4(ones, ones, ones, ones);
     }
@@ -264,7 +278,12 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_>::TH
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  const int per_head = a.nseq * a.q_blocks;
+  // tile t of the (head, sequence, tile) numbering -> sequence g = head * nseq + seq, tile in sequence
+  auto tile_seq = [&](int t, int& qt) -> int {
+    const int g = t / a.tps;
+    qt = t - g * a.tps;
+    return g;
+  };
 
   // the n-th work item of this CTA is published by the producer through wq[n % WQ]: the first is
   // blockIdx.x, later ones come from the launch's atomic ticket counter, so a CTA that started late
@@ -295,31 +314,43 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_>::TH
         }
         if (w >= a.work) break;
         const WorkItem wi = work_item(a, w);
-        const int u = wi.u;
-        const int h = u / per_head;
-        const int rem = u - h * per_head;
-        const int s = rem / a.q_blocks;
-        const int qb = rem - s * a.q_blocks;
-        const int q_row = int(h * a.Tq + (int64_t)s * a.Lq + qb * Cfg::ROWS);
-        const int kv_row = int(h * a.Tk + (int64_t)s * a.Lk);
+        const int t0 = wi.u * NT;
+        int qt0;
+        const int gA = tile_seq(t0, qt0);
+        const int last = (t0 + NT <= a.total_tiles ? t0 + NT : a.total_tiles) - 1;
+        int qtl;
+        const int nslot = PACK && tile_seq(last, qtl) != gA ? 2 : 1;  // K/V of one or two sequences
+        int kv_row[2];
+        for (int b = 0; b < nslot; ++b) {
+          const int hb = (gA + b) / a.nseq;
+          kv_row[b] = int(hb * a.Tk + (int64_t)(gA + b - hb * a.nseq) * a.Lk);
+        }
         mbar_wait(q_empty, (n & 1) ^ 1);
         mbar_expect_tx(q_full, NT * Cfg::Q_TILE_BYTES);
-        for (int i = 0; i < NT; ++i)
+        for (int i = 0; i < NT; ++i) {
+          int qt;
+          const int g = tile_seq(t0 + i, qt);
+          const int hq = g / a.nseq;
+          // tiles past the last one (packed, final unit only) load any rows; their output is dropped
+          const int q_row = t0 + i < a.total_tiles ? int(hq * a.Tq + (int64_t)(g - hq * a.nseq) * a.Lq + qt * 128) : 0;
           for (int pn = 0; pn < Cfg::PANELS; ++pn)
             tma_load_2d_hint(sQ + i * Cfg::Q_TILE_BYTES + pn * Cfg::QPANEL_BYTES, &tmQ, q_full,
-                             pn * Cfg::PANEL_COLS, q_row + 128 * i, pol_q);
+                             pn * Cfg::PANEL_COLS, q_row, pol_q);
+        }
         for (int j = wi.j0; j < wi.j0 + wi.cnt; ++j, ++c) {
           const uint32_t st = c % KST, ph = (c / KST) & 1;
           mbar_wait(&k_empty[st], ph ^ 1);
-          mbar_expect_tx(&k_full[st], Cfg::KV_TILE_BYTES);
-          for (int pn = 0; pn < Cfg::PANELS; ++pn)
-            tma_load_2d_hint(sK + st * Cfg::KV_TILE_BYTES + pn * Cfg::KVPANEL_BYTES, &tmK, &k_full[st],
-                             pn * Cfg::PANEL_COLS, kv_row + BKV * j, pol_kv);
+          mbar_expect_tx(&k_full[st], nslot * Cfg::KV_TILE_BYTES);
+          for (int b = 0; b < nslot; ++b)
+            for (int pn = 0; pn < Cfg::PANELS; ++pn)
+              tma_load_2d_hint(sK + st * Cfg::K_STAGE_BYTES + b * Cfg::KV_TILE_BYTES + pn * Cfg::KVPANEL_BYTES, &tmK,
+                               &k_full[st], pn * Cfg::PANEL_COLS, kv_row[b] + BKV * j, pol_kv);
           mbar_wait(&v_empty[st], ph ^ 1);
-          mbar_expect_tx(&v_full[st], Cfg::KV_TILE_BYTES);
-          for (int pn = 0; pn < Cfg::PANELS; ++pn)
-            tma_load_2d_hint(sV + st * Cfg::V_STAGE_BYTES + pn * Cfg::KVPANEL_BYTES, &tmV, &v_full[st],
-                             pn * Cfg::PANEL_COLS, kv_row + BKV * j, pol_kv);
+          mbar_expect_tx(&v_full[st], nslot * Cfg::KV_TILE_BYTES);
+          for (int b = 0; b < nslot; ++b)
+            for (int pn = 0; pn < Cfg::PANELS; ++pn)
+              tma_load_2d_hint(sV + st * Cfg::VS_STAGE_BYTES + b * Cfg::V_STAGE_BYTES + pn * Cfg::KVPANEL_BYTES, &tmV,
+                               &v_full[st], pn * Cfg::PANEL_COLS, kv_row[b] + BKV * j, pol_kv);
         }
       }
     }
@@ -367,16 +398,27 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_>::TH
         for (;; ++n) {
           const int w = wq_take(n);
           if (w >= a.work) break;
-          const int nkv = work_item(a, w).cnt;
+          const WorkItem wi = work_item(a, w);
+          const int nkv = wi.cnt;
+          // PACK: bit i = Q tile i belongs to the unit's second sequence (K/V slot B of every stage)
+          uint32_t bmask = 0;
+          if constexpr (PACK) {
+            int qt;
+            const int gA = tile_seq(wi.u * NT, qt);
+            for (int i = 1; i < NT; ++i)
+              if (wi.u * NT + i < a.total_tiles && tile_seq(wi.u * NT + i, qt) != gA) bmask |= 1u << i;
+          }
+          auto koff = [&](int i) -> uint32_t { return PACK && ((bmask >> i) & 1) ? Cfg::KV_TILE_BYTES : 0; };
+          auto voff = [&](int i) -> uint32_t { return PACK && ((bmask >> i) & 1) ? Cfg::V_STAGE_BYTES : 0; };
           mbar_wait(q_full, n & 1);
           tc_fence_after();
           {  // S(0): the previous unit's P / S columns were consumed by its last PVs (in order)
             const uint32_t st = c % KST, ph = (c / KST) & 1;
             mbar_wait(&k_full[st], ph);
             tc_fence_after();
-            const uint32_t ks = smem_u32(sK + st * Cfg::KV_TILE_BYTES);
+            const uint32_t ks = smem_u32(sK + st * Cfg::K_STAGE_BYTES);
             for (int i = 0; i < NT; ++i) {
-              issue_qk(i, ks);
+              issue_qk(i, ks + koff(i));
               mma_commit_if(lead, &s_full[i]);
             }
             mma_commit_if(lead, &k_empty[st]);
@@ -386,8 +428,8 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_>::TH
             const uint32_t st = c % KST, ph = (c / KST) & 1;
             const bool has_next = j + 1 < nkv;
             const uint32_t nst = (c + 1) % KST, nph = ((c + 1) / KST) & 1;
-            const uint32_t vs = smem_u32(sV + st * Cfg::V_STAGE_BYTES);
-            const uint32_t nks = smem_u32(sK + nst * Cfg::KV_TILE_BYTES);
+            const uint32_t vs = smem_u32(sV + st * Cfg::VS_STAGE_BYTES);
+            const uint32_t nks = smem_u32(sK + nst * Cfg::K_STAGE_BYTES);
             mbar_wait(&v_full[st], ph);
             if (has_next) mbar_wait(&k_full[nst], nph);
             for (int i = 0; i < NT; ++i) {
@@ -399,10 +441,10 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_>::TH
               if (j == 0) mbar_wait(&o_empty[i], (n & 1) ^ 1);
               VX_TRACE(trace_slot_mma(int(n), j, i, 0));
               tc_fence_after();
-              issue_pv(i, vs, j > 0);
+              issue_pv(i, vs + voff(i), j > 0);
               // S_i(j+1) overwrites P_i(j): executes after PV_i(j) (tcgen05 issue order). Predicated
               // rather than branched, so the issue path has no branch.
-              issue_qk(i, nks, has_next);
+              issue_qk(i, nks + koff(i), has_next);
               mma_commit_if(lead && has_next, &s_full[i]);
               mma_commit_if(lead && !has_next, &p_free[i]);  // last PV of the unit
               VX_TRACE(trace_slot_mma(int(n), j, i, 1));
@@ -426,7 +468,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_>::TH
             const uint32_t st = c % KST, ph = (c / KST) & 1;
             mbar_wait(&k_full[st], ph);
             tc_fence_after();
-            const uint32_t ks = smem_u32(sK + st * Cfg::KV_TILE_BYTES);
+            const uint32_t ks = smem_u32(sK + st * Cfg::K_STAGE_BYTES);
             for (int i = 0; i < NT; ++i) {
               if (n > 0) mbar_wait(&s_free[i], sfree_ph);
               tc_fence_after();
@@ -442,7 +484,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_>::TH
             if (j + 1 < nkv) {  // run one KV tile ahead: S(j+1) as soon as S(j) has been loaded
               const uint32_t nst = (c + 1) % KST, nph = ((c + 1) / KST) & 1;
               mbar_wait(&k_full[nst], nph);
-              const uint32_t nks = smem_u32(sK + nst * Cfg::KV_TILE_BYTES);
+              const uint32_t nks = smem_u32(sK + nst * Cfg::K_STAGE_BYTES);
               for (int i = 0; i < NT; ++i) {
                 mbar_wait(&s_free[i], sfree_ph);
                 tc_fence_after();
@@ -453,7 +495,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_>::TH
               mma_commit_if(lead, &k_empty[nst]);
               mma_commit_if(lead && j + 2 == nkv, q_empty);
             }
-            const uint32_t vs = smem_u32(sV + st * Cfg::V_STAGE_BYTES);
+            const uint32_t vs = smem_u32(sV + st * Cfg::VS_STAGE_BYTES);
             mbar_wait(&v_full[st], ph);
             for (int i = 0; i < NT; ++i) {
               mbar_wait(&p_full[i], pfull_ph);
@@ -486,12 +528,13 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_>::TH
       if (w >= a.work) break;
       const WorkItem wi = work_item(a, w);
       const int nkv = wi.cnt;
-      const int u = wi.u;
-      const int h = u / per_head;
-      const int rem = u - h * per_head;
-      const int s = rem / a.q_blocks;
-      const int qb = rem - s * a.q_blocks;
-      const int q_local = qb * Cfg::ROWS + tile * 128 + r;
+      const int t = wi.u * NT + tile;
+      int qt;
+      const int g = tile_seq(t, qt);
+      const int h = g / a.nseq;
+      const int s = g - h * a.nseq;
+      const int q_local = qt * 128 + r;
+      const bool row_valid = t < a.total_tiles && q_local < a.Lq;
       float m_run = -INFINITY;
       float l_run = 0.f;
       for (int j = 0; j < nkv; ++j) {
@@ -810,7 +853,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_>::TH
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&o_empty[tile]);
-      if (q_local < a.Lq) {
+      if (row_valid) {
         const float inv = 1.0f / l_run;
         const int64_t orow = (int64_t)s * a.Lq + q_local;
         const float lse_new = (m_run + __log2f(l_run)) * 0.69314718055994531f;
@@ -1012,9 +1055,9 @@ static unsigned* sched_counters(cudaStream_t st) {
 }
 
 template <int D, int EMU, int NT = (D == 128 ? 1 : 2), int BKV = 128, bool ALIAS = false, bool SUMV = false,
-          bool NOHINT = false, bool SPEC = false, bool LDSPLIT = false, bool PSM = false>
+          bool NOHINT = false, bool SPEC = false, bool LDSPLIT = false, bool PSM = false, bool PACK = false>
 static int launch_fmha(const void* q, const void* k, const void* v, AttnArgs args, cudaStream_t st) {
-  using Cfg = AttnCfg<D, NT, BKV, ALIAS, SUMV, PSM>;
+  using Cfg = AttnCfg<D, NT, BKV, ALIAS, SUMV, PSM, PACK>;
   CUtensorMap tq, tk, tv;
   constexpr int PC = Cfg::PANEL_COLS;
   if (!make_tmap_2d_bf16(&tq, q, (uint64_t)args.H * args.Tq, D, D, 128, PC, Cfg::SWIZZLE)) return VX_E_ARG;
@@ -1022,7 +1065,10 @@ static int launch_fmha(const void* q, const void* k, const void* v, AttnArgs arg
   if (!make_tmap_2d_bf16(&tv, v, (uint64_t)args.H * args.Tk, D, D, BKV, PC, Cfg::SWIZZLE)) return VX_E_ARG;
   args.q_blocks = (args.Lq + Cfg::ROWS - 1) / Cfg::ROWS;
   args.kv_tiles = (args.Lk + BKV - 1) / BKV;
-  args.units = args.H * args.nseq * args.q_blocks;
+  args.tps = PACK ? (args.Lq + 127) / 128 : args.q_blocks * NT;
+  if (PACK && (args.tps < NT || args.merge != 0)) return VX_E_ARG;  // a unit spans at most two sequences
+  args.total_tiles = args.H * args.nseq * args.tps;
+  args.units = (args.total_tiles + NT - 1) / NT;
   // KV-split tail: when the last wave of units would leave more than half the SMs idle, split each
   // of its units over `parts` CTAs (contiguous KV ranges) and merge the partials afterwards
   const int sms = num_sms();
@@ -1039,7 +1085,7 @@ static int launch_fmha(const void* q, const void* k, const void* v, AttnArgs arg
 #endif
   // only for long units: each split costs a merge launch and fp32 partial round trips, which a
   // frame-attention unit (29 KV tiles) does not earn back (S=20 frame layer 0.215 -> 0.228 ms)
-  if (split_on && tail > 0 && 2 * tail <= sms && args.kv_tiles >= 128) {
+  if (split_on && !PACK && tail > 0 && 2 * tail <= sms && args.kv_tiles >= 128) {
     int parts = sms / tail;
     if (parts > args.kv_tiles / 2) parts = args.kv_tiles / 2;  // >= 2 KV tiles per item
     if (parts >= 2 && (int64_t)parts * args.kv_tiles < (1ll << 31)) {
@@ -1053,7 +1099,7 @@ static int launch_fmha(const void* q, const void* k, const void* v, AttnArgs arg
     }
   }
   args.work = args.split_from + (args.units - args.split_from) * args.parts;
-  auto kern = fmha_kernel<D, EMU, NT, BKV, ALIAS, SUMV, NOHINT, SPEC, LDSPLIT, PSM>;
+  auto kern = fmha_kernel<D, EMU, NT, BKV, ALIAS, SUMV, NOHINT, SPEC, LDSPLIT, PSM, PACK>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
@@ -1141,6 +1187,19 @@ static int attention_impl(const void* q, const void* k, const void* v, void* out
 #elif VX_FMHA_W96
     return launch_fmha<64, 2, 3, 96, true, true, true, true, false>(q, k, v, a, st);
 #else
+    // frame attention (several sequences whose 128-row tile count is not a multiple of 4, e.g. 1374
+    // rows = 11 tiles): units of 4 consecutive tiles across sequence boundaries
+    const int tps = (Lq + 127) / 128;
+#ifdef VX_DIAG
+    static const bool pack_on = [] {
+      const char* e = getenv("VX_FMHA_PACK");  // diagnostic build only: 0 = one sequence per unit
+      return !(e && atoi(e) == 0);
+    }();
+#else
+    constexpr bool pack_on = true;
+#endif
+    if (pack_on && merge == 0 && nseq > 1 && tps >= 4 && tps % 4 != 0)
+      return launch_fmha<64, 2, 4, 48, true, true, true, true, true, false, true>(q, k, v, a, st);
     return launch_fmha<64, 2, 4, 48, true, true, true, true, true>(q, k, v, a, st);
 #endif
   }

@@ -151,8 +151,15 @@ def _sdpa_ref(q, k, v, nseq, Lq, Lk):
                                         (64, 2, 2, 4099), (64, 1, 1, 8192),
                                         # > 148 work units: CTAs run several units (unit hand-offs)
                                         (64, 16, 12, 1374), (64, 16, 1, 6000),
-                                        # KV-split tail across sequences: 26 units of 130 KV tiles
-                                        (64, 1, 2, 6200), (64, 3, 3, 6200)])
+                                        # packed units (tiles per sequence not a multiple of 4; 6200: 49 tiles)
+                                        (64, 1, 2, 6200), (64, 3, 3, 6200),
+                                        # packed, last unit with tiles past the end (15 / 110 / 21 / 133 tiles)
+                                        (64, 1, 3, 600), (64, 2, 5, 1374), (64, 3, 7, 700), (64, 7, 2, 1100),
+                                        # packed, 5 tiles per sequence: units straddle sequence and head boundaries
+                                        (64, 3, 2, 513), (64, 4, 9, 520),
+                                        # KV-split tail across sequences (48 tiles per sequence, not packed): 24
+                                        # units of 128 KV tiles
+                                        (64, 1, 2, 6144)])
 def test_attention_matches_sdpa(ops, D, H, nseq, L):
     T = nseq * L
     q = _bf(H, T, D, seed=20)
