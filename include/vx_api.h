@@ -75,6 +75,8 @@ typedef struct vx_epilogue {
   int patch_start;            /* 1 + registers */
   int grid_w;                 /* patches per image row */
   float eps;                  /* q/k LayerNorm eps */
+  float q_scale;              /* VX_EPI_QKV: q is multiplied by this before its bf16 store (0 = 1); the
+                                 aggregator stores q * log2(e)/sqrt(head_dim) for VX_ATTN_Q_LOG2 */
 } vx_epilogue;
 
 /* D[M,N] = A[M,K] (bf16, row stride lda) . B[N,K]^T (bf16, row stride ldb) with
@@ -108,6 +110,14 @@ int vx_attention(const void* q, const void* k, const void* v, void* out, int64_t
 int vx_attention_merge(const void* q, const void* k, const void* v, int mode, float* o_acc, int64_t ld_acc,
                        float* lse_acc, void* out, int64_t ldo, int D, int H, int nseq, int Lq, int Lk,
                        int64_t Tq, int64_t Tk, void* stream);
+/* Both of the above with flags: mode 0 = vx_attention (out, optional lse in lse_acc), 1-3 =
+ * vx_attention_merge.  VX_ATTN_Q_LOG2: q already holds q * log2(e)/sqrt(D) (the qkv epilogue's
+ * q_scale), so the scores come out of the MMA in log2 units and the softmax skips one multiply per
+ * score; results (out, natural-log lse) mean the same as without the flag. */
+enum { VX_ATTN_Q_LOG2 = 1 };
+int vx_attention_ex(const void* q, const void* k, const void* v, int mode, float* o_acc, int64_t ld_acc,
+                    float* lse_acc, void* out, int64_t ldo, int D, int H, int nseq, int Lq, int Lk, int64_t Tq,
+                    int64_t Tk, int flags, void* stream);
 
 /* Camera head, fp32 parts ("bf16 except MLP in heads").
  * vx_linear_f32: out[M, N] = epi(X[M, K] . W[N, K]^T + bias), fp32 SIMT (X row stride ldx; ldx = 0

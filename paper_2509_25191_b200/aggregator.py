@@ -99,10 +99,14 @@ class Workspace:
     v: torch.Tensor
     o: torch.Tensor
     h: torch.Tensor
+    # q stored pre-scaled by log2(e)/sqrt(d) (the qkv epilogue's q_scale) and attention told so
+    # (ops.attention(..., q_log2=True)): the FMHA then reads scores in log2 units directly. A global
+    # attention hook receives q in this form.
+    q_log2: bool = True
 
 
 def alloc_workspace(cfg: VGGTConfig, S: int, device="cuda", rows_per_head: Optional[int] = None,
-                    kv: Optional[tuple] = None) -> Workspace:
+                    kv: Optional[tuple] = None, q_log2: bool = True) -> Workspace:
     """Per-forward buffers for S views.  `rows_per_head` (>= S * tokens_per_frame) is the per-head row
     stride of q/k/v; `kv` = (k, v) [H, rows_per_head, d] supplied by the frame-sharded ring (its send
     buffer: the QKV epilogue then writes the local K/V where the first ring step sends them from)."""
@@ -124,6 +128,7 @@ def alloc_workspace(cfg: VGGTConfig, S: int, device="cuda", rows_per_head: Optio
         v=kv[1],
         o=torch.empty(T, C, device=device, dtype=torch.bfloat16),
         h=torch.empty(chunk_rows, cfg.mlp_hidden, device=device, dtype=torch.bfloat16),
+        q_log2=q_log2,
     )
 
 
@@ -152,16 +157,17 @@ def run_block(W: DeviceWeights, name: str, ws: Workspace, S: int, frame_attn: bo
                          rope=W.rope, tokens_per_frame=N, patch_start=cfg.patch_start_idx, grid_w=cfg.grid,
                          eps=cfg.ln_eps)
         ops.gemm(ws.xn, W[name + ".attn.qkv.weight"], ops.EPI_QKV, bias=W[name + ".attn.qkv.bias"],
-                 qkv=(ws.q, ws.k, ws.v), head_dim=cfg.head_dim, tokens_total=ws.q.shape[1], **extra)
+                 qkv=(ws.q, ws.k, ws.v), head_dim=cfg.head_dim, tokens_total=ws.q.shape[1],
+                 q_scale=ops.Q_LOG2_SCALE(cfg.head_dim) if ws.q_log2 else 0.0, **extra)
     if frame_attn:
         with phase("attn_frame"):
-            ops.attention(ws.q, ws.k, ws.v, ws.o, nseq=S, Lq=N, Lk=N)
+            ops.attention(ws.q, ws.k, ws.v, ws.o, nseq=S, Lq=N, Lk=N, q_log2=ws.q_log2)
     elif global_attn is not None:
         with phase("attn_global"):
             global_attn(ws.q, ws.k, ws.v, ws.o)
     else:
         with phase("attn_global"):
-            ops.attention(ws.q, ws.k, ws.v, ws.o, nseq=1, Lq=T, Lk=T)
+            ops.attention(ws.q, ws.k, ws.v, ws.o, nseq=1, Lq=T, Lk=T, q_log2=ws.q_log2)
     with phase("gemm_proj"):
         ops.gemm(ws.o, W[name + ".attn.proj.weight"], ops.EPI_RESID, bias=W[name + ".attn.proj.bias"],
                  resid=ws.x, gamma=W[name + ".ls1.gamma"])

@@ -43,6 +43,9 @@
 #ifndef VX_FMHA_W96
 #define VX_FMHA_W96 0
 #endif
+#ifndef VX_FMHA_NOMAX_EMU  // exp pairs (of 8) on the FMA pipe in the max-free kernel
+#define VX_FMHA_NOMAX_EMU 2
+#endif
 
 namespace vx {
 
@@ -74,6 +77,11 @@ struct AttnArgs {
   // finished (the last one resets both, so the counters are zero again for the next launch on the
   // stream); nullptr = static round-robin (while a stream is being captured before the counters exist)
   unsigned* sched;
+  // max-free launches (NOMAX kernel): bad[0] is set when a row's result is not trustworthy (P or O
+  // out of range); the exact kernel then runs as a fixup (fixup = 1): it exits at once unless bad[0]
+  // is set, otherwise recomputes the whole launch, and its last CTA clears bad[0] (bad[1] counts them)
+  unsigned* bad;
+  int fixup;
 };
 
 // work-item queue depth (shared-memory ring from the TMA producer to the MMA and softmax warps)
@@ -194,13 +202,22 @@ constexpr float RESCALE_THRESHOLD = 8.0f;  // log2 units
 
 // EMU_PAIRS_OF_8: of every 8 exp pairs, this many use the FMA-pipe polynomial
 template <int D, int EMU_PAIRS_OF_8, int NT_, int BKV_, bool ALIAS_, bool SUMV_, bool NOHINT = false,
-          bool SPEC_ = false, bool LDSPLIT = false, bool PSM_ = false, bool PACK_ = false>
+          bool SPEC_ = false, bool LDSPLIT = false, bool PSM_ = false, bool PACK_ = false, bool NOMAX_ = false,
+          bool QL2_ = false>
 __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PACK_>::THREADS, 1)
     fmha_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                 const __grid_constant__ CUtensorMap tmV, const AttnArgs a) {
+  // fixup launch after a max-free one: nothing to do unless some row was flagged
+  if (a.fixup && *reinterpret_cast<volatile unsigned*>(a.bad) == 0u) return;
   using Cfg = AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PACK_>;
   constexpr bool ALIAS = ALIAS_;
   constexpr bool PACK = PACK_;
+  // NOMAX: no running max at all — P = 2^(s * scale * log2e) with m = 0 (no row max, no vote, no
+  // rescale; the first tile of a unit is no longer special). Exact whenever no P or O leaves the fp32
+  // range, which the epilogue checks per row; a flagged launch is recomputed by the exact kernel.
+  constexpr bool NOMAX = NOMAX_;
+  constexpr bool QL2 = QL2_ && NOMAX_;  // (the exact kernel uses scale_log2 = 1 for pre-scaled q)
+  static_assert(!NOMAX || (ALIAS_ && SUMV_ && BKV_ == 48 && !PSM_), "NOMAX is implemented for the 4 x 48 aliased kernel");
   constexpr bool PSM = PSM_;
   // speculative exps (step_spec) need P writes that can be repeated before p_full: aliased or
   // shared-memory P only
@@ -535,7 +552,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PAC
       const int s = g - h * a.nseq;
       const int q_local = qt * 128 + r;
       const bool row_valid = t < a.total_tiles && q_local < a.Lq;
-      float m_run = -INFINITY;
+      float m_run = NOMAX ? 0.f : -INFINITY;
       float l_run = 0.f;
       for (int j = 0; j < nkv; ++j) {
         VX_TRACE(trace_slot_sm(unit_n, wl, lane, tile, j, 0));
@@ -671,7 +688,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PAC
         // only need columns 0-31, and the wait for the rest sits just before pair 16
         // (not with PSM: s_free is arrived right after the S load so S(j+1) can be issued into it)
         constexpr bool SPLIT_LD = SPEC && LDSPLIT && BKV == 48 && !PSM;
-        const bool spec_now = SPEC && j > 0 && valid >= BKV;
+        const bool spec_now = (SPEC && j > 0 && valid >= BKV) || (NOMAX && valid >= BKV);
         if (SPLIT_LD && spec_now) {
           tmem_ld32(S_addr, sr);
           tmem_wait_ld();
@@ -733,7 +750,9 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PAC
                 if (c == 16) tmem_wait_ld_dep16(sr + 32);
               }
               const int e = 64 * hf + 2 * c;
-              const uint64_t x = f2_fma(f2_pack(__uint_as_float(sr[e]), __uint_as_float(sr[e + 1])), SL2, NEGM);
+              // QL2 (max-free, q pre-scaled by log2(e)/sqrt(d)): the score already is the exponent
+              const uint64_t x = QL2 ? f2_pack(__uint_as_float(sr[e]), __uint_as_float(sr[e + 1]))
+                                     : f2_fma(f2_pack(__uint_as_float(sr[e]), __uint_as_float(sr[e + 1])), SL2, NEGM);
               float x0, x1, p0, p1;
               f2_unpack(x, x0, x1);
               if ((c & 7) >= 8 - EMU_PAIRS_OF_8) {
@@ -832,9 +851,22 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PAC
             row_sums(1.0f);
           }
         };
-        if (valid < BKV) step(BoolTag<true>{});
-        else if (spec_now) step_spec();
-        else step(BoolTag<false>{});
+        if constexpr (NOMAX) {
+          if (valid < BKV) {
+#pragma unroll
+            for (int c = 0; c < BKV; ++c)
+              if (c >= valid) sr[c] = 0xff800000u;
+            exps(f2_pack(0.f, 0.f), BoolTag<false>{});
+          } else {
+            exps(f2_pack(0.f, 0.f), BoolTag<SPLIT_LD>{});
+          }
+        } else if (valid < BKV) {
+          step(BoolTag<true>{});
+        } else if (spec_now) {
+          step_spec();
+        } else {
+          step(BoolTag<false>{});
+        }
         tmem_wait_st();
         if constexpr (PSM) fence_proxy_async_smem();  // P stores visible to the tensor core's async proxy
         tc_fence_before();
@@ -850,6 +882,14 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PAC
       tmem_ld_n<DL>(O_addr, orr);
       tmem_wait_ld();
       if constexpr (SUMV) l_run = __uint_as_float(orr[D]);  // sum_k P_ik from the ones panel
+      if constexpr (NOMAX) {
+        // trustworthy iff the row sum is well inside the normal fp32 range and O is finite (O <= l max|v|)
+        float chk = 0.f;
+#pragma unroll
+        for (int c = 0; c < D; ++c) chk += __uint_as_float(orr[c]);
+        const bool bad = row_valid && !(l_run > 1e-30f && l_run < 1e30f && fabsf(chk) < 3.0e38f);
+        if (__any_sync(0xffffffff, bad) && lane == 0) atomicOr(a.bad, 1u);
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&o_empty[tile]);
@@ -922,6 +962,13 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PAC
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
+  }
+  if (a.fixup && threadIdx.x == 0) {  // a fixup that ran: the last CTA clears the flag for the next launch
+    __threadfence();
+    if (atomicAdd(a.bad + 1, 1u) == gridDim.x - 1) {
+      atomicExch(a.bad, 0u);
+      atomicExch(a.bad + 1, 0u);
+    }
   }
   if (a.sched && threadIdx.x == 0) {  // every ticket of this CTA is taken: the last CTA resets the counters
     __threadfence();
@@ -1045,8 +1092,8 @@ static unsigned* sched_counters(cudaStream_t st) {
   if (it != ctrs.end()) return it->second;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
-  unsigned* p = nullptr;
-  if (cudaMalloc(&p, 2 * sizeof(unsigned)) != cudaSuccess || cudaMemset(p, 0, 2 * sizeof(unsigned)) != cudaSuccess) {
+  unsigned* p = nullptr;  // [ticket, CTAs done, bad flag, fixup CTAs done]
+  if (cudaMalloc(&p, 4 * sizeof(unsigned)) != cudaSuccess || cudaMemset(p, 0, 4 * sizeof(unsigned)) != cudaSuccess) {
     cudaGetLastError();
     return nullptr;
   }
@@ -1055,7 +1102,8 @@ static unsigned* sched_counters(cudaStream_t st) {
 }
 
 template <int D, int EMU, int NT = (D == 128 ? 1 : 2), int BKV = 128, bool ALIAS = false, bool SUMV = false,
-          bool NOHINT = false, bool SPEC = false, bool LDSPLIT = false, bool PSM = false, bool PACK = false>
+          bool NOHINT = false, bool SPEC = false, bool LDSPLIT = false, bool PSM = false, bool PACK = false,
+          bool NOMAX = false, bool QL2 = false>
 static int launch_fmha(const void* q, const void* k, const void* v, AttnArgs args, cudaStream_t st) {
   using Cfg = AttnCfg<D, NT, BKV, ALIAS, SUMV, PSM, PACK>;
   CUtensorMap tq, tk, tv;
@@ -1099,7 +1147,7 @@ static int launch_fmha(const void* q, const void* k, const void* v, AttnArgs arg
     }
   }
   args.work = args.split_from + (args.units - args.split_from) * args.parts;
-  auto kern = fmha_kernel<D, EMU, NT, BKV, ALIAS, SUMV, NOHINT, SPEC, LDSPLIT, PSM, PACK>;
+  auto kern = fmha_kernel<D, EMU, NT, BKV, ALIAS, SUMV, NOHINT, SPEC, LDSPLIT, PSM, PACK, NOMAX, QL2>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
@@ -1120,7 +1168,7 @@ static int launch_fmha(const void* q, const void* k, const void* v, AttnArgs arg
 
 static int attention_impl(const void* q, const void* k, const void* v, void* out, int64_t ldo, float* lse, int D,
                           int H, int nseq, int Lq, int Lk, int64_t Tq, int64_t Tk, int merge, float* o_acc,
-                          int64_t ld_acc, void* stream) {
+                          int64_t ld_acc, int flags, void* stream) {
   VX_CHECK_ARG(q && k && v, "vx_attention: null pointer");
   VX_CHECK_ARG(merge == 1 || merge == 2 || out, "vx_attention: null out");
   VX_CHECK_ARG(D == 32 || D == 64 || D == 128, "vx_attention: head_dim %d unsupported (32, 64, 128)", D);
@@ -1142,7 +1190,8 @@ static int attention_impl(const void* q, const void* k, const void* v, void* out
   a.o_acc = o_acc;
   a.ld_acc = ld_acc;
   // q_blocks / kv_tiles / units depend on the kernel configuration: set in launch_fmha
-  a.scale_log2 = (1.0f / sqrtf(float(D))) * 1.4426950408889634f;
+  const bool q_log2 = (flags & VX_ATTN_Q_LOG2) != 0;
+  a.scale_log2 = q_log2 ? 1.0f : (1.0f / sqrtf(float(D))) * 1.4426950408889634f;
   a.out = reinterpret_cast<__nv_bfloat16*>(out);
   a.ldo = ldo;
   a.lse = lse;
@@ -1198,8 +1247,25 @@ static int attention_impl(const void* q, const void* k, const void* v, void* out
 #else
     constexpr bool pack_on = true;
 #endif
-    if (pack_on && merge == 0 && nseq > 1 && tps >= 4 && tps % 4 != 0)
-      return launch_fmha<64, 2, 4, 48, true, true, true, true, true, false, true>(q, k, v, a, st);
+    const bool pack = pack_on && merge == 0 && nseq > 1 && tps >= 4 && tps % 4 != 0;
+    // plain launches run max-free first (NOMAX) and then the exact kernel as a fixup that exits at once
+    // unless a row was flagged; ring-merge steps (in-place accumulation) and stream capture (no flag
+    // storage) run the exact kernel only
+    unsigned* flag = merge == 0 ? sched_counters(st) : nullptr;
+    if (flag) {
+      a.bad = flag + 2;
+      constexpr int E = VX_FMHA_NOMAX_EMU;
+      int e;
+      if (q_log2)
+        e = pack ? launch_fmha<64, E, 4, 48, true, true, true, true, true, false, true, true, true>(q, k, v, a, st)
+                 : launch_fmha<64, E, 4, 48, true, true, true, true, true, false, false, true, true>(q, k, v, a, st);
+      else
+        e = pack ? launch_fmha<64, E, 4, 48, true, true, true, true, true, false, true, true>(q, k, v, a, st)
+                 : launch_fmha<64, E, 4, 48, true, true, true, true, true, false, false, true>(q, k, v, a, st);
+      if (e != VX_OK) return e;
+      a.fixup = 1;
+    }
+    if (pack) return launch_fmha<64, 2, 4, 48, true, true, true, true, true, false, true>(q, k, v, a, st);
     return launch_fmha<64, 2, 4, 48, true, true, true, true, true>(q, k, v, a, st);
 #endif
   }
@@ -1211,7 +1277,7 @@ static int attention_impl(const void* q, const void* k, const void* v, void* out
 
 extern "C" int vx_attention(const void* q, const void* k, const void* v, void* out, int64_t ldo, float* lse, int D,
                             int H, int nseq, int Lq, int Lk, int64_t Tq, int64_t Tk, void* stream) {
-  return vx::attention_impl(q, k, v, out, ldo, lse, D, H, nseq, Lq, Lk, Tq, Tk, 0, nullptr, 0, stream);
+  return vx::attention_impl(q, k, v, out, ldo, lse, D, H, nseq, Lq, Lk, Tq, Tk, 0, nullptr, 0, 0, stream);
 }
 
 extern "C" int vx_attention_merge(const void* q, const void* k, const void* v, int mode, float* o_acc, int64_t ld_acc,
@@ -1219,7 +1285,16 @@ extern "C" int vx_attention_merge(const void* q, const void* k, const void* v, i
                                   int64_t Tq, int64_t Tk, void* stream) {
   VX_CHECK_ARG(mode >= 1 && mode <= 3, "vx_attention_merge: mode must be 1 (first), 2 (merge) or 3 (final)");
   return vx::attention_impl(q, k, v, mode == 3 ? out : nullptr, ldo, lse_acc, D, H, nseq, Lq, Lk, Tq, Tk, mode, o_acc,
-                            ld_acc, stream);
+                            ld_acc, 0, stream);
+}
+
+extern "C" int vx_attention_ex(const void* q, const void* k, const void* v, int mode, float* o_acc, int64_t ld_acc,
+                               float* lse_acc, void* out, int64_t ldo, int D, int H, int nseq, int Lq, int Lk,
+                               int64_t Tq, int64_t Tk, int flags, void* stream) {
+  VX_CHECK_ARG(mode >= 0 && mode <= 3, "vx_attention_ex: mode must be 0 (plain) or 1-3 (ring merge)");
+  VX_CHECK_ARG((flags & ~VX_ATTN_Q_LOG2) == 0, "vx_attention_ex: unknown flags 0x%x", flags);
+  return vx::attention_impl(q, k, v, mode == 1 || mode == 2 ? nullptr : out, ldo, lse_acc, D, H, nseq, Lq, Lk, Tq, Tk,
+                            mode, o_acc, ld_acc, flags, stream);
 }
 
 #ifdef VX_FMHA_TRACE

@@ -215,6 +215,10 @@ VX_DEVICE void epi_qkv_head(const GemmArgs& a, int row, int col, float* v) {
   }
   __nv_bfloat16* base = reinterpret_cast<__nv_bfloat16*>(which == 0 ? e.q : (which == 1 ? e.k : e.v));
   uint4* dst = reinterpret_cast<uint4*>(base + ((size_t)h * e.tokens_total + row) * D);
+  if (which == 0 && e.q_scale != 0.f) {
+#pragma unroll
+    for (int j = 0; j < D; ++j) v[j] *= e.q_scale;
+  }
 #pragma unroll
   for (int j = 0; j < D / 8; ++j)
     dst[j] = make_uint4(pack_bf16(v[8 * j], v[8 * j + 1]), pack_bf16(v[8 * j + 2], v[8 * j + 3]),
@@ -232,14 +236,15 @@ VX_DEVICE void epi_qkv_scatter32(const GemmArgs& a, int row, int col, const uint
   const int h = hc / e.head_dim, off = hc - h * e.head_dim;
   __nv_bfloat16* base = reinterpret_cast<__nv_bfloat16*>(which == 0 ? e.q : (which == 1 ? e.k : e.v));
   uint4* dst = reinterpret_cast<uint4*>(base + ((size_t)h * e.tokens_total + row) * e.head_dim + off);
+  const float qs = which == 0 && e.q_scale != 0.f ? e.q_scale : 1.0f;
+#define VX_QV(i, bb) ((__uint_as_float(r[8 * j + i]) + bb) * qs)
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const float4 b0 = pre.b[2 * j], b1 = pre.b[2 * j + 1];
-    dst[j] = make_uint4(pack_bf16(__uint_as_float(r[8 * j + 0]) + b0.x, __uint_as_float(r[8 * j + 1]) + b0.y),
-                        pack_bf16(__uint_as_float(r[8 * j + 2]) + b0.z, __uint_as_float(r[8 * j + 3]) + b0.w),
-                        pack_bf16(__uint_as_float(r[8 * j + 4]) + b1.x, __uint_as_float(r[8 * j + 5]) + b1.y),
-                        pack_bf16(__uint_as_float(r[8 * j + 6]) + b1.z, __uint_as_float(r[8 * j + 7]) + b1.w));
+    dst[j] = make_uint4(pack_bf16(VX_QV(0, b0.x), VX_QV(1, b0.y)), pack_bf16(VX_QV(2, b0.z), VX_QV(3, b0.w)),
+                        pack_bf16(VX_QV(4, b1.x), VX_QV(5, b1.y)), pack_bf16(VX_QV(6, b1.z), VX_QV(7, b1.w)));
   }
+#undef VX_QV
 }
 
 // ---------------------------------------------------------------------------

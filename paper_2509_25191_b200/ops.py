@@ -8,6 +8,7 @@ is not a B200 the import / call fails loudly.
 from __future__ import annotations
 
 import ctypes
+import math
 import os
 from pathlib import Path
 
@@ -17,6 +18,7 @@ _LIB_PATH = Path(__file__).resolve().parent / "libvx.so"
 
 EPI_BF16, EPI_GELU, EPI_RESID, EPI_QKV, EPI_PATCH, EPI_F32 = range(6)
 LF_F32, LF_GELU, LF_SILU_BF16, LF_POSE = range(4)  # vx_linear_f32 epilogues
+ATTN_Q_LOG2 = 1  # vx_attention_ex flag: q pre-scaled by log2(e)/sqrt(d)
 
 _vp = ctypes.c_void_p
 _i64 = ctypes.c_int64
@@ -33,7 +35,7 @@ class Epilogue(ctypes.Structure):
         ("rope_cos", _vp), ("rope_sin", _vp),
         ("embed_dim", _i32), ("head_dim", _i32), ("tokens_total", _i32),
         ("tokens_per_frame", _i32), ("patch_start", _i32), ("grid_w", _i32),
-        ("eps", _f32),
+        ("eps", _f32), ("q_scale", _f32),
     ]
 
 
@@ -58,7 +60,7 @@ class GaProblem(ctypes.Structure):
     ]
 
 
-EXPORTED_SYMBOLS = ("vx_gemm", "vx_attention", "vx_attention_merge", "vx_layernorm", "vx_layernorm_gather", "vx_patchify",
+EXPORTED_SYMBOLS = ("vx_gemm", "vx_attention", "vx_attention_merge", "vx_attention_ex", "vx_layernorm", "vx_layernorm_gather", "vx_patchify",
                     "vx_special_tokens", "vx_dino_tokens", "vx_linear_f32", "vx_adaln_modulate",
                     "vx_upsample_bilinear", "vx_gemm_spatial", "vx_epipolar_residuals",
                     "vx_epipolar_accumulate", "vx_ga_decode", "vx_ga_residuals", "vx_ga_loss_grad",
@@ -82,6 +84,9 @@ def load_library(path: os.PathLike | None = None) -> ctypes.CDLL:
     lib.vx_attention.argtypes = [_vp, _vp, _vp, _vp, _i64, _vp, _i32, _i32, _i32, _i32, _i32, _i64, _i64, _vp]
     lib.vx_attention_merge.argtypes = [_vp, _vp, _vp, _i32, _vp, _i64, _vp, _vp, _i64, _i32, _i32, _i32, _i32, _i32,
                                        _i64, _i64, _vp]
+    if hasattr(lib, "vx_attention_ex"):  # (absent from builds before it; tools/ A/B older libraries)
+        lib.vx_attention_ex.argtypes = [_vp, _vp, _vp, _i32, _vp, _i64, _vp, _vp, _i64, _i32, _i32, _i32, _i32,
+                                        _i32, _i64, _i64, _i32, _vp]
     lib.vx_layernorm.argtypes = [_vp, _i32, _i64, _vp, _i32, _i64, _vp, _vp, _i32, _i32, _f32, _vp]
     lib.vx_layernorm_gather.argtypes = [_vp, _i32, _i64, _vp, _i32, _i64, _vp, _vp, _i32, _i32, _f32, _i32, _i32,
                                         _i32, _vp]
@@ -110,8 +115,8 @@ def load_library(path: os.PathLike | None = None) -> ctypes.CDLL:
     lib.vx_version.restype = ctypes.c_char_p
     lib.vx_launch_count.restype = ctypes.c_uint64
     for name in EXPORTED_SYMBOLS:
-        if name in ("vx_last_error", "vx_version", "vx_launch_count"):
-            continue
+        if name in ("vx_last_error", "vx_version", "vx_launch_count") or not hasattr(lib, name):
+            continue  # (tests/test_abi.py checks that the product library exports every symbol)
         getattr(lib, name).restype = _i32
     if path is None:
         _lib = lib
@@ -169,8 +174,9 @@ def _rowmajor(t, name):
 # ---------------------------------------------------------------------------
 def gemm(a: torch.Tensor, w: torch.Tensor, epi: int = EPI_BF16, bias=None, out=None, resid=None,
          gamma=None, kept=None, qkv=None, qk_norm=None, rope=None, head_dim=0, tokens_total=0,
-         tokens_per_frame=1, patch_start=0, grid_w=1, eps=1e-5):
-    """D = a @ w.T with the given fused epilogue (see include/vx_api.h)."""
+         tokens_per_frame=1, patch_start=0, grid_w=1, eps=1e-5, q_scale=0.0):
+    """D = a @ w.T with the given fused epilogue (see include/vx_api.h). EPI_QKV: q_scale != 0
+    multiplies q before its bf16 store (Q_LOG2_SCALE(d) for attention(..., q_log2=True))."""
     load_library()
     _req(a, torch.bfloat16, "a")
     _req(w, torch.bfloat16, "w")
@@ -217,6 +223,7 @@ def gemm(a: torch.Tensor, w: torch.Tensor, epi: int = EPI_BF16, bias=None, out=N
         ep.embed_dim = N // 3
         ep.head_dim = head_dim
         ep.tokens_total = tokens_total
+        ep.q_scale = q_scale
     ep.tokens_per_frame = tokens_per_frame
     ep.patch_start = patch_start
     ep.grid_w = grid_w
@@ -225,8 +232,14 @@ def gemm(a: torch.Tensor, w: torch.Tensor, epi: int = EPI_BF16, bias=None, out=N
     return out
 
 
-def attention(q, k, v, out, nseq: int, Lq: int, Lk: int, lse=None):
-    """Flash attention over q [H, Tq, d], k/v [H, Tk, d] -> out [Tq', H*d] (bf16)."""
+def Q_LOG2_SCALE(head_dim: int) -> float:
+    """q scale that puts the attention scores in log2 units (gemm q_scale for attention q_log2=True)."""
+    return 1.4426950408889634 / math.sqrt(head_dim)
+
+
+def attention(q, k, v, out, nseq: int, Lq: int, Lk: int, lse=None, q_log2: bool = False):
+    """Flash attention over q [H, Tq, d], k/v [H, Tk, d] -> out [Tq', H*d] (bf16). q_log2: q already
+    holds q * Q_LOG2_SCALE(d) (the qkv epilogue's q_scale); the result means the same."""
     load_library()
     for t, nm in ((q, "q"), (k, "k"), (v, "v"), (out, "out")):
         _req(t, torch.bfloat16, nm)
@@ -239,12 +252,17 @@ def attention(q, k, v, out, nseq: int, Lq: int, Lk: int, lse=None):
     ldo = _rowmajor(out, "out")
     if lse is not None:
         _req(lse, torch.float32, "lse")
-    _check(_lib.vx_attention(_ptr(q), _ptr(k), _ptr(v), _ptr(out), ldo, _ptr(lse), D, H, nseq, Lq, Lk,
-                             Tq, Tk, _stream()), "vx_attention")
+    if q_log2:
+        _check(_lib.vx_attention_ex(_ptr(q), _ptr(k), _ptr(v), 0, None, 0, _ptr(lse), _ptr(out), ldo, D, H, nseq, Lq,
+                                    Lk, Tq, Tk, ATTN_Q_LOG2, _stream()), "vx_attention_ex")
+    else:
+        _check(_lib.vx_attention(_ptr(q), _ptr(k), _ptr(v), _ptr(out), ldo, _ptr(lse), D, H, nseq, Lq, Lk,
+                                 Tq, Tk, _stream()), "vx_attention")
     return out
 
 
-def attention_merge(q, k, v, mode: int, o_acc, lse_acc, out=None, nseq: int = 1, Lq: int = 0, Lk: int = 0):
+def attention_merge(q, k, v, mode: int, o_acc, lse_acc, out=None, nseq: int = 1, Lq: int = 0, Lk: int = 0,
+                    q_log2: bool = False):
     """One ring step with the fused LSE merge (vx_attention_merge): mode 1 first / 2 merge / 3 final (-> out)."""
     load_library()
     for t, nm in ((q, "q"), (k, "k"), (v, "v")):
@@ -260,9 +278,14 @@ def attention_merge(q, k, v, mode: int, o_acc, lse_acc, out=None, nseq: int = 1,
     if mode == 3:
         _req(out, torch.bfloat16, "out")
         ldo = _rowmajor(out, "out")
-    _check(_lib.vx_attention_merge(_ptr(q), _ptr(k), _ptr(v), mode, _ptr(o_acc), ld_acc, _ptr(lse_acc),
-                                   _ptr(out) if mode == 3 else None, ldo, D, H, nseq, Lq or Tq, Lk or Tk, Tq, Tk,
-                                   _stream()), "vx_attention_merge")
+    if q_log2:
+        _check(_lib.vx_attention_ex(_ptr(q), _ptr(k), _ptr(v), mode, _ptr(o_acc), ld_acc, _ptr(lse_acc),
+                                    _ptr(out) if mode == 3 else None, ldo, D, H, nseq, Lq or Tq, Lk or Tk, Tq, Tk,
+                                    ATTN_Q_LOG2, _stream()), "vx_attention_ex")
+    else:
+        _check(_lib.vx_attention_merge(_ptr(q), _ptr(k), _ptr(v), mode, _ptr(o_acc), ld_acc, _ptr(lse_acc),
+                                       _ptr(out) if mode == 3 else None, ldo, D, H, nseq, Lq or Tq, Lk or Tk, Tq, Tk,
+                                       _stream()), "vx_attention_merge")
 
 
 def layernorm(x, w, b, eps, out=None, out_dtype=torch.bfloat16):

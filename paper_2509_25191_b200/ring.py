@@ -101,7 +101,7 @@ class TorchDistComm:
 
 class FrameShardedRing:
     def __init__(self, cfg: VGGTConfig, device, group=None, comm=None,
-                 partial_attention: Optional[Callable] = None, merge: Callable = lse_merge):
+                 partial_attention: Optional[Callable] = None, merge: Callable = lse_merge, q_log2: bool = False):
         self.cfg = cfg
         self.device = torch.device(device)
         self.comm = comm if comm is not None else TorchDistComm(group)
@@ -110,6 +110,10 @@ class FrameShardedRing:
         # default: vx_attention_merge (LSE merge fused into the FMHA epilogue); injected functions are
         # for the CPU (gloo) tests of the ring schedule
         self.fused = partial_attention is None
+        # q arrives pre-scaled by log2(e)/sqrt(d) (VGGT's aggregator); only the fused vx path reads it so
+        if q_log2 and not self.fused:
+            raise ValueError("q_log2 needs the fused vx ring step (no partial_attention)")
+        self.q_log2 = q_log2
         self.partial = partial_attention or _vx_partial
         self.merge = merge
         self.split: Optional[List[Tuple[int, int]]] = None
@@ -171,7 +175,11 @@ class FrameShardedRing:
         g, r = self.world, self.rank
         Tl = self.tokens_of(r)
         if g == 1:
-            self.partial(q, k, v, o, None, Tl, Tl)
+            if self.fused:
+                from . import ops
+                ops.attention(q, k, v, o, nseq=1, Lq=Tl, Lk=Tl, q_log2=self.q_log2)
+            else:
+                self.partial(q, k, v, o, None, Tl, Tl)
             return
         bufs, o_acc, lse_acc = self.begin(H, d, q.dtype)  # no-op after VGGT._aggregate's begin()
         if k.data_ptr() != bufs[0, 0].data_ptr():  # K/V not produced in place (tests, custom callers)
@@ -195,7 +203,7 @@ class FrameShardedRing:
             if self.fused:  # one launch: partial attention + running log-sum-exp merge (+ final bf16 write)
                 from . import ops
                 mode = 1 if step == 0 else (3 if step == g - 1 else 2)
-                ops.attention_merge(q, kb, vb, mode, o_acc, lse_acc, out=o, Lq=Tl, Lk=Lk)
+                ops.attention_merge(q, kb, vb, mode, o_acc, lse_acc, out=o, Lq=Tl, Lk=Lk, q_log2=self.q_log2)
             else:
                 self.partial(q[:, :Tl], kb, vb, o_s, lse_s, Tl, Lk)
                 self.merge(o_acc, lse_acc, o_s, lse_s)

@@ -55,7 +55,7 @@ class VGGT:
         self.ring = None
         if dist:
             from .ring import FrameShardedRing
-            self.ring = FrameShardedRing(self.cfg, self.device, comm=comm)
+            self.ring = FrameShardedRing(self.cfg, self.device, comm=comm, q_log2=True)
 
     # -- helpers ------------------------------------------------------------
     def _head_streams(self, dev):

@@ -102,8 +102,9 @@ def _rope_ref(x, pos, freq=100.0):
     return rope_2d(x, pos, freq)
 
 
+@pytest.mark.parametrize("q_log2", [False, True])
 @pytest.mark.parametrize("C,H,S,grid", [(1024, 16, 2, 37), (128, 4, 8, 8), (256, 4, 3, 9)])
-def test_gemm_qkv_qknorm_rope(ops, C, H, S, grid):
+def test_gemm_qkv_qknorm_rope(ops, C, H, S, grid, q_log2):
     from oracle.vggt_ref import positions, rope_tables
     from paper_2509_25191_b200.config import VGGTConfig
     cfg = VGGTConfig(img_size=grid * 14, embed_dim=C, num_heads=H)
@@ -120,14 +121,15 @@ def test_gemm_qkv_qknorm_rope(ops, C, H, S, grid):
     q = torch.empty(H, T, d, device="cuda", dtype=torch.bfloat16)
     k = torch.empty_like(q)
     v = torch.empty_like(q)
+    qs = ops.Q_LOG2_SCALE(d) if q_log2 else 0.0  # q stored pre-scaled for attention(..., q_log2=True)
     ops.gemm(a, w, ops.EPI_QKV, bias=bias, qkv=(q, k, v), qk_norm=(qw, qb, kw, kb), rope=(cos_q, sin_q),
              head_dim=d, tokens_total=T, tokens_per_frame=tpf, patch_start=cfg.patch_start_idx, grid_w=grid,
-             eps=1e-5)
+             eps=1e-5, q_scale=qs)
     y = (a.float() @ w.float().T + bias).cpu().view(T, 3, H, d).permute(1, 2, 0, 3)  # (3, H, T, d)
     qr = F.layer_norm(y[0], (d,), qw.cpu(), qb.cpu(), 1e-5)
     kr = F.layer_norm(y[1], (d,), kw.cpu(), kb.cpu(), 1e-5)
     pos = positions(cfg).repeat(S, 1)
-    qr = _rope_ref(qr, pos)
+    qr = _rope_ref(qr, pos) * (qs or 1.0)
     kr = _rope_ref(kr, pos)
     assert rel(q.cpu(), qr) < 5e-3
     assert rel(k.cpu(), kr) < 5e-3
@@ -184,6 +186,49 @@ def test_attention_large_logits_rescale(ops, L):
     ops.attention(q, k, v, out, 1, L, L)
     ref, _ = _sdpa_ref(q, k, v, 1, L, L)
     assert rel(out, ref) < 1e-2
+
+
+@pytest.mark.parametrize("D,H,nseq,L", [(64, 16, 3, 1374), (64, 2, 1, 5000), (64, 1, 3, 600), (32, 4, 8, 69),
+                                        (128, 4, 1, 300), (64, 1, 2, 6144)])
+def test_attention_q_log2_matches_plain(ops, D, H, nseq, L):
+    # q pre-multiplied by log2(e)/sqrt(D) (the qkv epilogue's q_scale) + VX_ATTN_Q_LOG2: same result
+    T = nseq * L
+    q = _bf(H, T, D, seed=20)
+    k = _bf(H, T, D, seed=21)
+    v = _bf(H, T, D, seed=22)
+    qs = (q.float() * ops.Q_LOG2_SCALE(D)).to(torch.bfloat16)
+    out = torch.empty(T, H * D, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(H, T, device="cuda")
+    ops.attention(qs, k, v, out, nseq, L, L, lse=lse, q_log2=True)
+    ref, lse_ref = _sdpa_ref(qs.float() / ops.Q_LOG2_SCALE(D), k, v, nseq, L, L)
+    assert rel(out, ref) < 1e-2
+    assert (lse - lse_ref).abs().max().item() < 1e-2
+
+
+@pytest.mark.parametrize("case", ["overflow", "underflow", "after_fallback"])
+@pytest.mark.parametrize("nseq,L", [(1, 3000), (3, 1374)])
+def test_attention_max_free_fallback(ops, case, nseq, L):
+    # plain launches run without a running max (P = 2^(s*scale*log2e)); rows whose P or O would leave
+    # the fp32 range are flagged and the launch is recomputed by the exact kernel
+    H, D = 2, 64
+    T = nseq * L
+    if case == "overflow":  # scores up to ~300 in log2 units: 2^300 overflows fp32
+        q, k = _bf(H, T, D, scale=8.0, seed=50), _bf(H, T, D, scale=8.0, seed=51)
+    elif case == "underflow":  # every score ~ -185 in log2 units: all P would flush to zero
+        q = torch.full((H, T, D), 4.0, device="cuda", dtype=torch.bfloat16)
+        k = torch.full((H, T, D), -4.0, device="cuda", dtype=torch.bfloat16) + _bf(H, T, D, scale=0.01, seed=52)
+    else:  # an ordinary launch right after a flagged one (the flag must have been cleared)
+        ops.attention(_bf(H, T, D, scale=8.0, seed=50), _bf(H, T, D, scale=8.0, seed=51),
+                      _bf(H, T, D, seed=53), torch.empty(T, H * D, device="cuda", dtype=torch.bfloat16), nseq, L, L)
+        q, k = _bf(H, T, D, seed=54), _bf(H, T, D, seed=55)
+    v = _bf(H, T, D, seed=53)
+    out = torch.empty(T, H * D, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(H, T, device="cuda")
+    ops.attention(q, k, v, out, nseq, L, L, lse=lse)
+    ref, lse_ref = _sdpa_ref(q, k, v, nseq, L, L)
+    assert torch.isfinite(out.float()).all()
+    assert rel(out, ref) < 1e-2
+    assert ((lse - lse_ref).abs() / lse_ref.abs().clamp_min(1.0)).max().item() < 1e-3
 
 
 @pytest.mark.parametrize("Lq,Lk", [(700, 1900), (333, 6000), (4200, 257),
@@ -353,11 +398,15 @@ def test_upsample_bilinear_matches_interpolate(ops):
 @pytest.mark.parametrize("shards,Lq", [([700], 600), ([300, 411], 600), ([513, 200, 333, 90], 600),
                                        # 152 units = 1 wave + 4: KV-split tail in every merge mode
                                        ([6200], 512 * 37 + 100), ([6200, 6300, 6150], 512 * 37 + 100)])
-def test_attention_ring_merge_matches_full(ops, shards, Lq):
+@pytest.mark.parametrize("q_log2", [False, True])
+def test_attention_ring_merge_matches_full(ops, shards, Lq, q_log2):
     # the ring's fused-merge steps (vx_attention_merge) over K/V shards == attention over all keys
     H, D = 4, 64
     Lk = sum(shards)
     q = _bf(H, Lq, D, seed=50)
+    qa = (q.float() * ops.Q_LOG2_SCALE(D)).to(torch.bfloat16) if q_log2 else q
+    if q_log2:
+        q = qa.float() / ops.Q_LOG2_SCALE(D)  # the fp32 reference sees the same rounded q
     k = _bf(H, Lk, D, seed=51)
     v = _bf(H, Lk, D, seed=52)
     ref, lse_ref = _sdpa_ref(q, k, v, 1, Lq, Lk)
@@ -371,7 +420,7 @@ def test_attention_ring_merge_matches_full(ops, shards, Lq):
         mode = 3 if i == len(shards) - 1 and i > 0 else (1 if i == 0 else 2)
         if len(shards) == 1:
             mode = 1
-        ops.attention_merge(q, ks, vs, mode, o_acc, lse, out=out, Lq=Lq, Lk=n)
+        ops.attention_merge(qa, ks, vs, mode, o_acc, lse, out=out, Lq=Lq, Lk=n, q_log2=q_log2)
         off += n
     got = o_acc if len(shards) == 1 else out
     assert rel(got, ref) < 1e-2

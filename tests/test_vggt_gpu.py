@@ -161,8 +161,8 @@ def _patch_attention(monkeypatch, rule):
     from paper_2509_25191_b200 import ops
     real = ops.attention
 
-    def patched(q, k, v, out, nseq, Lq, Lk, lse=None):
-        return rule(real, q, k, v, out, nseq, Lq, Lk, lse)
+    def patched(q, k, v, out, nseq, Lq, Lk, lse=None, q_log2=False):
+        return rule(lambda *a, **kw: real(*a, q_log2=q_log2, **kw), q, k, v, out, nseq, Lq, Lk, lse)
 
     monkeypatch.setattr(ops, "attention", patched)
 

@@ -22,8 +22,10 @@ def main():
     ap.add_argument("--views", type=int, default=200, help="frame layer views")
     ap.add_argument("--global-views", type=int, nargs="*", default=[20, 200])
     ap.add_argument("--rounds", type=int, default=6)
+    ap.add_argument("--q-log2", default="", help="A,B flags: 1 = call B (or A) with q pre-scaled (VX_ATTN_Q_LOG2), e.g. 0,1")
     args = ap.parse_args()
     libs = [ops.load_library(p) for p in args.libs]
+    ql2 = [f == "1" for f in args.q_log2.split(",")] if args.q_log2 else [False, False]
     N, H, d = 1374, 16, 64
     cases = [("frame", args.views, args.views, N)] + [("global", v, 1, v * N) for v in args.global_views]
     res = {}
@@ -39,12 +41,12 @@ def main():
                 idx = li if r % 2 == 0 else 1 - li
                 ops._lib = lib
                 for _ in range(1):
-                    ops.attention(q, k, v, o, nseq, L, L)
+                    ops.attention(q, k, v, o, nseq, L, L, q_log2=ql2[idx])
                 torch.cuda.synchronize()
                 s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 s.record()
                 for _ in range(reps):
-                    ops.attention(q, k, v, o, nseq, L, L)
+                    ops.attention(q, k, v, o, nseq, L, L, q_log2=ql2[idx])
                 e.record()
                 e.synchronize()
                 ts[idx].append(s.elapsed_time(e) / reps)
