@@ -77,10 +77,15 @@ struct AttnArgs {
   // finished (the last one resets both, so the counters are zero again for the next launch on the
   // stream); nullptr = static round-robin (while a stream is being captured before the counters exist)
   unsigned* sched;
-  // max-free launches (NOMAX kernel): bad[0] is set when a row's result is not trustworthy (P or O
-  // out of range); the exact kernel then runs as a fixup (fixup = 1): it exits at once unless bad[0]
-  // is set, otherwise recomputes the whole launch, and its last CTA clears bad[0] (bad[1] counts them)
+  // max-free launches (NOMAX kernel): a unit with a row whose result is not trustworthy (P or O out
+  // of the fp32 range) is appended to fix_list (bad[0] = entries; more than fix_cap = recompute every
+  // unit). The exact kernel then runs as a fixup (fixup = 1) over the listed units only: it exits at
+  // once when the list is empty, and its last CTA clears bad[0] (bad[1] counts its CTAs). Plain
+  // launches write every unit and the fixup overwrites the listed ones; ring-merge launches (in-place
+  // O / lse accumulation) skip writing a flagged unit altogether, so the fixup merges it exactly once.
   unsigned* bad;
+  unsigned* fix_list;
+  int fix_cap;
   int fixup;
 };
 
@@ -207,8 +212,20 @@ template <int D, int EMU_PAIRS_OF_8, int NT_, int BKV_, bool ALIAS_, bool SUMV_,
 __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PACK_>::THREADS, 1)
     fmha_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                 const __grid_constant__ CUtensorMap tmV, const AttnArgs a) {
-  // fixup launch after a max-free one: nothing to do unless some row was flagged
-  if (a.fixup && *reinterpret_cast<volatile unsigned*>(a.bad) == 0u) return;
+  // fixup launch after a max-free one: nothing to do unless some unit was flagged; otherwise its work
+  // items are the listed units (whole units, no KV split)
+  int nwork = a.work;
+  bool fix_all = false;
+  if (a.fixup) {
+    const unsigned nb = *reinterpret_cast<volatile unsigned*>(a.bad);
+    if (nb == 0u) return;
+    fix_all = nb > unsigned(a.fix_cap);
+    nwork = fix_all ? a.units : int(nb);
+  }
+  auto item = [&](int w) -> WorkItem {
+    if (a.fixup) return {fix_all ? w : int(a.fix_list[w]), 0, a.kv_tiles, -1, 0};
+    return work_item(a, w);
+  };
   using Cfg = AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PACK_>;
   constexpr bool ALIAS = ALIAS_;
   constexpr bool PACK = PACK_;
@@ -251,6 +268,9 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PAC
   uint64_t* wq_empty = wq_full + WQ; // [WQ] MMA warp + softmax warps -> producer: slot read
   volatile int* wq = reinterpret_cast<volatile int*>(wq_empty + WQ);  // [WQ] work item indices
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wq_empty + WQ) + WQ;
+  // NOMAX: [0] last unit this CTA appended to the fix list (plain launches: de-duplication);
+  // [1 + (n & 1)] = n + 1 when a row of this CTA's n-th unit is flagged (ring-merge launches)
+  [[maybe_unused]] volatile int* unit_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -273,6 +293,11 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PAC
       mbar_init(&p_full[i], 4);
       mbar_init(&p_free[i], 1);
       mbar_init(&o_empty[i], 4);
+    }
+    if constexpr (NOMAX_) {
+      unit_flag[0] = -1;
+      unit_flag[1] = 0;
+      unit_flag[2] = 0;
     }
     for (int i = 0; i < WQ; ++i) {
       mbar_init(&wq_full[i], 1);
@@ -329,8 +354,8 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PAC
           wq[slot] = w;
           mbar_arrive(&wq_full[slot]);
         }
-        if (w >= a.work) break;
-        const WorkItem wi = work_item(a, w);
+        if (w >= nwork) break;
+        const WorkItem wi = item(w);
         const int t0 = wi.u * NT;
         int qt0;
         const int gA = tile_seq(t0, qt0);
@@ -414,8 +439,8 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PAC
       if constexpr (ALIAS) {
         for (;; ++n) {
           const int w = wq_take(n);
-          if (w >= a.work) break;
-          const WorkItem wi = work_item(a, w);
+          if (w >= nwork) break;
+          const WorkItem wi = item(w);
           const int nkv = wi.cnt;
           // PACK: bit i = Q tile i belongs to the unit's second sequence (K/V slot B of every stage)
           uint32_t bmask = 0;
@@ -477,8 +502,8 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PAC
       } else {
         for (;; ++n) {
           const int w = wq_take(n);
-          if (w >= a.work) break;
-          const int nkv = work_item(a, w).cnt;
+          if (w >= nwork) break;
+          const int nkv = item(w).cnt;
           mbar_wait(q_full, n & 1);
           tc_fence_after();
           {  // S(0) of both tiles; the S buffers were released by the previous unit's last s_free
@@ -542,8 +567,8 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PAC
     [[maybe_unused]] int unit_n = 0;
     for (;; ++unit_n) {
       const int w = wq_take(uint32_t(unit_n));
-      if (w >= a.work) break;
-      const WorkItem wi = work_item(a, w);
+      if (w >= nwork) break;
+      const WorkItem wi = item(w);
       const int nkv = wi.cnt;
       const int t = wi.u * NT + tile;
       int qt;
@@ -882,18 +907,31 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PAC
       tmem_ld_n<DL>(O_addr, orr);
       tmem_wait_ld();
       if constexpr (SUMV) l_run = __uint_as_float(orr[D]);  // sum_k P_ik from the ones panel
+      [[maybe_unused]] bool skip_unit = false;
       if constexpr (NOMAX) {
         // trustworthy iff the row sum is well inside the normal fp32 range and O is finite (O <= l max|v|)
         float chk = 0.f;
 #pragma unroll
         for (int c = 0; c < D; ++c) chk += __uint_as_float(orr[c]);
         const bool bad = row_valid && !(l_run > 1e-30f && l_run < 1e30f && fabsf(chk) < 3.0e38f);
-        if (__any_sync(0xffffffff, bad) && lane == 0) atomicOr(a.bad, 1u);
+        const bool wbad = __any_sync(0xffffffff, bad);
+        auto append = [&]() {
+          const unsigned idx = atomicAdd(a.bad, 1u);
+          if (idx < unsigned(a.fix_cap)) a.fix_list[idx] = unsigned(wi.u);
+        };
+        if (a.merge == 0) {  // written anyway; the fixup overwrites the unit
+          if (wbad && lane == 0 && atomicExch(const_cast<int*>(unit_flag), wi.u) != wi.u) append();
+        } else {  // the whole unit is written only if none of its rows is flagged
+          if (wbad && lane == 0) unit_flag[1 + (unit_n & 1)] = unit_n + 1;
+          named_bar_sync(1, 128 * NT);
+          skip_unit = unit_flag[1 + (unit_n & 1)] == unit_n + 1;
+          if (skip_unit && tile == 0 && wl == 0 && lane == 0) append();
+        }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&o_empty[tile]);
-      if (row_valid) {
+      if (row_valid && !skip_unit) {
         const float inv = 1.0f / l_run;
         const int64_t orow = (int64_t)s * a.Lq + q_local;
         const float lse_new = (m_run + __log2f(l_run)) * 0.69314718055994531f;
@@ -963,7 +1001,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PAC
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
-  if (a.fixup && threadIdx.x == 0) {  // a fixup that ran: the last CTA clears the flag for the next launch
+  if (a.fixup && threadIdx.x == 0) {  // a fixup that ran: the last CTA clears the list for the next launch
     __threadfence();
     if (atomicAdd(a.bad + 1, 1u) == gridDim.x - 1) {
       atomicExch(a.bad, 0u);
@@ -1075,9 +1113,34 @@ static float* split_scratch(cudaStream_t st, size_t floats) {
   return p;
 }
 
-// Per-stream work-ticket counters of the FMHA (2 x u32, zero between launches: each launch's last
-// CTA resets them). Allocated and zeroed once per stream; not while the stream is being captured
-// (the launch then falls back to static round-robin scheduling).
+// Per-stream unit list of the max-free launches' fixup (AttnArgs::fix_list), grown to the largest
+// unit count seen; not allocated while the stream is being captured (the launch then runs the exact
+// kernel only).
+static unsigned* fix_buffer(cudaStream_t st, int64_t cap) {
+  static std::mutex mu;
+  static std::map<cudaStream_t, std::pair<unsigned*, int64_t>> bufs;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = bufs.find(st);
+  if (it != bufs.end() && it->second.second >= cap) return it->second.first;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
+  unsigned* p = nullptr;
+  if (cudaMalloc(&p, cap * sizeof(unsigned)) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  if (it != bufs.end()) {  // grow: queued work on this stream may still read the old list
+    cudaStreamSynchronize(st);
+    cudaFree(it->second.first);
+  }
+  bufs[st] = {p, cap};
+  return p;
+}
+
+// Per-stream work-ticket counters of the FMHA and the max-free launches' fix-list count (4 x u32,
+// zero between launches: each launch's last CTA resets them). Allocated and zeroed once per stream;
+// not while the stream is being captured (the launch then falls back to static round-robin
+// scheduling and the exact kernel).
 static unsigned* sched_counters(cudaStream_t st) {
 #ifdef VX_DIAG
   {  // diagnostic build only: VX_FMHA_STATIC=1 = static round-robin (read per launch for in-process A/B)
@@ -1133,7 +1196,10 @@ static int launch_fmha(const void* q, const void* k, const void* v, AttnArgs arg
 #endif
   // only for long units: each split costs a merge launch and fp32 partial round trips, which a
   // frame-attention unit (29 KV tiles) does not earn back (S=20 frame layer 0.215 -> 0.228 ms)
-  if (split_on && !PACK && tail > 0 && 2 * tail <= sms && args.kv_tiles >= 128) {
+  // (not for a fixup, whose work items are listed units, nor for a max-free ring-merge step, whose
+  // flagged units must not be merged by the split-merge kernel)
+  if (split_on && !PACK && !args.fixup && !(NOMAX && args.merge != 0) && tail > 0 && 2 * tail <= sms &&
+      args.kv_tiles >= 128) {
     int parts = sms / tail;
     if (parts > args.kv_tiles / 2) parts = args.kv_tiles / 2;  // >= 2 KV tiles per item
     if (parts >= 2 && (int64_t)parts * args.kv_tiles < (1ll << 31)) {
@@ -1248,12 +1314,16 @@ static int attention_impl(const void* q, const void* k, const void* v, void* out
     constexpr bool pack_on = true;
 #endif
     const bool pack = pack_on && merge == 0 && nseq > 1 && tps >= 4 && tps % 4 != 0;
-    // plain launches run max-free first (NOMAX) and then the exact kernel as a fixup that exits at once
-    // unless a row was flagged; ring-merge steps (in-place accumulation) and stream capture (no flag
-    // storage) run the exact kernel only
-    unsigned* flag = merge == 0 ? sched_counters(st) : nullptr;
-    if (flag) {
+    // run max-free first (NOMAX) and then the exact kernel as a fixup over the flagged units (it exits
+    // at once when there are none); while the stream is being captured (no list storage) only the
+    // exact kernel runs
+    unsigned* flag = sched_counters(st);
+    const int64_t cap = (int64_t)H * nseq * tps;  // >= units of any configuration
+    unsigned* list = flag && cap < (1ll << 30) ? fix_buffer(st, cap) : nullptr;
+    if (flag && list) {
       a.bad = flag + 2;
+      a.fix_list = list;
+      a.fix_cap = int(cap);
       constexpr int E = VX_FMHA_NOMAX_EMU;
       int e;
       if (q_log2)

@@ -427,6 +427,31 @@ def test_attention_ring_merge_matches_full(ops, shards, Lq, q_log2):
     assert (lse - lse_ref).abs().max().item() < 1e-2
 
 
+@pytest.mark.parametrize("scale", [8.0, 1.0])
+def test_attention_ring_merge_fallback(ops, scale):
+    # ring steps run max-free too: a unit with an overflowing row must not be merged by the max-free
+    # kernel (in-place O / lse), only once by the exact fixup; scale 8 overflows in some units, and
+    # the second case runs an ordinary ring right after (list cleared)
+    H, D, Lq, shards = 2, 64, 3000, [2500, 1700, 2100]
+    Lk = sum(shards)
+    q = _bf(H, Lq, D, scale=scale, seed=60)
+    k = _bf(H, Lk, D, scale=scale, seed=61)
+    v = _bf(H, Lk, D, seed=62)
+    ref, lse_ref = _sdpa_ref(q, k, v, 1, Lq, Lk)
+    o_acc = torch.empty(Lq, H * D, device="cuda")
+    lse = torch.empty(H, Lq, device="cuda")
+    out = torch.empty(Lq, H * D, device="cuda", dtype=torch.bfloat16)
+    off = 0
+    for i, n in enumerate(shards):
+        mode = 1 if i == 0 else (3 if i == len(shards) - 1 else 2)
+        ops.attention_merge(q, k[:, off:off + n].contiguous(), v[:, off:off + n].contiguous(), mode, o_acc, lse,
+                            out=out, Lq=Lq, Lk=n)
+        off += n
+    assert torch.isfinite(out.float()).all()
+    assert rel(out, ref) < 1e-2
+    assert ((lse - lse_ref).abs() / lse_ref.abs().clamp_min(1.0)).max().item() < 1e-3
+
+
 @pytest.mark.gpu
 def test_c_abi_rejects_bad_shapes(ops):
     """Every entry point validates its arguments and reports through vx_last_error (no CUDA fault)."""
