@@ -100,11 +100,11 @@ int vx_gemm(int epi, const void* A, int64_t lda, const void* B, int64_t ldb, int
  * allocated on the stream's first launch, reset by each launch's last CTA), so CTAs that start late
  * (SMs held by a concurrent kernel, e.g. an NCCL transfer) take fewer units; results do not depend
  * on the assignment (each unit's arithmetic is fixed).
- * D = 64 plain launches run a max-free softmax (P = 2^score, no running max) and then the exact
- * kernel as a fixup that exits at once unless some row's sum or output left the safe fp32 range
- * (flag in the same per-stream words), in which case it recomputes the launch: results are those
- * of the exact kernel either way, up to rounding. While the stream is being captured, and for the
- * merge modes, only the exact kernel runs. */
+ * D = 64 launches (plain and ring merge) run a max-free softmax (P = 2^score, no running max) and
+ * then the exact kernel as a fixup over the work units with a row whose sum or output left the safe
+ * fp32 range (a per-stream list; the fixup exits at once when it is empty): results are those of
+ * the exact kernel either way, up to rounding. While the stream is being captured only the exact
+ * kernel runs. */
 int vx_attention(const void* q, const void* k, const void* v, void* out, int64_t ldo, float* lse,
                  int D, int H, int nseq, int Lq, int Lk, int64_t Tq, int64_t Tk, void* stream);
 /* One K/V-ring step of frame-sharded global attention with the log-sum-exp merge
