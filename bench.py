@@ -288,7 +288,7 @@ def main():
                 tj = json.load(f)
             if tj.get("views") == S:  # measured for this workload's launch only
                 traffic = tj.get("dram_bytes_per_launch")
-        roofline = {"bound": "tensor", "kernel": "vx fmha_kernel<64> (global attention)",
+        roofline = {"bound": "tensor", "kernel": "vx fmha_kernel<64> global attention (max-free launch + exact-fixup check launch)",
                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                     "peak_source": peaks["source"] + " bf16_tflops_sustained",
                     "flops_per_launch": attn_flops, "avg_launch_ms": ga["avg_ms"], "traffic": traffic}
