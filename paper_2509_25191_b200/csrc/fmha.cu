@@ -46,6 +46,9 @@
 #ifndef VX_FMHA_NOMAX_EMU  // exp pairs (of 8) on the FMA pipe in the max-free kernel
 #define VX_FMHA_NOMAX_EMU 2
 #endif
+#ifndef VX_FMHA_NOMAX_W64  // max-free kernel with 64-wide KV tiles and FADD row sums
+#define VX_FMHA_NOMAX_W64 0
+#endif
 
 namespace vx {
 
@@ -234,7 +237,8 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PAC
   // range, which the epilogue checks per row; a flagged launch is recomputed by the exact kernel.
   constexpr bool NOMAX = NOMAX_;
   constexpr bool QL2 = QL2_ && NOMAX_;  // (the exact kernel uses scale_log2 = 1 for pre-scaled q)
-  static_assert(!NOMAX || (ALIAS_ && SUMV_ && BKV_ == 48 && !PSM_), "NOMAX is implemented for the 4 x 48 aliased kernel");
+  static_assert(!NOMAX || (ALIAS_ && !PSM_ && ((SUMV_ && BKV_ == 48) || (!SUMV_ && BKV_ == 64))),
+                "NOMAX is implemented for the aliased 4 x 48 ones-panel and 4 x 64 kernels");
   constexpr bool PSM = PSM_;
   // speculative exps (step_spec) need P writes that can be repeated before p_full: aliased or
   // shared-memory P only
@@ -586,6 +590,49 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PAC
         VX_TRACE(trace_slot_sm(unit_n, wl, lane, tile, j, 1));
         sph ^= 1;
         tc_fence_after();
+        if constexpr (NOMAX && BKV == 64) {
+          // 64-wide KV tiles (4 tiles: 4 x (64 S/P + 64 O) = 512 TMEM columns, row sums by FADD2): two
+          // 32-column halves, P of half h to words [16h, 16h + 16) — over S columns the first half
+          // has already loaded
+          const int valid = a.Lk - BKV * (wi.j0 + j);
+          uint64_t rs[2] = {0, 0};
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf) {
+            uint32_t sr[32];
+            uint32_t pk[16];
+            tmem_ld32(S_addr + 32 * hf, sr);
+            tmem_wait_ld();
+            if (valid < BKV) {
+#pragma unroll
+              for (int c = 0; c < 32; ++c)
+                if (32 * hf + c >= valid) sr[c] = 0xff800000u;
+            }
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+              const uint64_t x = QL2 ? f2_pack(__uint_as_float(sr[2 * c]), __uint_as_float(sr[2 * c + 1]))
+                                     : f2_mul(f2_pack(__uint_as_float(sr[2 * c]), __uint_as_float(sr[2 * c + 1])), SL2);
+              float x0, x1, p0, p1;
+              f2_unpack(x, x0, x1);
+              if ((c & 7) >= 8 - EMU_PAIRS_OF_8) {
+                ex2_poly2<2>(x0, x1, p0, p1);
+              } else {
+                p0 = ex2(x0);
+                p1 = ex2(x1);
+              }
+              rs[c & 1] = f2_add(rs[c & 1], f2_pack(p0, p1));
+              pk[c] = pack_bf16(p0, p1);
+            }
+            tmem_st16(P_addr + 16 * hf, pk);
+          }
+          float r0, r1;
+          f2_unpack(f2_add(rs[0], rs[1]), r0, r1);
+          l_run += r0 + r1;
+          tmem_wait_st();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&p_full[tile]);
+          continue;
+        }
         if constexpr (BKV == 96) {
           // 96-wide KV tiles (3 Q tiles fit TMEM: 3 x (96 S/P + 72 O) = 504 columns), processed as two
           // 48-column halves A = S[0, 48), B = S[48, 96) so the registers stay those of one half. P (96
@@ -910,9 +957,13 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PAC
       [[maybe_unused]] bool skip_unit = false;
       if constexpr (NOMAX) {
         // trustworthy iff the row sum is well inside the normal fp32 range and O is finite (O <= l max|v|)
-        float chk = 0.f;
+        uint64_t c4[4] = {0, 0, 0, 0};  // packed partial sums (NaN / inf propagate), a short dependency chain
 #pragma unroll
-        for (int c = 0; c < D; ++c) chk += __uint_as_float(orr[c]);
+        for (int c = 0; c < D / 2; ++c)
+          c4[c & 3] = f2_add(c4[c & 3], f2_pack(__uint_as_float(orr[2 * c]), __uint_as_float(orr[2 * c + 1])));
+        float c0, c1;
+        f2_unpack(f2_add(f2_add(c4[0], c4[1]), f2_add(c4[2], c4[3])), c0, c1);
+        const float chk = c0 + c1;
         const bool bad = row_valid && !(l_run > 1e-30f && l_run < 1e30f && fabsf(chk) < 3.0e38f);
         const bool wbad = __any_sync(0xffffffff, bad);
         auto append = [&]() {
@@ -1326,12 +1377,21 @@ static int attention_impl(const void* q, const void* k, const void* v, void* out
       a.fix_cap = int(cap);
       constexpr int E = VX_FMHA_NOMAX_EMU;
       int e;
+#if VX_FMHA_NOMAX_W64
+      if (q_log2)
+        e = pack ? launch_fmha<64, E, 4, 64, true, false, true, true, false, false, true, true, true>(q, k, v, a, st)
+                 : launch_fmha<64, E, 4, 64, true, false, true, true, false, false, false, true, true>(q, k, v, a, st);
+      else
+        e = pack ? launch_fmha<64, E, 4, 64, true, false, true, true, false, false, true, true>(q, k, v, a, st)
+                 : launch_fmha<64, E, 4, 64, true, false, true, true, false, false, false, true>(q, k, v, a, st);
+#else
       if (q_log2)
         e = pack ? launch_fmha<64, E, 4, 48, true, true, true, true, true, false, true, true, true>(q, k, v, a, st)
                  : launch_fmha<64, E, 4, 48, true, true, true, true, true, false, false, true, true>(q, k, v, a, st);
       else
         e = pack ? launch_fmha<64, E, 4, 48, true, true, true, true, true, false, true, true>(q, k, v, a, st)
                  : launch_fmha<64, E, 4, 48, true, true, true, true, true, false, false, true>(q, k, v, a, st);
+#endif
       if (e != VX_OK) return e;
       a.fixup = 1;
     }
