@@ -427,6 +427,29 @@ def test_attention_ring_merge_matches_full(ops, shards, Lq, q_log2):
     assert (lse - lse_ref).abs().max().item() < 1e-2
 
 
+@pytest.mark.parametrize("warm", [True, False])
+def test_attention_under_graph_capture(ops, warm):
+    # warm stream: the max-free launch and its fixup are captured (per-stream words and list exist);
+    # fresh stream: nothing may be allocated during capture, so the exact kernel alone is captured
+    H, D, nseq, L = 2, 64, 3, 1374
+    T = nseq * L
+    q, k, v = _bf(H, T, D, seed=70), _bf(H, T, D, seed=71), _bf(H, T, D, seed=72)
+    out = torch.empty(T, H * D, device="cuda", dtype=torch.bfloat16)
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        if warm:
+            ops.attention(q, k, v, out, nseq, L, L)
+        st.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            ops.attention(q, k, v, out, nseq, L, L)
+    out.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    ref, _ = _sdpa_ref(q, k, v, nseq, L, L)
+    assert rel(out, ref) < 1e-2
+
+
 @pytest.mark.parametrize("scale", [8.0, 1.0])
 def test_attention_ring_merge_fallback(ops, scale):
     # ring steps run max-free too: a unit with an overflowing row must not be merged by the max-free
