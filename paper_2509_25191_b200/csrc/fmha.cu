@@ -234,7 +234,8 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PAC
   constexpr bool PACK = PACK_;
   // NOMAX: no running max at all — P = 2^(s * scale * log2e) with m = 0 (no row max, no vote, no
   // rescale; the first tile of a unit is no longer special). Exact whenever no P or O leaves the fp32
-  // range, which the epilogue checks per row; a flagged launch is recomputed by the exact kernel.
+  // range, which the epilogue checks per row; units with a flagged row are recomputed by the exact
+  // kernel (fixup launch over AttnArgs::fix_list).
   constexpr bool NOMAX = NOMAX_;
   constexpr bool QL2 = QL2_ && NOMAX_;  // (the exact kernel uses scale_log2 = 1 for pre-scaled q)
   static_assert(!NOMAX || (ALIAS_ && !PSM_ && ((SUMV_ && BKV_ == 48) || (!SUMV_ && BKV_ == 64))),
