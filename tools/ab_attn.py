@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--views", type=int, default=200, help="frame layer views")
     ap.add_argument("--global-views", type=int, nargs="*", default=[20, 200])
     ap.add_argument("--rounds", type=int, default=6)
+    ap.add_argument("--reps", type=int, default=0, help="launches per timed sample (default: 2 global / 10 frame)")
     ap.add_argument("--q-log2", default="", help="A,B flags: 1 = call B (or A) with q pre-scaled (VX_ATTN_Q_LOG2), e.g. 0,1")
     args = ap.parse_args()
     libs = [ops.load_library(p) for p in args.libs]
@@ -34,7 +35,7 @@ def main():
         q, k, v = (torch.randn(H, T, d, device="cuda", dtype=torch.bfloat16) for _ in range(3))
         o = torch.empty(T, H * d, device="cuda", dtype=torch.bfloat16)
         fl = 4.0 * nseq * L * L * H * d
-        reps = 2 if T > 100000 else 10
+        reps = args.reps or (2 if nseq == 1 and T > 100000 else 10)
         ts = [[], []]
         for r in range(args.rounds):
             for li, lib in enumerate(libs if r % 2 == 0 else libs[::-1]):
