@@ -191,13 +191,17 @@ __device__ unsigned long long* g_fmha_trace = nullptr;
   do {                 \
   } while (0)
 #endif
-// trace slots: softmax tile t (lane 0 of its first warp), iteration j < 64, point k < 5:
-//   (t * 64 + j) * 8 + k; MMA thread: 4096 + (j * 4 + i) * 2 + {0: p_full seen, 1: S(j+1) committed}
+// trace slots (CTA 0's first two units, up to 32 KV tiles each: iteration jj = 32 * unit + j):
+// softmax tile t (lane 0 of its first warp), point k < 8: (t * 64 + jj) * 8 + k (0 wait for S, 1 S
+// ready, 2 max (exact kernel) / output stores begin (unit's last tile), 3 exps done, 4 P-ready
+// arrive, 5 O final, 6 epilogue done, 7 O read); MMA thread: 4096 + (jj * 4 + i) * 2 + {0: p_full
+// seen, 1: S(j+1) committed}, 6000 + 4 * unit + i: S(0) committed, 6100 + unit: q_full seen;
+// producer: 6230 + unit q_empty seen, 6240 + 2 * unit + j: K stage j of the unit free
 VX_DEVICE int trace_slot_sm(int unit_n, int wl, int lane, int tile, int j, int k) {
-  return (unit_n == 0 && wl == 0 && lane == 0 && j < 64) ? (tile * 64 + j) * 8 + k : -1;
+  return (unit_n < 2 && wl == 0 && lane == 0 && j < 32) ? (tile * 64 + unit_n * 32 + j) * 8 + k : -1;
 }
 VX_DEVICE int trace_slot_mma(int unit_n, int j, int i, int k) {
-  return (unit_n == 0 && j < 64) ? 4096 + (j * 4 + i) * 2 + k : -1;
+  return (unit_n < 2 && j < 32) ? 4096 + ((unit_n * 32 + j) * 4 + i) * 2 + k : -1;
 }
 
 template <bool B>
@@ -373,6 +377,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PAC
           kv_row[b] = int(hb * a.Tk + (int64_t)(gA + b - hb * a.nseq) * a.Lk);
         }
         mbar_wait(q_empty, (n & 1) ^ 1);
+        VX_TRACE(n < 2 ? 6230 + int(n) : -1);
         mbar_expect_tx(q_full, NT * Cfg::Q_TILE_BYTES);
         for (int i = 0; i < NT; ++i) {
           int qt;
@@ -387,6 +392,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PAC
         for (int j = wi.j0; j < wi.j0 + wi.cnt; ++j, ++c) {
           const uint32_t st = c % KST, ph = (c / KST) & 1;
           mbar_wait(&k_empty[st], ph ^ 1);
+          VX_TRACE(n < 2 && j - wi.j0 < 2 ? 6240 + 2 * int(n) + (j - wi.j0) : -1);
           mbar_expect_tx(&k_full[st], nslot * Cfg::KV_TILE_BYTES);
           for (int b = 0; b < nslot; ++b)
             for (int pn = 0; pn < Cfg::PANELS; ++pn)
@@ -458,6 +464,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PAC
           auto koff = [&](int i) -> uint32_t { return PACK && ((bmask >> i) & 1) ? Cfg::KV_TILE_BYTES : 0; };
           auto voff = [&](int i) -> uint32_t { return PACK && ((bmask >> i) & 1) ? Cfg::V_STAGE_BYTES : 0; };
           mbar_wait(q_full, n & 1);
+          VX_TRACE(n < 2 ? 6100 + int(n) : -1);
           tc_fence_after();
           {  // S(0): the previous unit's P / S columns were consumed by its last PVs (in order)
             const uint32_t st = c % KST, ph = (c / KST) & 1;
@@ -467,6 +474,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PAC
             for (int i = 0; i < NT; ++i) {
               issue_qk(i, ks + koff(i));
               mma_commit_if(lead, &s_full[i]);
+              VX_TRACE(n < 2 ? 6000 + 4 * int(n) + i : -1);
             }
             mma_commit_if(lead, &k_empty[st]);
             mma_commit_if(lead && nkv == 1, q_empty);
@@ -949,6 +957,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PAC
       }
       mbar_wait(&p_free[tile], pv_cnt & 1);
       ++pv_cnt;
+      VX_TRACE(trace_slot_sm(unit_n, wl, lane, tile, nkv - 1, 5));
       tc_fence_after();
       constexpr int DL = (DO + 15) / 16 * 16;  // load width (a 72-column O reads 8 unused columns)
       uint32_t orr[DL];
@@ -983,6 +992,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PAC
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&o_empty[tile]);
+      VX_TRACE(trace_slot_sm(unit_n, wl, lane, tile, nkv - 1, 7));
       if (row_valid && !skip_unit) {
         const float inv = 1.0f / l_run;
         const int64_t orow = (int64_t)s * a.Lq + q_local;
@@ -997,6 +1007,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PAC
                                  __uint_as_float(orr[4 * c + 2]) * inv, __uint_as_float(orr[4 * c + 3]) * inv);
           a.part_lse[item * Cfg::ROWS + lr] = lse_new;
         } else if (a.merge == 0) {
+          VX_TRACE(trace_slot_sm(unit_n, wl, lane, tile, nkv - 1, 2));
           uint4* dst = reinterpret_cast<uint4*>(a.out + orow * a.ldo + h * D);
 #pragma unroll
           for (int c = 0; c < D / 8; ++c) {
@@ -1045,6 +1056,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PAC
           *lacc = lse_out;
         }
       }
+      VX_TRACE(trace_slot_sm(unit_n, wl, lane, tile, nkv - 1, 6));
     }
   }
   tc_fence_before();
