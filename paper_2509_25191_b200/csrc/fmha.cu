@@ -90,6 +90,7 @@ struct AttnArgs {
   unsigned* fix_list;
   int fix_cap;
   int fixup;
+  int out32;  // out and ldo allow 32-byte row stores
 };
 
 // work-item queue depth (shared-memory ring from the TMA producer to the MMA and softmax warps)
@@ -130,7 +131,11 @@ struct AttnCfg {
   static constexpr int DO = D + (SUMV ? 8 : 0);            // O accumulator columns (N of the PV MMA)
   static constexpr int NT = NT_;                           // 128-row Q tiles per CTA (TMEM budget)
   static constexpr int BKV = BKV_;                         // KV rows per tile (score columns)
-  static constexpr int KST = D == 128 ? 2 : (BKV <= 64 ? 4 : 3);
+  // SUMV kernels (d = 64 product kernels): one shared ones panel instead of one per V stage, and two
+  // Q buffers so a unit's Q loads while the previous unit still runs (the 64 KB reload was the
+  // largest piece of the unit-boundary gap of 29-tile frame units); packed: 3 K/V stages to fit
+  static constexpr int QBUF = SUMV_ ? 2 : 1;
+  static constexpr int KST = D == 128 ? 2 : (BKV <= 64 ? (PACK && SUMV_ ? 3 : 4) : 3);
   static constexpr int PANEL_COLS = D == 32 ? 32 : 64;     // one swizzle atom wide (<= 128 B)
   static constexpr int PANELS = D / PANEL_COLS;            // D = 128: two 64-column panels
   static constexpr uint32_t ROW_BYTES = PANEL_COLS * 2;    // bytes per row inside a panel
@@ -138,7 +143,8 @@ struct AttnCfg {
   static constexpr uint32_t KVPANEL_BYTES = BKV * ROW_BYTES;
   static constexpr uint32_t Q_TILE_BYTES = PANELS * QPANEL_BYTES;
   static constexpr uint32_t KV_TILE_BYTES = PANELS * KVPANEL_BYTES;
-  static constexpr uint32_t V_STAGE_BYTES = KV_TILE_BYTES + (SUMV ? KVPANEL_BYTES : 0);  // + ones panel
+  static constexpr uint32_t V_STAGE_BYTES = KV_TILE_BYTES;
+  static constexpr uint32_t ONES_BYTES = SUMV ? KVPANEL_BYTES : 0;  // the ones panel (second MN atom of V)
   static constexpr int SWIZZLE = D == 32 ? 64 : 128;
   static constexpr uint32_t LAYOUT = D == 32 ? 4 : 2;      // SWIZZLE_64B / SWIZZLE_128B
   static constexpr uint32_t SBO = 8 * ROW_BYTES;           // 8-row core-matrix group
@@ -147,9 +153,9 @@ struct AttnCfg {
   static constexpr uint32_t BAR_BYTES = 512;
   static constexpr uint32_t P_TILE_BYTES = PSM ? 128 * 128 : 0;  // 128 rows x 128 B (BKV <= 64 bf16 used)
   static constexpr uint32_t K_STAGE_BYTES = KV_SLOTS * KV_TILE_BYTES;   // [K_A | K_B]
-  static constexpr uint32_t VS_STAGE_BYTES = KV_SLOTS * V_STAGE_BYTES;  // [V_A ones | V_B ones]
-  static constexpr uint32_t SMEM =
-      NT * (Q_TILE_BYTES + P_TILE_BYTES) + KST * (K_STAGE_BYTES + VS_STAGE_BYTES) + 1024 + BAR_BYTES;
+  static constexpr uint32_t VS_STAGE_BYTES = KV_SLOTS * V_STAGE_BYTES;  // [V_A | V_B]
+  static constexpr uint32_t SMEM = QBUF * NT * Q_TILE_BYTES + NT * P_TILE_BYTES + KST * (K_STAGE_BYTES + VS_STAGE_BYTES) +
+                                   ONES_BYTES + 1024 + BAR_BYTES;
   // TMEM columns: S_i [BKV fp32] ... | P_i [BKV/2] (neither ALIAS nor PSM) ... | O_i [DO fp32] ...
   static constexpr uint32_t O_BASE = ((NT * BKV + (ALIAS || PSM ? 0 : NT * BKV / 2)) + 31) / 32 * 32;
   static_assert(O_BASE + NT * DO <= 512, "TMEM budget");
@@ -257,14 +263,16 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PAC
   // visible to the compiler: LDS/STS instead of generic loads)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   constexpr int NT = Cfg::NT;
-  uint8_t* sQ = smem;                                 // NT tiles
-  [[maybe_unused]] uint8_t* sP = sQ + NT * Cfg::Q_TILE_BYTES;  // PSM: NT P tiles (1024-aligned)
+  constexpr int QB = Cfg::QBUF;
+  uint8_t* sQ = smem;                                 // QB x NT tiles
+  [[maybe_unused]] uint8_t* sP = sQ + QB * NT * Cfg::Q_TILE_BYTES;  // PSM: NT P tiles (1024-aligned)
   uint8_t* sK = sP + NT * Cfg::P_TILE_BYTES;          // KST stages (K tile per slot)
-  uint8_t* sV = sK + KST * Cfg::K_STAGE_BYTES;        // KST stages (V tile [+ ones panel] per slot)
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sV + KST * Cfg::VS_STAGE_BYTES);
-  uint64_t* q_full = bar;
-  uint64_t* q_empty = bar + 1;
-  uint64_t* k_full = bar + 2;
+  uint8_t* sV = sK + KST * Cfg::K_STAGE_BYTES;        // KST stages (V tile per slot)
+  [[maybe_unused]] uint8_t* sOnes = sV + KST * Cfg::VS_STAGE_BYTES;  // SUMV: the ones panel (1024-aligned)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sOnes + Cfg::ONES_BYTES);
+  uint64_t* q_full = bar;       // [QB]
+  uint64_t* q_empty = bar + QB;  // [QB]
+  uint64_t* k_full = bar + 2 * QB;
   uint64_t* k_empty = k_full + KST;
   uint64_t* v_full = k_empty + KST;
   uint64_t* v_empty = v_full + KST;
@@ -288,8 +296,10 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PAC
     tma_prefetch_desc(&tmQ);
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
-    mbar_init(q_full, 1);
-    mbar_init(q_empty, 1);
+    for (int b = 0; b < QB; ++b) {
+      mbar_init(&q_full[b], 1);
+      mbar_init(&q_empty[b], 1);
+    }
     for (int s = 0; s < KST; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&k_empty[s], 1);
@@ -315,13 +325,10 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PAC
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, 512);
-  if constexpr (SUMV) {  // the constant ones panel of every V stage (read by the tensor core)
+  if constexpr (SUMV) {  // the constant ones panel every V stage's descriptor points its second atom at
     const uint32_t ones = 0x3f803f80u;  // bf16x2 (1, 1)
-    for (uint32_t o = threadIdx.x * 16; o < KST * Cfg::KV_SLOTS * Cfg::KVPANEL_BYTES; o += Cfg::THREADS * 16) {
-      const uint32_t st = o / Cfg::KVPANEL_BYTES, off = o % Cfg::KVPANEL_BYTES;  // st: stage x slot
-      *reinterpret_cast<uint4*>(sV + st * Cfg::V_STAGE_BYTES + Cfg::KV_TILE_BYTES + off) =
-          make_uint4(ones, ones, ones, ones);
-    }
+    for (uint32_t o = threadIdx.x * 16; o < Cfg::ONES_BYTES; o += Cfg::THREADS * 16)
+      *reinterpret_cast<uint4*>(sOnes + o) = make_uint4(ones, ones, ones, ones);
     fence_proxy_async_smem();
   }
   tc_fence_before();
@@ -376,9 +383,10 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PAC
           const int hb = (gA + b) / a.nseq;
           kv_row[b] = int(hb * a.Tk + (int64_t)(gA + b - hb * a.nseq) * a.Lk);
         }
-        mbar_wait(q_empty, (n & 1) ^ 1);
+        const uint32_t qb = QB == 2 ? (n & 1) : 0, qph = QB == 2 ? ((n >> 1) & 1) : (n & 1);
+        mbar_wait(&q_empty[qb], qph ^ 1);
         VX_TRACE(n < 2 ? 6230 + int(n) : -1);
-        mbar_expect_tx(q_full, NT * Cfg::Q_TILE_BYTES);
+        mbar_expect_tx(&q_full[qb], NT * Cfg::Q_TILE_BYTES);
         for (int i = 0; i < NT; ++i) {
           int qt;
           const int g = tile_seq(t0 + i, qt);
@@ -386,7 +394,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PAC
           // tiles past the last one (packed, final unit only) load any rows; their output is dropped
           const int q_row = t0 + i < a.total_tiles ? int(hq * a.Tq + (int64_t)(g - hq * a.nseq) * a.Lq + qt * 128) : 0;
           for (int pn = 0; pn < Cfg::PANELS; ++pn)
-            tma_load_2d_hint(sQ + i * Cfg::Q_TILE_BYTES + pn * Cfg::QPANEL_BYTES, &tmQ, q_full,
+            tma_load_2d_hint(sQ + (qb * NT + i) * Cfg::Q_TILE_BYTES + pn * Cfg::QPANEL_BYTES, &tmQ, &q_full[qb],
                              pn * Cfg::PANEL_COLS, q_row, pol_q);
         }
         for (int j = wi.j0; j < wi.j0 + wi.cnt; ++j, ++c) {
@@ -420,12 +428,13 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PAC
       // descriptors: one base per operand, offsets added in 16-byte units (smem addresses < 256 KB
       // keep the 14-bit start-address field from carrying into the next field)
       const uint64_t qdesc0 = make_sdesc(q0, 16, Cfg::SBO, Cfg::LAYOUT);
+      uint32_t qsel = 0;  // byte offset of this unit's Q buffer
       auto issue_qk = [&](int i, uint32_t ks, bool issue = true) {
         const uint64_t kd = make_sdesc(ks, 16, Cfg::SBO, Cfg::LAYOUT);
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
           const uint32_t kstep = (k % KSTEPS_PER_PANEL) * 32;
-          const uint32_t qoff = i * Cfg::Q_TILE_BYTES + (k / KSTEPS_PER_PANEL) * Cfg::QPANEL_BYTES + kstep;
+          const uint32_t qoff = qsel + i * Cfg::Q_TILE_BYTES + (k / KSTEPS_PER_PANEL) * Cfg::QPANEL_BYTES + kstep;
           const uint32_t koff = (k / KSTEPS_PER_PANEL) * Cfg::KVPANEL_BYTES + kstep;
           mma_ss_if(lead && issue, tmem + Cfg::tS(i), qdesc0 + (qoff >> 4), kd + (koff >> 4), idesc_qk, k > 0);
         }
@@ -433,7 +442,8 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PAC
       // V is the MN-major B operand: for D = 128 its two 64-column panels are the two MN atoms (LBO)
       [[maybe_unused]] const uint64_t pdesc0 = make_sdesc(smem_u32(sP), 16, 1024, 2);  // PSM: K-major SW128
       auto issue_pv = [&](int i, uint32_t vs, uint32_t acc) {
-        const uint64_t vd = make_sdesc(vs, Cfg::KVPANEL_BYTES, Cfg::SBO, Cfg::LAYOUT);
+        // SUMV: the second MN atom (LBO away) is the shared ones panel
+        const uint64_t vd = make_sdesc(vs, SUMV ? smem_u32(sOnes) - vs : Cfg::KVPANEL_BYTES, Cfg::SBO, Cfg::LAYOUT);
 #pragma unroll
         for (int kk = 0; kk < BKV / 16; ++kk) {
           if constexpr (PSM)  // P_i from shared memory: 16 bf16 = 32 bytes per k-step within the 128-B row
@@ -463,7 +473,9 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PAC
           }
           auto koff = [&](int i) -> uint32_t { return PACK && ((bmask >> i) & 1) ? Cfg::KV_TILE_BYTES : 0; };
           auto voff = [&](int i) -> uint32_t { return PACK && ((bmask >> i) & 1) ? Cfg::V_STAGE_BYTES : 0; };
-          mbar_wait(q_full, n & 1);
+          const uint32_t qb = QB == 2 ? (n & 1) : 0, qph = QB == 2 ? ((n >> 1) & 1) : (n & 1);
+          qsel = qb * NT * Cfg::Q_TILE_BYTES;
+          mbar_wait(&q_full[qb], qph);
           VX_TRACE(n < 2 ? 6100 + int(n) : -1);
           tc_fence_after();
           {  // S(0): the previous unit's P / S columns were consumed by its last PVs (in order)
@@ -477,7 +489,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PAC
               VX_TRACE(n < 2 ? 6000 + 4 * int(n) + i : -1);
             }
             mma_commit_if(lead, &k_empty[st]);
-            mma_commit_if(lead && nkv == 1, q_empty);
+            mma_commit_if(lead && nkv == 1, &q_empty[qb]);
           }
           for (int j = 0; j < nkv; ++j, ++c) {
             const uint32_t st = c % KST, ph = (c / KST) & 1;
@@ -508,7 +520,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PAC
             mma_commit_if(lead, &v_empty[st]);
             if (has_next) {
               mma_commit_if(lead, &k_empty[nst]);
-              mma_commit_if(lead && j + 2 == nkv, q_empty);
+              mma_commit_if(lead && j + 2 == nkv, &q_empty[qb]);
             }
           }
         }
@@ -1008,14 +1020,27 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PAC
           a.part_lse[item * Cfg::ROWS + lr] = lse_new;
         } else if (a.merge == 0) {
           VX_TRACE(trace_slot_sm(unit_n, wl, lane, tile, nkv - 1, 2));
-          uint4* dst = reinterpret_cast<uint4*>(a.out + orow * a.ldo + h * D);
+          __nv_bfloat16* orow_p = a.out + orow * a.ldo + h * D;
+#define VX_O(i) (__uint_as_float(orr[i]) * inv)
+          if (a.out32) {  // 32-byte stores: each lane writes whole sectors, half the store transactions
 #pragma unroll
-          for (int c = 0; c < D / 8; ++c) {
-#define VX_O(i) (__uint_as_float(orr[8 * c + i]) * inv)
-            dst[c] = make_uint4(pack_bf16(VX_O(0), VX_O(1)), pack_bf16(VX_O(2), VX_O(3)),
-                                pack_bf16(VX_O(4), VX_O(5)), pack_bf16(VX_O(6), VX_O(7)));
-#undef VX_O
+            for (int c = 0; c < D / 16; ++c) {
+              const int b = 16 * c;
+              st_global_v8(orow_p + b, pack_bf16(VX_O(b), VX_O(b + 1)), pack_bf16(VX_O(b + 2), VX_O(b + 3)),
+                           pack_bf16(VX_O(b + 4), VX_O(b + 5)), pack_bf16(VX_O(b + 6), VX_O(b + 7)),
+                           pack_bf16(VX_O(b + 8), VX_O(b + 9)), pack_bf16(VX_O(b + 10), VX_O(b + 11)),
+                           pack_bf16(VX_O(b + 12), VX_O(b + 13)), pack_bf16(VX_O(b + 14), VX_O(b + 15)));
+            }
+          } else {
+            uint4* dst = reinterpret_cast<uint4*>(orow_p);
+#pragma unroll
+            for (int c = 0; c < D / 8; ++c) {
+              const int b = 8 * c;
+              dst[c] = make_uint4(pack_bf16(VX_O(b), VX_O(b + 1)), pack_bf16(VX_O(b + 2), VX_O(b + 3)),
+                                  pack_bf16(VX_O(b + 4), VX_O(b + 5)), pack_bf16(VX_O(b + 6), VX_O(b + 7)));
+            }
           }
+#undef VX_O
           if (a.lse) a.lse[h * a.Tq + orow] = lse_new;
         } else {
           // ring step: log-sum-exp merge with the running (O, lse) of the blocks seen so far
@@ -1324,6 +1349,7 @@ static int attention_impl(const void* q, const void* k, const void* v, void* out
   a.scale_log2 = q_log2 ? 1.0f : (1.0f / sqrtf(float(D))) * 1.4426950408889634f;
   a.out = reinterpret_cast<__nv_bfloat16*>(out);
   a.ldo = ldo;
+  a.out32 = out && (reinterpret_cast<uintptr_t>(out) % 32 == 0) && (ldo % 16 == 0) && (D % 16 == 0);
   a.lse = lse;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (D == 64) {
