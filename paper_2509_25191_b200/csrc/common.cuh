@@ -410,6 +410,18 @@ VX_DEVICE void st_global_v8(void* p, uint32_t a0, uint32_t a1, uint32_t a2, uint
                "r"(a4), "r"(a5), "r"(a6), "r"(a7)
                : "memory");
 }
+// 64 bytes (16 packed words, e.g. 32 bf16) to global memory: two 32-byte stores when p is 32-byte
+// aligned (whole sectors per lane), else four 16-byte ones
+VX_DEVICE void store_64b(void* p, const uint32_t* w) {
+  if ((reinterpret_cast<uintptr_t>(p) & 31u) == 0) {
+    st_global_v8(p, w[0], w[1], w[2], w[3], w[4], w[5], w[6], w[7]);
+    st_global_v8(reinterpret_cast<uint8_t*>(p) + 32, w[8], w[9], w[10], w[11], w[12], w[13], w[14], w[15]);
+  } else {
+    uint4* d = reinterpret_cast<uint4*>(p);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) d[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+  }
+}
 VX_DEVICE void st_shared_f32(uint32_t addr, float v) {
   asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
 }

@@ -117,15 +117,14 @@ VX_DEVICE void epi_chunk32(const GemmArgs& a, int row, int col, const uint32_t* 
   }
   if (row >= a.M) return;
   if constexpr (EPI == VX_EPI_BF16 || EPI == VX_EPI_GELU) {
-    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(e.out) + (size_t)row * e.ldo + col);
+    uint32_t w[16];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      float t[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) t[u] = (EPI == VX_EPI_GELU) ? gelu_erf_fast(v[8 * j + u]) : v[8 * j + u];
-      dst[j] = make_uint4(pack_bf16(t[0], t[1]), pack_bf16(t[2], t[3]), pack_bf16(t[4], t[5]),
-                          pack_bf16(t[6], t[7]));
+    for (int u = 0; u < 16; ++u) {
+      const float t0 = (EPI == VX_EPI_GELU) ? gelu_erf_fast(v[2 * u]) : v[2 * u];
+      const float t1 = (EPI == VX_EPI_GELU) ? gelu_erf_fast(v[2 * u + 1]) : v[2 * u + 1];
+      w[u] = pack_bf16(t0, t1);
     }
+    store_64b(reinterpret_cast<__nv_bfloat16*>(e.out) + (size_t)row * e.ldo + col, w);
   } else if constexpr (EPI == VX_EPI_F32) {
     float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(e.out) + (size_t)row * e.ldo + col);
 #pragma unroll
@@ -214,15 +213,19 @@ VX_DEVICE void epi_qkv_head(const GemmArgs& a, int row, int col, float* v) {
     }
   }
   __nv_bfloat16* base = reinterpret_cast<__nv_bfloat16*>(which == 0 ? e.q : (which == 1 ? e.k : e.v));
-  uint4* dst = reinterpret_cast<uint4*>(base + ((size_t)h * e.tokens_total + row) * D);
+  // a head row is D * 2 = 64 or 128 bytes at a multiple of its size: 32-byte stores (whole sectors)
+  __nv_bfloat16* dst = base + ((size_t)h * e.tokens_total + row) * D;
   if (which == 0 && e.q_scale != 0.f) {
 #pragma unroll
     for (int j = 0; j < D; ++j) v[j] *= e.q_scale;
   }
 #pragma unroll
-  for (int j = 0; j < D / 8; ++j)
-    dst[j] = make_uint4(pack_bf16(v[8 * j], v[8 * j + 1]), pack_bf16(v[8 * j + 2], v[8 * j + 3]),
-                        pack_bf16(v[8 * j + 4], v[8 * j + 5]), pack_bf16(v[8 * j + 6], v[8 * j + 7]));
+  for (int j = 0; j < D / 16; ++j) {
+    const float* w = v + 16 * j;
+    st_global_v8(dst + 16 * j, pack_bf16(w[0], w[1]), pack_bf16(w[2], w[3]), pack_bf16(w[4], w[5]),
+                 pack_bf16(w[6], w[7]), pack_bf16(w[8], w[9]), pack_bf16(w[10], w[11]), pack_bf16(w[12], w[13]),
+                 pack_bf16(w[14], w[15]));
+  }
 }
 
 // q/k/v scatter without qk-norm / RoPE (camera-head trunk, head_dim = e.head_dim, any multiple of
@@ -350,22 +353,16 @@ VX_DEVICE void epi_spatial32(const GemmArgs& a, const PixInfo& pi, int col, cons
     }
   }
   {
-    uint4* d = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(sp.out1) +
-                                        pix_index(pi.f, yo, xo, Ho, Wo, sp.out1_pad) * Cout + c);
+    uint32_t w[16];
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-      d[q] = make_uint4(pack_bf16(v[8 * q], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
-                        pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+    for (int u = 0; u < 16; ++u) w[u] = pack_bf16(v[2 * u], v[2 * u + 1]);
+    store_64b(reinterpret_cast<__nv_bfloat16*>(sp.out1) + pix_index(pi.f, yo, xo, Ho, Wo, sp.out1_pad) * Cout + c, w);
   }
   if (sp.out2) {
-    uint4* d = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(sp.out2) +
-                                        pix_index(pi.f, yo, xo, Ho, Wo, sp.out2_pad) * Cout + c);
+    uint32_t w[16];
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-      d[q] = make_uint4(pack_bf16(fmaxf(v[8 * q], 0.f), fmaxf(v[8 * q + 1], 0.f)),
-                        pack_bf16(fmaxf(v[8 * q + 2], 0.f), fmaxf(v[8 * q + 3], 0.f)),
-                        pack_bf16(fmaxf(v[8 * q + 4], 0.f), fmaxf(v[8 * q + 5], 0.f)),
-                        pack_bf16(fmaxf(v[8 * q + 6], 0.f), fmaxf(v[8 * q + 7], 0.f)));
+    for (int u = 0; u < 16; ++u) w[u] = pack_bf16(fmaxf(v[2 * u], 0.f), fmaxf(v[2 * u + 1], 0.f));
+    store_64b(reinterpret_cast<__nv_bfloat16*>(sp.out2) + pix_index(pi.f, yo, xo, Ho, Wo, sp.out2_pad) * Cout + c, w);
   }
 }
 
