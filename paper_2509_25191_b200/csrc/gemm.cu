@@ -238,16 +238,15 @@ VX_DEVICE void epi_qkv_scatter32(const GemmArgs& a, int row, int col, const uint
   const int hc = col - which * C;
   const int h = hc / e.head_dim, off = hc - h * e.head_dim;
   __nv_bfloat16* base = reinterpret_cast<__nv_bfloat16*>(which == 0 ? e.q : (which == 1 ? e.k : e.v));
-  uint4* dst = reinterpret_cast<uint4*>(base + ((size_t)h * e.tokens_total + row) * e.head_dim + off);
   const float qs = which == 0 && e.q_scale != 0.f ? e.q_scale : 1.0f;
-#define VX_QV(i, bb) ((__uint_as_float(r[8 * j + i]) + bb) * qs)
+  uint32_t w[16];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const float4 b0 = pre.b[2 * j], b1 = pre.b[2 * j + 1];
-    dst[j] = make_uint4(pack_bf16(VX_QV(0, b0.x), VX_QV(1, b0.y)), pack_bf16(VX_QV(2, b0.z), VX_QV(3, b0.w)),
-                        pack_bf16(VX_QV(4, b1.x), VX_QV(5, b1.y)), pack_bf16(VX_QV(6, b1.z), VX_QV(7, b1.w)));
+  for (int j = 0; j < 8; ++j) {
+    const float4 bb = pre.b[j];
+    w[2 * j] = pack_bf16((__uint_as_float(r[4 * j]) + bb.x) * qs, (__uint_as_float(r[4 * j + 1]) + bb.y) * qs);
+    w[2 * j + 1] = pack_bf16((__uint_as_float(r[4 * j + 2]) + bb.z) * qs, (__uint_as_float(r[4 * j + 3]) + bb.w) * qs);
   }
-#undef VX_QV
+  store_64b(base + ((size_t)h * e.tokens_total + row) * e.head_dim + off, w);
 }
 
 // ---------------------------------------------------------------------------
