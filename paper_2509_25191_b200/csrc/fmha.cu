@@ -978,7 +978,11 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PAC
       if constexpr (SUMV) l_run = __uint_as_float(orr[D]);  // sum_k P_ik from the ones panel
       [[maybe_unused]] bool skip_unit = false;
       if constexpr (NOMAX) {
-        // trustworthy iff the row sum is well inside the normal fp32 range and O is finite (O <= l max|v|)
+        // trustworthy iff 1e-30 < l < 1e30 and the O row is finite. The upper bound matters: every P is at
+        // most l, so l < 1e30 (~2^100) proves every exponent was below 100, and the FMA-pipe exp2 (exponent
+        // inserted into the float bits) is only valid below 2^128 — above that it wraps instead of giving
+        // inf (measured: an upper bound of 3e38 lets large-logit rows through with 2e-2 errors). The
+        // lower bound keeps the row's largest P far from the 2^-126 flush.
         uint64_t c4[4] = {0, 0, 0, 0};  // packed partial sums (NaN / inf propagate), a short dependency chain
 #pragma unroll
         for (int c = 0; c < D / 2; ++c)
