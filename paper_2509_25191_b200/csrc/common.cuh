@@ -432,11 +432,17 @@ VX_DEVICE float ld_shared_f32(uint32_t addr) {
 }
 // two 2^x at once on the FMA pipe (packed polynomial); returns (2^lo, 2^hi).
 // DEG 3: rel. err 2.2e-4; DEG 2: rel. err 1.8e-3 (below the bf16 rounding P receives anyway)
-template <int DEG = 3>
+// SAT_HI also clamps x at 127 (the exponent insertion below wraps into the sign bit past 2^128 instead
+// of saturating; callers whose x is not bounded by a subtracted row max need it)
+template <int DEG = 3, bool SAT_HI = false>
 VX_DEVICE void ex2_poly2(float x0, float x1, float& y0, float& y1) {
   const uint64_t MAGIC = f2_pack(12582912.0f, 12582912.0f);
   const uint64_t NMAGIC = f2_pack(-12582912.0f, -12582912.0f);
   const uint64_t NEG1 = f2_pack(-1.0f, -1.0f);
+  if constexpr (SAT_HI) {
+    x0 = fminf(x0, 127.0f);
+    x1 = fminf(x1, 127.0f);
+  }
   const uint64_t x = f2_pack(fmaxf(x0, -126.0f), fmaxf(x1, -126.0f));
   const uint64_t t = f2_add(x, MAGIC);
   const uint64_t f = f2_fma(f2_add(t, NMAGIC), NEG1, x);

@@ -635,7 +635,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PAC
               float x0, x1, p0, p1;
               f2_unpack(x, x0, x1);
               if ((c & 7) >= 8 - EMU_PAIRS_OF_8) {
-                ex2_poly2<2>(x0, x1, p0, p1);
+                ex2_poly2<2, true>(x0, x1, p0, p1);
               } else {
                 p0 = ex2(x0);
                 p1 = ex2(x1);
@@ -849,7 +849,7 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PAC
               float x0, x1, p0, p1;
               f2_unpack(x, x0, x1);
               if ((c & 7) >= 8 - EMU_PAIRS_OF_8) {
-                ex2_poly2<2>(x0, x1, p0, p1);
+                ex2_poly2<2, NOMAX>(x0, x1, p0, p1);
               } else {
                 p0 = ex2(x0);
                 p1 = ex2(x1);

@@ -427,6 +427,25 @@ def test_attention_ring_merge_matches_full(ops, shards, Lq, q_log2):
     assert (lse - lse_ref).abs().max().item() < 1e-2
 
 
+@pytest.mark.parametrize("key", [14, 15, 30, 47, 5])
+def test_attention_max_free_single_huge_logit(ops, key):
+    # one query row whose only large score (~160 in log2 units, past 2^128) sits on key `key`:
+    # columns 12-15 / 28-31 / 44-47 of a 48-wide KV tile take the FMA-pipe exp2, whose exponent
+    # insertion must saturate (not wrap) so the row is flagged and recomputed; the answer is v[key]
+    H, D, L = 1, 64, 96
+    q = _bf(H, L, D, scale=0.01, seed=80)
+    k = _bf(H, L, D, scale=0.01, seed=81)
+    v = _bf(H, L, D, seed=82)
+    q[0, 0, 0] = 30.0
+    k[0, key, 0] = 30.0
+    out = torch.empty(L, H * D, device="cuda", dtype=torch.bfloat16)
+    ops.attention(q, k, v, out, 1, L, L)
+    ref, _ = _sdpa_ref(q, k, v, 1, L, L)
+    assert torch.isfinite(out.float()).all()
+    assert rel(out[:1], v[0, key:key + 1].float()) < 1e-2
+    assert rel(out, ref) < 1e-2
+
+
 @pytest.mark.parametrize("warm", [True, False])
 def test_attention_under_graph_capture(ops, warm):
     # warm stream: the max-free launch and its fixup are captured (per-stream words and list exist);
