@@ -335,29 +335,6 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PAC
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-#if VX_FMHA_QFAKE
-  constexpr bool QFAKE_OK = D == 64 && Cfg::O_BASE + NT * Cfg::DO <= 480 && !PSM_;
-  if constexpr (QFAKE_OK) {
-    if (warp >= 4 && warp < 8) {
-      uint32_t z[32];
-#pragma unroll
-      for (int c = 0; c < 32; ++c) {  // pseudo-random bf16 pairs in (-2, 2): realistic operand toggling
-        uint32_t hsh = (lane * 32 + c + 1) * 2654435761u ^ (warp * 40503u);
-        hsh ^= hsh >> 13;
-        hsh *= 0x5bd1e995u;
-        hsh ^= hsh >> 15;
-        const float f0 = (float(hsh & 0xffffu) / 32768.0f - 1.0f) * 2.0f;
-        const float f1 = (float(hsh >> 16) / 32768.0f - 1.0f) * 2.0f;
-        z[c] = pack_bf16(f0, f1);
-      }
-      tmem_st32(tmem + (uint32_t((warp & 3) * 32) << 16) + 480, z);
-      tmem_wait_st();
-    }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-  }
-#endif
 
   // tile t of the (head, sequence, tile) numbering -> sequence g = head * nseq + seq, tile in sequence
   auto tile_seq = [&](int t, int& qt) -> int {
@@ -459,13 +436,6 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PAC
           const uint32_t kstep = (k % KSTEPS_PER_PANEL) * 32;
           const uint32_t qoff = qsel + i * Cfg::Q_TILE_BYTES + (k / KSTEPS_PER_PANEL) * Cfg::QPANEL_BYTES + kstep;
           const uint32_t koff = (k / KSTEPS_PER_PANEL) * Cfg::KVPANEL_BYTES + kstep;
-#if VX_FMHA_QFAKE
-          // diagnostic upper bound: A (= Q) read from 32 zeroed spare TMEM columns instead of shared memory
-          if constexpr (QFAKE_OK) {
-            mma_ts_if(lead && issue, tmem + Cfg::tS(i), tmem + 480 + k * 8, kd + (koff >> 4), idesc_qk, k > 0);
-            continue;
-          }
-#endif
           mma_ss_if(lead && issue, tmem + Cfg::tS(i), qdesc0 + (qoff >> 4), kd + (koff >> 4), idesc_qk, k > 0);
         }
       };
