@@ -87,3 +87,41 @@ def test_ring_fused_merge_matches_global_attention(S, world, monkeypatch):
         err = ((o.float() - ref[sl]).norm() / ref[sl].norm()).item()
         assert err < 1e-2, (rank, err)
         assert fake.step == world - 1
+
+
+@pytest.mark.gpu
+def test_ring_over_nccl_loopback(tmp_path):
+    """The ring's exchange through real NCCL P2P (ring.TorchDistComm, a world-size-1 group sending to
+    itself; tests/nccl_loopback_worker.py): every virtual rank's merged output equals one attention
+    call, over two layers, with the receive buffer zeroed before each transfer; and the whole
+    VGGT(dist=True) forward over the same transport equals a single-GPU forward of rank 0's views."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    out = tmp_path / "loopback.json"
+    env = dict(os.environ, OUT=str(out), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    r = subprocess.run([sys.executable, os.path.join(root, "tests", "nccl_loopback_worker.py")], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    res = json.loads(out.read_text())
+    assert [c["world"] for c in res["ring"]] == [2, 3, 4]
+    for c in res["ring"]:
+        assert c["transfers"] == 2 * (c["world"] - 1), c  # g - 1 NCCL steps per layer, two layers
+        assert max(c["rel_err"]) < 1e-2, c
+    f = res["forward"]
+    assert f["frame_offset"] == 0 and f["local_views"] == 3, f
+    assert f["transfers"] == f["layers"], f  # one ring step per global layer at g = 2
+    assert f["gathers"] >= 1, f  # the camera tokens
+    for k in ("depth", "depth_conf", "world_points", "world_points_conf", "pose"):
+        assert f[k] < 1e-2, (k, f)
+    assert f["pose_copies"] < 1e-5, f
