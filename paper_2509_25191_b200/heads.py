@@ -279,10 +279,6 @@ class DPTHeadDevice:
         cfg = self.W.cfg
         layers = [kept[i] for i in cfg.kept_layers]
         S = layers[0].shape[0]
-        # balanced chunks of at most `chunk` views (20 views: 10 + 10, not 16 + 4), so the last chunk's
-        # kernels still fill the GPU
-        n = -(-S // chunk)
-        size = -(-S // n) if n else chunk
-        for s0 in range(0, S, size):
-            s1 = min(S, s0 + size)
+        for s0 in range(0, S, chunk):
+            s1 = min(S, s0 + chunk)
             self.forward_chunk([l[s0:s1] for l in layers], out_pred[s0:s1], out_conf[s0:s1])
