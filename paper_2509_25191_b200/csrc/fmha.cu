@@ -46,6 +46,9 @@
 #ifndef VX_FMHA_NOMAX_EMU  // exp pairs (of 8) on the FMA pipe in the max-free kernel
 #define VX_FMHA_NOMAX_EMU 2
 #endif
+#ifndef VX_FMHA_ONES_ALL  // 1: the row-sum panel all ones (round-2 builds before the single ones column)
+#define VX_FMHA_ONES_ALL 0
+#endif
 #ifndef VX_FMHA_NOMAX_W64  // max-free kernel with 64-wide KV tiles and FADD row sums
 #define VX_FMHA_NOMAX_W64 0
 #endif
@@ -326,9 +329,21 @@ __global__ void __launch_bounds__(AttnCfg<D, NT_, BKV_, ALIAS_, SUMV_, PSM_, PAC
   }
   if (warp == 2) tmem_alloc(tmem_slot, 512);
   if constexpr (SUMV) {  // the constant ones panel every V stage's descriptor points its second atom at
+#if VX_FMHA_ONES_ALL
     const uint32_t ones = 0x3f803f80u;  // bf16x2 (1, 1)
     for (uint32_t o = threadIdx.x * 16; o < Cfg::ONES_BYTES; o += Cfg::THREADS * 16)
       *reinterpret_cast<uint4*>(sOnes + o) = make_uint4(ones, ones, ones, ones);
+#else
+    // one column of ones (MN index 0 -> O column D = the row sum), zeros in the other 7 columns the PV
+    // MMA reads (N = D + 8): zero operands cost the tensor core less switching energy under the power
+    // cap. SW128 MN-major rows of 128 B, one per key: logical 16-byte chunk 0 of row r sits at
+    // physical chunk r % 8 (the panel is 1024-byte aligned).
+    for (uint32_t o = threadIdx.x * 16; o < Cfg::ONES_BYTES; o += Cfg::THREADS * 16) {
+      const uint32_t row = o >> 7, chunk = (o >> 4) & 7;
+      const uint32_t w0 = (chunk ^ (row & 7)) == 0 ? 0x3f80u : 0u;  // bf16 1.0 in the chunk's first element
+      *reinterpret_cast<uint4*>(sOnes + o) = make_uint4(w0, 0u, 0u, 0u);
+    }
+#endif
     fence_proxy_async_smem();
   }
   tc_fence_before();
@@ -1183,13 +1198,23 @@ __global__ void __launch_bounds__(256) fmha_split_merge(const AttnArgs a) {
   if (g == 0) a.lse[h * a.Tq + orow] = lse_out;
 }
 
+// The per-stream device buffers below are keyed by (current device, stream): the legacy default
+// stream has the same handle on every device, and a buffer belongs to the device it was allocated on.
+using StreamKey = std::pair<int, cudaStream_t>;
+static StreamKey stream_key(cudaStream_t st) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return {dev, st};
+}
+
 // Per-stream scratch for the KV-split tail (at most one wave of items: num_sms x ROWS x (D + 1)
 // fp32). Allocated once per stream and kept; not allocated while the stream is being captured.
 static float* split_scratch(cudaStream_t st, size_t floats) {
   static std::mutex mu;
-  static std::map<cudaStream_t, std::pair<float*, size_t>> bufs;
+  static std::map<StreamKey, std::pair<float*, size_t>> bufs;
   std::lock_guard<std::mutex> lock(mu);
-  auto it = bufs.find(st);
+  const StreamKey key = stream_key(st);
+  auto it = bufs.find(key);
   if (it != bufs.end() && it->second.second >= floats) return it->second.first;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
@@ -1202,7 +1227,7 @@ static float* split_scratch(cudaStream_t st, size_t floats) {
     cudaStreamSynchronize(st);
     cudaFree(it->second.first);
   }
-  bufs[st] = {p, floats};
+  bufs[key] = {p, floats};
   return p;
 }
 
@@ -1211,9 +1236,10 @@ static float* split_scratch(cudaStream_t st, size_t floats) {
 // kernel only).
 static unsigned* fix_buffer(cudaStream_t st, int64_t cap) {
   static std::mutex mu;
-  static std::map<cudaStream_t, std::pair<unsigned*, int64_t>> bufs;
+  static std::map<StreamKey, std::pair<unsigned*, int64_t>> bufs;
   std::lock_guard<std::mutex> lock(mu);
-  auto it = bufs.find(st);
+  const StreamKey key = stream_key(st);
+  auto it = bufs.find(key);
   if (it != bufs.end() && it->second.second >= cap) return it->second.first;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
@@ -1226,7 +1252,7 @@ static unsigned* fix_buffer(cudaStream_t st, int64_t cap) {
     cudaStreamSynchronize(st);
     cudaFree(it->second.first);
   }
-  bufs[st] = {p, cap};
+  bufs[key] = {p, cap};
   return p;
 }
 
@@ -1242,9 +1268,10 @@ static unsigned* sched_counters(cudaStream_t st) {
   }
 #endif
   static std::mutex mu;
-  static std::map<cudaStream_t, unsigned*> ctrs;
+  static std::map<StreamKey, unsigned*> ctrs;
   std::lock_guard<std::mutex> lock(mu);
-  auto it = ctrs.find(st);
+  const StreamKey key = stream_key(st);
+  auto it = ctrs.find(key);
   if (it != ctrs.end()) return it->second;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
@@ -1253,7 +1280,7 @@ static unsigned* sched_counters(cudaStream_t st) {
     cudaGetLastError();
     return nullptr;
   }
-  ctrs[st] = p;
+  ctrs[key] = p;
   return p;
 }
 
