@@ -132,7 +132,9 @@ class DPTHeadDevice:
 
     def __init__(self, W: DeviceWeights, head: str, activation: str):
         self.W, self.head, self.activation = W, head, activation
-        self._bufs: Dict[tuple, torch.Tensor] = {}  # zero-bordered activation buffers, see _pad
+        self._bufs: Dict[tuple, torch.Tensor] = {}  # zero-bordered activation buffers, see _pad / prepare
+        self._prepared = False
+        self._zeroed = False
         cfg = W.cfg
         dev = W.patch_w.device
         g = cfg.grid
@@ -170,13 +172,56 @@ class DPTHeadDevice:
         self.head_w = hw.reshape(hw.shape[0], -1).float().contiguous()
         self.head_b = W[head + "scratch.output_conv2.2.bias"].float().contiguous()
 
+    def buffer_plan(self) -> List[tuple]:
+        """The (slot, H, W, C) of every zero-bordered buffer forward_chunk uses (see _pad)."""
+        cfg = self.W.cfg
+        g, oc, Fh, img = cfg.grid, cfg.dpt_out_channels, cfg.dpt_features, cfg.img_size
+        sizes = [4 * g, 2 * g, g, (g + 1) // 2]
+        sc = self.head + "scratch."
+        plan = [("f0", sizes[0], sizes[0], oc[0]), ("f1", sizes[1], sizes[1], oc[1]), ("f2", g, g, oc[2]),
+                ("y3", g, g, oc[3]), ("f3", sizes[3], sizes[3], oc[3])]
+        plan += [(f"{n}{i}", sizes[i], sizes[i], Fh) for i in range(4) for n in ("l", "lr")]
+        plan.append((f"{sc}refinenet4.resConfUnit2.h", sizes[3], sizes[3], Fh))
+        for r, li in ((3, 2), (2, 1), (1, 0)):
+            hs = sizes[li]
+            plan += [(f"{sc}refinenet{r}.resConfUnit1.{n}", hs, hs, Fh) for n in ("h", "o", "o2")]
+            plan.append((f"{sc}refinenet{r}.resConfUnit2.h", hs, hs, Fh))
+        plan += [("oc1", 2 * sizes[0], 2 * sizes[0], Fh), ("u", img, img, Fh // 2)]
+        return plan
+
+    def prepare(self, frames: int, dev) -> None:
+        """Allocate this forward's zero-bordered buffers for chunks of up to `frames` views from the
+        CURRENT stream's pool; their borders are zeroed by the head's first call on its own stream (the
+        producing kernels overwrite the whole interior). VGGT.forward calls this on the main stream before
+        the head streams wait on it and `release()`s after the main stream has waited for them, so the
+        memory returns to the main stream's pool and the next forward's aggregator reuses it; nothing is
+        held between forwards."""
+        self._bufs = {(slot, H, W, C): torch.empty(frames, H + 2, W + 2, C, device=dev, dtype=torch.bfloat16)
+                      for slot, H, W, C in self.buffer_plan()}
+        self._prepared = True
+        self._zeroed = False
+
+    def _zero_borders(self) -> None:
+        """Zero the border rows and columns of the prepared buffers on the current stream (the head's
+        own stream, which has waited for the main stream): two strided fills per buffer."""
+        for (_, H, W, C), b in self._bufs.items():
+            b[:, 0::H + 1].zero_()                                   # rows 0 and H+1
+            b.view(-1, W + 2, C)[:, 0::W + 1].zero_()                # columns 0 and W+1 of every row
+        self._zeroed = True
+
+    def release(self) -> None:
+        self._bufs = {}
+        self._prepared = False
+
     def _pad(self, slot: str, Fr: int, H: int, W: int, C: int, dev) -> torch.Tensor:
-        """Zero-bordered NHWC buffer [Fr, H+2, W+2, C] for `slot`, cached across frame chunks and calls:
-        the producing kernels overwrite the whole interior, so the border is zeroed once at allocation
-        instead of zero-filling every buffer of every chunk."""
+        """Zero-bordered NHWC buffer [Fr, H+2, W+2, C] for `slot`, reused across the frame chunks of a
+        call: the producing kernels overwrite the whole interior, so the border is zeroed once per
+        forward instead of zero-filling every buffer of every chunk."""
         key = (slot, H, W, C)
         buf = self._bufs.get(key)
         if buf is None or buf.shape[0] < Fr or buf.device != torch.device(dev):
+            if self._prepared:  # buffer_plan() is out of step with forward_chunk
+                raise RuntimeError(f"DPT buffer {key} x {Fr} views is not in the prepared plan")
             buf = torch.zeros(Fr, H + 2, W + 2, C, device=dev, dtype=torch.bfloat16)
             self._bufs[key] = buf
         return buf[:Fr]
@@ -279,6 +324,11 @@ class DPTHeadDevice:
         cfg = self.W.cfg
         layers = [kept[i] for i in cfg.kept_layers]
         S = layers[0].shape[0]
+        own = not self._prepared  # standalone call: buffers allocated lazily on this stream, dropped after
+        if self._prepared and not self._zeroed:
+            self._zero_borders()
         for s0 in range(0, S, chunk):
             s1 = min(S, s0 + chunk)
             self.forward_chunk([l[s0:s1] for l in layers], out_pred[s0:s1], out_conf[s0:s1])
+        if own:
+            self.release()

@@ -139,6 +139,12 @@ class VGGT:
         with phase("heads"):
             cur = torch.cuda.current_stream(dev)
             s_d, s_p = self._head_streams(dev)
+            # the DPT heads' zero-bordered buffers come from the main stream's pool (allocated here, before
+            # the side streams wait on it, and released after the main stream has waited for them), so the
+            # next forward's aggregator reuses that memory
+            F = min(Sl, cfg.head_chunk)
+            self.depth_head.prepare(F, dev)
+            self.point_head.prepare(F, dev)
             s_d.wait_stream(cur)
             s_p.wait_stream(cur)
             with torch.cuda.stream(s_d):
@@ -155,6 +161,8 @@ class VGGT:
             depth_conf.record_stream(s_d)
             pts.record_stream(s_p)
             pts_conf.record_stream(s_p)
+            self.depth_head.release()  # freed into the main stream's pool, ordered after s_d / s_p above
+            self.point_head.release()
         return {
             "pose_enc": pose_list[-1][None],
             "pose_enc_list": [p[None] for p in pose_list],
