@@ -227,6 +227,37 @@ def test_frame_chunking_is_exact():
         torch.testing.assert_close(a[k], b[k], rtol=1e-5, atol=1e-5)
 
 
+def test_forward_holds_no_head_buffers_and_repeats_bitwise():
+    """The DPT heads' zero-bordered buffers live for one forward only (allocated from the main stream's
+    pool, released after the head streams are joined): nothing stays allocated between forwards, and a
+    second forward — whose aggregator reuses that memory, borders re-zeroed — gives the same outputs.
+    A standalone head call (no prepare) still works and also keeps nothing."""
+    from paper_2509_25191_b200.vggt import VGGT
+    cfg = vggt_small()
+    sd = make_state_dict(cfg, 0)
+    images = synthetic_images(cfg, 5, 1).cuda()
+    m = VGGT(cfg, state_dict=sd)
+    a = m(images)
+    torch.cuda.synchronize()
+    assert not m.depth_head._bufs and not m.point_head._bufs
+    base = torch.cuda.memory_allocated()
+    b = m(images)
+    torch.cuda.synchronize()
+    for k in ("pose_enc", "depth", "depth_conf", "world_points", "world_points_conf"):
+        torch.testing.assert_close(a[k], b[k], rtol=1e-6, atol=1e-6, msg=k)
+    del b
+    torch.cuda.synchronize()
+    assert torch.cuda.memory_allocated() == base
+    kept, _ = m.aggregator(images)
+    kept = {i: t[0] for i, t in kept.items()}
+    S, H = images.shape[0], cfg.img_size
+    d, dc = torch.empty(S, H, H, 1, device="cuda"), torch.empty(S, H, H, device="cuda")
+    m.depth_head(kept, d, dc, 2)
+    torch.cuda.synchronize()
+    assert not m.depth_head._bufs
+    torch.testing.assert_close(d, a["depth"][0], rtol=1e-5, atol=1e-5)
+
+
 def test_prediction_set_export():
     from paper_2509_25191_b200.pose import to_prediction_set
     from paper_2509_25191_b200.vggt import VGGT
