@@ -135,6 +135,8 @@ class DPTHeadDevice:
         self._bufs: Dict[tuple, torch.Tensor] = {}  # zero-bordered activation buffers, see _pad / prepare
         self._prepared = False
         self._zeroed = False
+        self._dirty = False
+        self._under_tail: List[tuple] = []
         cfg = W.cfg
         dev = W.patch_w.device
         g = cfg.grid
@@ -189,24 +191,56 @@ class DPTHeadDevice:
         plan += [("oc1", 2 * sizes[0], 2 * sizes[0], Fh), ("u", img, img, Fh // 2)]
         return plan
 
+    # the last two buffers of a chunk: written after every other buffer of the chunk is dead, so they
+    # share memory with them (see prepare)
+    TAIL_SLOTS = ("oc1", "u")
+
     def prepare(self, frames: int, dev) -> None:
         """Allocate this forward's zero-bordered buffers for chunks of up to `frames` views from the
-        CURRENT stream's pool; their borders are zeroed by the head's first call on its own stream (the
-        producing kernels overwrite the whole interior). VGGT.forward calls this on the main stream before
-        the head streams wait on it and `release()`s after the main stream has waited for them, so the
-        memory returns to the main stream's pool and the next forward's aggregator reuses it; nothing is
-        held between forwards."""
-        self._bufs = {(slot, H, W, C): torch.empty(frames, H + 2, W + 2, C, device=dev, dtype=torch.bfloat16)
-                      for slot, H, W, C in self.buffer_plan()}
+        CURRENT stream's pool. VGGT.forward calls this on the main stream before the head streams wait on
+        it and `release()`s after the main stream has waited for them, so the memory returns to the main
+        stream's pool and the next forward's aggregator reuses it; nothing is held between forwards.
+
+        One arena per head: the body buffers (projections, layer_rn, the fusion blocks' residual units)
+        at consecutive offsets, and the two tail buffers (oc1: refinenet1's output on the 296 grid, u: the
+        518-grid input of the output head) at offset 0 over them — when the tail is written, every body
+        buffer of the chunk has been consumed, and oc1 is consumed before u is written. That halves the
+        heads' buffer memory (3.7 -> 1.9 GB per head at 16-view chunks, 1B shape). Borders: all are
+        zeroed by the head's first call on its own stream; a tail buffer's border is re-zeroed right
+        before its producer writes it, and the body buffers under the tail get theirs re-zeroed at the
+        start of the next chunk (the producing kernels overwrite every interior).
+        """
+        plan = self.buffer_plan()
+        align = 512  # bf16 elements (1 KB)
+        n_of = lambda H, W, C: -(-(frames * (H + 2) * (W + 2) * C) // align) * align
+        body = [p for p in plan if p[0] not in self.TAIL_SLOTS]
+        tail = [p for p in plan if p[0] in self.TAIL_SLOTS]
+        offs, off = {}, 0
+        for slot, H, W, C in body:
+            offs[(slot, H, W, C)] = off
+            off += n_of(H, W, C)
+        tail_n = max((n_of(H, W, C) for _, H, W, C in tail), default=0)
+        arena = torch.empty(max(off, tail_n), device=dev, dtype=torch.bfloat16)
+        self._bufs = {}
+        for slot, H, W, C in plan:
+            o = offs.get((slot, H, W, C), 0)
+            n = frames * (H + 2) * (W + 2) * C
+            self._bufs[(slot, H, W, C)] = arena[o:o + n].view(frames, H + 2, W + 2, C)
+        self._under_tail = [k for k, o in offs.items() if o < tail_n]
         self._prepared = True
         self._zeroed = False
+        self._dirty = False
+
+    @staticmethod
+    def _zero_border(b: torch.Tensor) -> None:
+        """Zero the border rows and columns of a [F, H+2, W+2, C] buffer: two strided fills."""
+        _, H2, W2, C = b.shape
+        b[:, 0::H2 - 1].zero_()                       # rows 0 and H+1
+        b.reshape(-1, W2, C)[:, 0::W2 - 1].zero_()    # columns 0 and W+1 of every row (a view: contiguous)
 
     def _zero_borders(self) -> None:
-        """Zero the border rows and columns of the prepared buffers on the current stream (the head's
-        own stream, which has waited for the main stream): two strided fills per buffer."""
-        for (_, H, W, C), b in self._bufs.items():
-            b[:, 0::H + 1].zero_()                                   # rows 0 and H+1
-            b.view(-1, W + 2, C)[:, 0::W + 1].zero_()                # columns 0 and W+1 of every row
+        for b in self._bufs.values():
+            self._zero_border(b)
         self._zeroed = True
 
     def release(self) -> None:
@@ -215,8 +249,9 @@ class DPTHeadDevice:
 
     def _pad(self, slot: str, Fr: int, H: int, W: int, C: int, dev) -> torch.Tensor:
         """Zero-bordered NHWC buffer [Fr, H+2, W+2, C] for `slot`, reused across the frame chunks of a
-        call: the producing kernels overwrite the whole interior, so the border is zeroed once per
-        forward instead of zero-filling every buffer of every chunk."""
+        call: the producing kernels overwrite the whole interior, so borders are zeroed once per forward
+        (and, for the buffers that share memory, as `prepare` describes) instead of zero-filling every
+        buffer of every chunk."""
         key = (slot, H, W, C)
         buf = self._bufs.get(key)
         if buf is None or buf.shape[0] < Fr or buf.device != torch.device(dev):
@@ -224,6 +259,9 @@ class DPTHeadDevice:
                 raise RuntimeError(f"DPT buffer {key} x {Fr} views is not in the prepared plan")
             buf = torch.zeros(Fr, H + 2, W + 2, C, device=dev, dtype=torch.bfloat16)
             self._bufs[key] = buf
+        if self._prepared and slot in self.TAIL_SLOTS:  # over body buffers: re-zero, mark them dirty
+            self._zero_border(buf[:Fr])
+            self._dirty = True
         return buf[:Fr]
 
     def _rcu(self, name, x_raw, x_relu, Fr, hs, res2=None, res2_pad=False, dense_out=False):
@@ -257,6 +295,10 @@ class DPTHeadDevice:
         bf = torch.bfloat16
         empty = lambda *sh: torch.empty(*sh, device=dev, dtype=bf)
         pad = lambda slot, h_, w_, c_: self._pad(slot, Fr, h_, w_, c_, dev)
+        if self._prepared and self._dirty:  # the previous chunk's tail buffers overwrote these borders
+            for k in self._under_tail:
+                self._zero_border(self._bufs[k][:Fr])
+            self._dirty = False
         sizes = [4 * g, 2 * g, g, (g + 1) // 2]
         feats = []
         for i, x in enumerate(layers):
