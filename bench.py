@@ -279,7 +279,10 @@ def main():
     ga = phases.get("attn_global")
     roofline = None
     if ga:
-        achieved = attn_flops / (ga["avg_ms"] / 1000.0) / 1e12
+        # per global layer: one launch on one GPU, the g ring steps with frame sharding, or (above
+        # cfg.q_chunk views) one launch per chunk of queries — all of a layer's time / layers
+        layer_ms = ga["total_ms"] / (args.steps * cfg.depth)
+        achieved = attn_flops / (layer_ms / 1000.0) / 1e12
         peak = peaks["bf16_tflops_sustained"]
         traffic = None
         tp = os.path.join(ROOT, "profiles", "fmha_traffic.json")
@@ -288,10 +291,10 @@ def main():
                 tj = json.load(f)
             if tj.get("views") == S:  # measured for this workload's launch only
                 traffic = tj.get("dram_bytes_per_launch")
-        roofline = {"bound": "tensor", "kernel": "vx fmha_kernel<64> global attention (max-free launch + exact-fixup check launch)",
+        roofline = {"bound": "tensor", "kernel": "vx fmha_kernel<64> global attention (max-free launch + exact-fixup check launch; per layer: one launch, or one per query chunk above cfg.q_chunk views)",
                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                     "peak_source": peaks["source"] + " bf16_tflops_sustained",
-                    "flops_per_launch": attn_flops, "avg_launch_ms": ga["avg_ms"], "traffic": traffic}
+                    "flops_per_launch": attn_flops, "avg_launch_ms": layer_ms, "traffic": traffic}
     total_flops = forward_flops(cfg, S, with_heads=not args.no_heads) / world
     model_tflops = total_flops / (ms_per_step / 1000.0) / 1e12
 

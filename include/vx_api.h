@@ -77,6 +77,10 @@ typedef struct vx_epilogue {
   float eps;                  /* q/k LayerNorm eps */
   float q_scale;              /* VX_EPI_QKV: q is multiplied by this before its bf16 store (0 = 1); the
                                  aggregator stores q * log2(e)/sqrt(head_dim) for VX_ATTN_Q_LOG2 */
+  int col_offset;             /* VX_EPI_QKV: the B rows are rows col_offset .. col_offset+N-1 of the
+                                 [3C, C] qkv weight (bias likewise sliced): output column c is q/k/v
+                                 column col_offset + c. 0 = the whole weight (N = 3C); C with N = 2C
+                                 writes K and V only, 0 with N = C q only (chunked-q global blocks) */
 } vx_epilogue;
 
 /* D[M,N] = A[M,K] (bf16, row stride lda) . B[N,K]^T (bf16, row stride ldb) with

@@ -16,7 +16,8 @@ HBM layout (T = S * tokens_per_frame rows, frame-major):
   x      fp32 [T, C]        residual stream
   xn     bf16 [T, C]        LayerNorm output (GEMM A operand)
   q,k,v  bf16 [H, T, d]     head-major: frame attention reads rows f*N..f*N+N-1
-                            of each head, global attention all T rows
+                            of each head, global attention all T rows (above cfg.q_chunk views
+                            q holds one chunk of frames: _attention_q_chunked)
   o      bf16 [T, C]        attention output (proj A operand); the same buffer as xn
   h      bf16 [chunk*N, 4C] MLP hidden (per frame chunk)
   kept   bf16 [S, N, 2C]    per kept layer: [frame_out | global_out]
@@ -106,10 +107,12 @@ class Workspace:
 
 
 def alloc_workspace(cfg: VGGTConfig, S: int, device="cuda", rows_per_head: Optional[int] = None,
-                    kv: Optional[tuple] = None, q_log2: bool = True) -> Workspace:
+                    kv: Optional[tuple] = None, q_log2: bool = True, q_frames: Optional[int] = None) -> Workspace:
     """Per-forward buffers for S views.  `rows_per_head` (>= S * tokens_per_frame) is the per-head row
     stride of q/k/v; `kv` = (k, v) [H, rows_per_head, d] supplied by the frame-sharded ring (its send
-    buffer: the QKV epilogue then writes the local K/V where the first ring step sends them from)."""
+    buffer: the QKV epilogue then writes the local K/V where the first ring step sends them from).
+    `q_frames` < S: q holds that many frames only, and run_block produces and consumes it chunk by chunk
+    (peak HBM: T x C bf16 less the chunk)."""
     T = S * cfg.tokens_per_frame
     R = rows_per_head or T
     if R < T:
@@ -127,7 +130,8 @@ def alloc_workspace(cfg: VGGTConfig, S: int, device="cuda", rows_per_head: Optio
     return Workspace(
         x=torch.empty(T, C, device=device, dtype=torch.float32),
         xn=xn,
-        q=torch.empty(H, R, d, device=device, dtype=torch.bfloat16),
+        q=torch.empty(H, (q_frames * cfg.tokens_per_frame if q_frames and q_frames < S else R), d, device=device,
+                      dtype=torch.bfloat16),
         k=kv[0],
         v=kv[1],
         o=xn,
@@ -153,25 +157,29 @@ def run_block(W: DeviceWeights, name: str, ws: Workspace, S: int, frame_attn: bo
     eps = cfg.ln_eps if eps is None else eps
     with phase("layernorm"):
         ops.layernorm(ws.x, W[name + ".norm1.weight"], W[name + ".norm1.bias"], eps, out=ws.xn)
-    with phase("gemm_qkv"):
-        extra = {}
-        if vggt_attn:
-            extra = dict(qk_norm=(W[name + ".attn.q_norm.weight"], W[name + ".attn.q_norm.bias"],
-                                  W[name + ".attn.k_norm.weight"], W[name + ".attn.k_norm.bias"]),
-                         rope=W.rope, tokens_per_frame=N, patch_start=cfg.patch_start_idx, grid_w=cfg.grid,
-                         eps=cfg.ln_eps)
-        ops.gemm(ws.xn, W[name + ".attn.qkv.weight"], ops.EPI_QKV, bias=W[name + ".attn.qkv.bias"],
-                 qkv=(ws.q, ws.k, ws.v), head_dim=cfg.head_dim, tokens_total=ws.q.shape[1],
-                 q_scale=ops.Q_LOG2_SCALE(cfg.head_dim) if ws.q_log2 else 0.0, **extra)
-    if frame_attn:
-        with phase("attn_frame"):
-            ops.attention(ws.q, ws.k, ws.v, ws.o, nseq=S, Lq=N, Lk=N, q_log2=ws.q_log2)
-    elif global_attn is not None:
-        with phase("attn_global"):
-            global_attn(ws.q, ws.k, ws.v, ws.o)
+    extra = {}
+    if vggt_attn:
+        extra = dict(qk_norm=(W[name + ".attn.q_norm.weight"], W[name + ".attn.q_norm.bias"],
+                              W[name + ".attn.k_norm.weight"], W[name + ".attn.k_norm.bias"]),
+                     rope=W.rope, tokens_per_frame=N, patch_start=cfg.patch_start_idx, grid_w=cfg.grid,
+                     eps=cfg.ln_eps)
+    qs = ops.Q_LOG2_SCALE(cfg.head_dim) if ws.q_log2 else 0.0
+    Rq = ws.q.shape[1]
+    if Rq < T:  # chunked q (alloc_workspace q_frames): frame-aligned chunks of Rq rows
+        _attention_q_chunked(W, name, ws, S, frame_attn, global_attn, extra, qs)
     else:
-        with phase("attn_global"):
-            ops.attention(ws.q, ws.k, ws.v, ws.o, nseq=1, Lq=T, Lk=T, q_log2=ws.q_log2)
+        with phase("gemm_qkv"):
+            ops.gemm(ws.xn, W[name + ".attn.qkv.weight"], ops.EPI_QKV, bias=W[name + ".attn.qkv.bias"],
+                     qkv=(ws.q, ws.k, ws.v), head_dim=cfg.head_dim, tokens_total=Rq, q_scale=qs, **extra)
+        if frame_attn:
+            with phase("attn_frame"):
+                ops.attention(ws.q, ws.k, ws.v, ws.o, nseq=S, Lq=N, Lk=N, q_log2=ws.q_log2)
+        elif global_attn is not None:
+            with phase("attn_global"):
+                global_attn(ws.q, ws.k, ws.v, ws.o)
+        else:
+            with phase("attn_global"):
+                ops.attention(ws.q, ws.k, ws.v, ws.o, nseq=1, Lq=T, Lk=T, q_log2=ws.q_log2)
     with phase("gemm_proj"):
         ops.gemm(ws.o, W[name + ".attn.proj.weight"], ops.EPI_RESID, bias=W[name + ".attn.proj.bias"],
                  resid=ws.x, gamma=W[name + ".ls1.gamma"])
@@ -188,6 +196,48 @@ def run_block(W: DeviceWeights, name: str, ws: Workspace, S: int, frame_attn: bo
             ops.gemm(hb, W[name + ".mlp.fc2.weight"], ops.EPI_RESID, bias=W[name + ".mlp.fc2.bias"],
                      resid=ws.x[r0:r1], gamma=W[name + ".ls2.gamma"],
                      kept=None if kept_half is None else kept_half[r0:r1])
+
+
+def _attention_q_chunked(W: DeviceWeights, name: str, ws: Workspace, S: int, frame_attn: bool,
+                         global_attn: Optional[GlobalAttnFn], extra: dict, qs: float):
+    """qkv GEMM + attention with q held one chunk of frames at a time (ws.q has Rq = chunk rows per head).
+
+    Frame blocks: per chunk, q/k/v of the chunk (k/v in the first H x Rq x d elements of the k/v buffers,
+    idle in a frame block) and the chunk's frame attention. Global blocks: K and V of all tokens first
+    (the qkv weight's rows C..3C, `col_offset` C), then per chunk its q (rows 0..C) and the attention of
+    its queries against all keys. xn and o share a buffer: a chunk's xn rows are read (by its q GEMM)
+    before its attention writes the same rows of o, and other chunks' rows are untouched."""
+    cfg = W.cfg
+    N = cfg.tokens_per_frame
+    T = S * N
+    C, H, d = cfg.embed_dim, cfg.num_heads, cfg.head_dim
+    Rq = ws.q.shape[1]
+    cf = Rq // N  # frames per chunk
+    w = W[name + ".attn.qkv.weight"]
+    b = W[name + ".attn.qkv.bias"]
+    if global_attn is not None:
+        raise ValueError("chunked q runs on one GPU only (the ring attends with the whole local q)")
+    if frame_attn:
+        kc = ws.k.view(-1)[: H * Rq * d].view(H, Rq, d)
+        vc = ws.v.view(-1)[: H * Rq * d].view(H, Rq, d)
+        for f0 in range(0, S, cf):
+            r0, r1 = f0 * N, min(S, f0 + cf) * N
+            with phase("gemm_qkv"):
+                ops.gemm(ws.xn[r0:r1], w, ops.EPI_QKV, bias=b, qkv=(ws.q, kc, vc), head_dim=d, tokens_total=Rq,
+                         q_scale=qs, **extra)
+            with phase("attn_frame"):
+                ops.attention(ws.q, kc, vc, ws.o[r0:r1], nseq=(r1 - r0) // N, Lq=N, Lk=N, q_log2=ws.q_log2)
+        return
+    with phase("gemm_qkv"):
+        ops.gemm(ws.xn, w[C:], ops.EPI_QKV, bias=b[C:], qkv=(ws.q, ws.k, ws.v), head_dim=d,
+                 tokens_total=ws.k.shape[1], q_scale=qs, embed_dim=C, col_offset=C, **extra)
+    for f0 in range(0, S, cf):
+        r0, r1 = f0 * N, min(S, f0 + cf) * N
+        with phase("gemm_qkv"):
+            ops.gemm(ws.xn[r0:r1], w[:C], ops.EPI_QKV, bias=b[:C], qkv=(ws.q, ws.k, ws.v), head_dim=d,
+                     tokens_total=Rq, q_scale=qs, embed_dim=C, col_offset=0, **extra)
+        with phase("attn_global"):
+            ops.attention(ws.q, ws.k, ws.v, ws.o[r0:r1], nseq=1, Lq=r1 - r0, Lk=T, q_log2=ws.q_log2)
 
 
 def embed(W: DeviceWeights, images: torch.Tensor, ws: Workspace, frame0_is_first: bool = True):

@@ -46,6 +46,8 @@ class VGGTConfig:
     # memory discipline (VGGT-X "VGGT--")
     frame_chunk: int = 128             # frames per chunk for frame-wise MLP work
     head_chunk: int = 16               # frames per DPT-head chunk (16: -9% head time vs 8 for +4 GB, tools/exp_dpt_chunk.py)
+    q_chunk: int = 256                 # above this many views (one GPU), q is produced and consumed this many frames
+                                       # at a time: K/V for all tokens, then per chunk q + attention (0 = never)
 
     def __post_init__(self):
         # native DPT convs use 64-channel K blocks and 32-channel output chunks

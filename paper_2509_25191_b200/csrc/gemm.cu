@@ -145,8 +145,9 @@ template <int D>
 VX_DEVICE void epi_qkv_head(const GemmArgs& a, int row, int col, float* v) {
   const vx_epilogue& e = a.ep;
   const int C = e.embed_dim;
-  const int which = col / C;
-  const int h = (col - which * C) / D;
+  const int gcol = col + e.col_offset;  // column of the whole [3C] q/k/v output (bias is sliced alike)
+  const int which = gcol / C;
+  const int h = (gcol - which * C) / D;
   if (e.bias) {
     const float4* b4 = reinterpret_cast<const float4*>(e.bias + col);
 #pragma unroll
@@ -234,8 +235,9 @@ VX_DEVICE void epi_qkv_scatter32(const GemmArgs& a, int row, int col, const uint
   const vx_epilogue& e = a.ep;
   if (row >= a.M) return;
   const int C = e.embed_dim;
-  const int which = col / C;
-  const int hc = col - which * C;
+  const int gcol = col + e.col_offset;
+  const int which = gcol / C;
+  const int hc = gcol - which * C;
   const int h = hc / e.head_dim, off = hc - h * e.head_dim;
   __nv_bfloat16* base = reinterpret_cast<__nv_bfloat16*>(which == 0 ? e.q : (which == 1 ? e.k : e.v));
   const float qs = which == 0 && e.q_scale != 0.f ? e.q_scale : 1.0f;
@@ -866,8 +868,10 @@ extern "C" int vx_gemm(int epi, const void* A, int64_t lda, const void* B, int64
   if (epi == VX_EPI_RESID) VX_CHECK_ARG(ep->resid && ep->gamma, "vx_gemm: resid epilogue needs resid+gamma");
   if (epi == VX_EPI_QKV) {
     VX_CHECK_ARG(ep->q && ep->k && ep->v, "vx_gemm: qkv epilogue needs q/k/v");
-    VX_CHECK_ARG(ep->head_dim > 0 && N == 3 * ep->embed_dim && ep->embed_dim % ep->head_dim == 0,
-                 "vx_gemm: qkv N != 3C");
+    VX_CHECK_ARG(ep->head_dim > 0 && ep->embed_dim % ep->head_dim == 0 && ep->col_offset >= 0 &&
+                     ep->col_offset % ep->head_dim == 0 && N % ep->head_dim == 0 && ep->col_offset + N <= 3 * ep->embed_dim,
+                 "vx_gemm: qkv columns [col_offset, col_offset + N) = [%d, %d) not head-aligned within 3C = %d",
+                 ep->col_offset, ep->col_offset + N, 3 * ep->embed_dim);
     VX_CHECK_ARG(ep->head_dim % 32 == 0 || ep->qn_w || ep->rope_cos, "vx_gemm: qkv scatter needs head_dim %% 32 == 0");
     VX_CHECK_ARG(ep->tokens_total >= M, "vx_gemm: tokens_total < M");
   }

@@ -35,7 +35,7 @@ class Epilogue(ctypes.Structure):
         ("rope_cos", _vp), ("rope_sin", _vp),
         ("embed_dim", _i32), ("head_dim", _i32), ("tokens_total", _i32),
         ("tokens_per_frame", _i32), ("patch_start", _i32), ("grid_w", _i32),
-        ("eps", _f32), ("q_scale", _f32),
+        ("eps", _f32), ("q_scale", _f32), ("col_offset", _i32),
     ]
 
 
@@ -174,9 +174,10 @@ def _rowmajor(t, name):
 # ---------------------------------------------------------------------------
 def gemm(a: torch.Tensor, w: torch.Tensor, epi: int = EPI_BF16, bias=None, out=None, resid=None,
          gamma=None, kept=None, qkv=None, qk_norm=None, rope=None, head_dim=0, tokens_total=0,
-         tokens_per_frame=1, patch_start=0, grid_w=1, eps=1e-5, q_scale=0.0):
+         tokens_per_frame=1, patch_start=0, grid_w=1, eps=1e-5, q_scale=0.0, embed_dim=0, col_offset=0):
     """D = a @ w.T with the given fused epilogue (see include/vx_api.h). EPI_QKV: q_scale != 0
-    multiplies q before its bf16 store (Q_LOG2_SCALE(d) for attention(..., q_log2=True))."""
+    multiplies q before its bf16 store (Q_LOG2_SCALE(d) for attention(..., q_log2=True)); w (and bias)
+    may be the row slice [col_offset, col_offset + N) of the [3C, C] qkv weight, with embed_dim = C."""
     load_library()
     _req(a, torch.bfloat16, "a")
     _req(w, torch.bfloat16, "w")
@@ -220,7 +221,8 @@ def gemm(a: torch.Tensor, w: torch.Tensor, epi: int = EPI_BF16, bias=None, out=N
             ep.qn_w, ep.qn_b, ep.kn_w, ep.kn_b = (t.data_ptr() for t in (qw, qb, kw, kb))
         if rope is not None:
             ep.rope_cos, ep.rope_sin = rope[0].data_ptr(), rope[1].data_ptr()
-        ep.embed_dim = N // 3
+        ep.embed_dim = embed_dim or N // 3
+        ep.col_offset = col_offset
         ep.head_dim = head_dim
         ep.tokens_total = tokens_total
         ep.q_scale = q_scale

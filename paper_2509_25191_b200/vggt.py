@@ -98,7 +98,8 @@ class VGGT:
 
     def _aggregate(self, local: torch.Tensor, f0: int) -> Dict[int, torch.Tensor]:
         if self.ring is None:
-            ws = alloc_workspace(self.cfg, local.shape[0], self.device)
+            S, qc = local.shape[0], self.cfg.q_chunk
+            ws = alloc_workspace(self.cfg, S, self.device, q_frames=qc if qc and S > qc else None)
             gattn = None
         else:  # K/V produced straight into the ring's send buffer, ring buffers allocated once per forward
             self.ring.begin()

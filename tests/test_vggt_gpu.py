@@ -227,6 +227,28 @@ def test_frame_chunking_is_exact():
         torch.testing.assert_close(a[k], b[k], rtol=1e-5, atol=1e-5)
 
 
+@pytest.mark.parametrize("patch_embed", ["conv", "dinov2"])
+def test_q_chunking_matches_whole_q(patch_embed):
+    """cfg.q_chunk (one GPU, many views): q produced and attended a chunk of frames at a time — frame blocks
+    per chunk, global blocks as K/V of all tokens (qkv weight rows C..3C through the GEMM's col_offset) then
+    per chunk q (rows 0..C) + attention against all keys — equals the whole-q forward (7 views in chunks of
+    2, 2, 2, 1; the DINOv2 encoder's frame blocks too)."""
+    from paper_2509_25191_b200.vggt import VGGT
+    cfg = vggt_small().with_(init_values=0.5, patch_embed=patch_embed,
+                             **({"dino_depth": 3} if patch_embed == "dinov2" else {}))
+    sd = make_state_dict(cfg, 0)
+    images = synthetic_images(cfg, 7, 1).cuda()
+    ma = VGGT(cfg.with_(q_chunk=0), state_dict=sd)
+    mb = VGGT(cfg.with_(q_chunk=2), state_dict=sd)
+    ka, _ = ma.aggregator(images)
+    kb, _ = mb.aggregator(images)
+    for i in cfg.kept_layers:
+        assert rel(kb[i], ka[i]) < 2e-3, (i, rel(kb[i], ka[i]))
+    a, b = ma(images), mb(images)
+    for k in ("pose_enc", "depth", "depth_conf", "world_points", "world_points_conf"):
+        assert rel(b[k], a[k]) < 2e-3, (k, rel(b[k], a[k]))
+
+
 def test_forward_holds_no_head_buffers_and_repeats_bitwise():
     """The DPT heads' zero-bordered buffers live for one forward only (allocated from the main stream's
     pool, released after the head streams are joined): nothing stays allocated between forwards, and a
