@@ -136,7 +136,8 @@ class DPTHeadDevice:
         self._prepared = False
         self._zeroed = False
         self._dirty = False
-        self._under_tail: List[tuple] = []
+        self._overlay: set = set()
+        self._under_overlay: List[tuple] = []
         cfg = W.cfg
         dev = W.patch_w.device
         g = cfg.grid
@@ -191,9 +192,15 @@ class DPTHeadDevice:
         plan += [("oc1", 2 * sizes[0], 2 * sizes[0], Fh), ("u", img, img, Fh // 2)]
         return plan
 
-    # the last two buffers of a chunk: written after every other buffer of the chunk is dead, so they
-    # share memory with them (see prepare)
+    # buffers laid over others (see prepare): refinenet1's residual units run when every buffer of the
+    # projections, layer_rn (but layer 1's) and refinenets 2-4 is dead; the last two buffers of a chunk
+    # (oc1: refinenet1's output on the 296 grid, u: the output head's 518-grid input) when all are
     TAIL_SLOTS = ("oc1", "u")
+
+    def _overlay_groups(self):
+        sc = self.head + "scratch."
+        rn1 = tuple(f"{sc}refinenet1.resConfUnit1.{n}" for n in ("h", "o", "o2")) + (f"{sc}refinenet1.resConfUnit2.h",)
+        return rn1, self.TAIL_SLOTS
 
     def prepare(self, frames: int, dev) -> None:
         """Allocate this forward's zero-bordered buffers for chunks of up to `frames` views from the
@@ -201,32 +208,46 @@ class DPTHeadDevice:
         it and `release()`s after the main stream has waited for them, so the memory returns to the main
         stream's pool and the next forward's aggregator reuses it; nothing is held between forwards.
 
-        One arena per head: the body buffers (projections, layer_rn, the fusion blocks' residual units)
-        at consecutive offsets, and the two tail buffers (oc1: refinenet1's output on the 296 grid, u: the
-        518-grid input of the output head) at offset 0 over them — when the tail is written, every body
-        buffer of the chunk has been consumed, and oc1 is consumed before u is written. That halves the
-        heads' buffer memory (3.7 -> 1.9 GB per head at 16-view chunks, 1B shape). Borders: all are
-        zeroed by the head's first call on its own stream; a tail buffer's border is re-zeroed right
-        before its producer writes it, and the body buffers under the tail get theirs re-zeroed at the
-        start of the next chunk (the producing kernels overwrite every interior).
+        One arena per head, laid out by liveness within a chunk: region 1 holds layer_rn 1's outputs (l0,
+        lr0: read by refinenet1, the last fusion block), region 2 every other body buffer (projections,
+        layer_rn 2-4, refinenets 2-4), refinenet1's residual-unit buffers sit over region 2 (all dead when
+        refinenet1 runs), and the two tail buffers over everything from offset 0 (oc1 is consumed before
+        u is written). 1B shape, 16-view chunks: 1.1 GB per head instead of 3.7 for separate buffers.
+        Borders: all are zeroed by the head's first call on its own stream; an overlaid buffer's border
+        is re-zeroed right before its producer writes it, and the buffers under an overlay get theirs
+        re-zeroed at the start of the next chunk (the producing kernels overwrite every interior).
         """
         plan = self.buffer_plan()
         align = 512  # bf16 elements (1 KB)
-        n_of = lambda H, W, C: -(-(frames * (H + 2) * (W + 2) * C) // align) * align
-        body = [p for p in plan if p[0] not in self.TAIL_SLOTS]
-        tail = [p for p in plan if p[0] in self.TAIL_SLOTS]
+        n_of = lambda H, W, C: -(-(frames * (H + 2) * (W + 2) * C) // align) * align  # noqa: E731
+        rn1, tail = self._overlay_groups()
+        region1 = [p for p in plan if p[0] in ("l0", "lr0")]
+        region2 = [p for p in plan if p[0] not in ("l0", "lr0") + rn1 + tail]
         offs, off = {}, 0
-        for slot, H, W, C in body:
-            offs[(slot, H, W, C)] = off
-            off += n_of(H, W, C)
-        tail_n = max((n_of(H, W, C) for _, H, W, C in tail), default=0)
-        arena = torch.empty(max(off, tail_n), device=dev, dtype=torch.bfloat16)
+        for p in region1:
+            offs[p] = off
+            off += n_of(*p[1:])
+        base2 = off
+        for p in region2:
+            offs[p] = off
+            off += n_of(*p[1:])
+        o1 = base2
+        for p in (p for p in plan if p[0] in rn1):
+            offs[p] = o1
+            o1 += n_of(*p[1:])
+        for p in (p for p in plan if p[0] in tail):
+            offs[p] = 0
+        size = max([off, o1] + [offs[p] + n_of(*p[1:]) for p in plan])
+        arena = torch.empty(size, device=dev, dtype=torch.bfloat16)
         self._bufs = {}
-        for slot, H, W, C in plan:
-            o = offs.get((slot, H, W, C), 0)
+        for p in plan:
+            slot, H, W, C = p
             n = frames * (H + 2) * (W + 2) * C
-            self._bufs[(slot, H, W, C)] = arena[o:o + n].view(frames, H + 2, W + 2, C)
-        self._under_tail = [k for k, o in offs.items() if o < tail_n]
+            self._bufs[p] = arena[offs[p]:offs[p] + n].view(frames, H + 2, W + 2, C)
+        over = [(offs[p], offs[p] + n_of(*p[1:])) for p in plan if p[0] in rn1 + tail]
+        self._overlay = set(rn1 + tail)
+        self._under_overlay = [p for p in plan if p[0] not in self._overlay and
+                               any(offs[p] < e and b < offs[p] + n_of(*p[1:]) for b, e in over)]
         self._prepared = True
         self._zeroed = False
         self._dirty = False
@@ -259,7 +280,7 @@ class DPTHeadDevice:
                 raise RuntimeError(f"DPT buffer {key} x {Fr} views is not in the prepared plan")
             buf = torch.zeros(Fr, H + 2, W + 2, C, device=dev, dtype=torch.bfloat16)
             self._bufs[key] = buf
-        if self._prepared and slot in self.TAIL_SLOTS:  # over body buffers: re-zero, mark them dirty
+        if self._prepared and slot in self._overlay:  # over other buffers: re-zero, mark those dirty
             self._zero_border(buf[:Fr])
             self._dirty = True
         return buf[:Fr]
@@ -295,8 +316,8 @@ class DPTHeadDevice:
         bf = torch.bfloat16
         empty = lambda *sh: torch.empty(*sh, device=dev, dtype=bf)
         pad = lambda slot, h_, w_, c_: self._pad(slot, Fr, h_, w_, c_, dev)
-        if self._prepared and self._dirty:  # the previous chunk's tail buffers overwrote these borders
-            for k in self._under_tail:
+        if self._prepared and self._dirty:  # the previous chunk's overlaid buffers overwrote these borders
+            for k in self._under_overlay:
                 self._zero_border(self._bufs[k][:Fr])
             self._dirty = False
         sizes = [4 * g, 2 * g, g, (g + 1) // 2]
