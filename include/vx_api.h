@@ -319,6 +319,8 @@ int vx_num_sms(void);
 /* Kernels this library has launched in this process (a CUDA-graph replay counts its kernel nodes). */
 uint64_t vx_launch_count(void);
 const char* vx_last_error(void);
+/* "vx <abi> sm_100a"; abi 0.2 added vx_epilogue.col_offset (a caller built against 0.1 passes a shorter
+ * struct: rebuild against this header) */
 const char* vx_version(void);
 
 #ifdef __cplusplus

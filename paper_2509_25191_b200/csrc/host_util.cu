@@ -88,7 +88,7 @@ bool make_tmap_2d(CUtensorMap* m, const void* ptr, bool f32, uint64_t rows, uint
 extern "C" {
 const char* vx_last_error(void) { return vx::g_err; }
 int vx_num_sms(void) { return vx::num_sms(); }
-const char* vx_version(void) { return "vx 0.1 sm_100a"; }
+const char* vx_version(void) { return "vx 0.2 sm_100a"; }  // 0.2: vx_epilogue.col_offset
 }
 
 extern "C" uint64_t vx_launch_count(void) { return vx::g_launches.load(std::memory_order_relaxed); }
