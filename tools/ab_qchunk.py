@@ -1,7 +1,8 @@
-"""In-process A/B of cfg.q_chunk on the 1B-shaped forward (one GPU): whole q against q produced and attended a
-chunk of frames at a time, alternating so clock and power drift hit every variant alike.
+"""In-process A/B of cfg.q_chunk (or another chunk field, --field frame_chunk) on the 1B-shaped forward (one
+GPU): whole q against q produced and attended a chunk of frames at a time, alternating so clock and power
+drift hit every variant alike.
 
-    python tools/ab_qchunk.py [--views 200] [--chunks 0 100 128] [--rounds 3]
+    python tools/ab_qchunk.py [--views 200] [--chunks 0 100 128] [--rounds 3] [--field q_chunk]
 Prints per-variant median ms per forward, the global-attention phase and peak HBM, one JSON line.
 """
 import argparse
@@ -19,6 +20,7 @@ def main():
     ap.add_argument("--views", type=int, default=200)
     ap.add_argument("--chunks", type=int, nargs="+", default=[0, 100, 128])
     ap.add_argument("--rounds", type=int, default=3)
+    ap.add_argument("--field", default="q_chunk")
     args = ap.parse_args()
     from paper_2509_25191_b200 import profiling
     from paper_2509_25191_b200.config import vggt_1b
@@ -27,7 +29,7 @@ def main():
     cfg = vggt_1b()
     sd = make_state_dict(cfg, 0)
     images = synthetic_images(cfg, args.views, 1).cuda()
-    models = {c: VGGT(cfg.with_(q_chunk=c), state_dict=sd) for c in args.chunks}
+    models = {c: VGGT(cfg.with_(**{args.field: c}), state_dict=sd) for c in args.chunks}
     for m in models.values():
         m(images)
     res = {c: {"ms": [], "attn_global_ms": [], "peak_gb": []} for c in args.chunks}
@@ -49,7 +51,7 @@ def main():
             res[c]["peak_gb"].append(torch.cuda.max_memory_allocated() / 1e9)
     med = lambda v: sorted(v)[len(v) // 2]  # noqa: E731
     out = {str(c): {k: round(med(v), 2) for k, v in r.items()} for c, r in res.items()}
-    print(json.dumps({"views": args.views, **out}))
+    print(json.dumps({"views": args.views, "field": args.field, **out}))
 
 
 if __name__ == "__main__":
